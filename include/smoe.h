@@ -1,0 +1,286 @@
+/*
+ * smoe.h — C-ABI of the B200-native speculative-token-shuffling MoE layer.
+ *
+ * This is the drop-in boundary for the online hot path of Speculative MoE
+ * (arXiv 2503.04398).  The reference (`/root/reference/pkg/src/moesched`) is a
+ * pure-Python package; its "FFI" is the Python module API.  Each entry point
+ * below names the reference function it replaces (file:line under
+ * /root/reference/pkg/src/moesched/).  The Python mirror that a user of the
+ * reference imports is `paper_2503_04398_b200` (ctypes over this library);
+ * INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer unless the parameter name ends in _h;
+ *   - `stream` is a cudaStream_t passed as void*; every call is stream-ordered
+ *     and asynchronous (no host synchronisation inside the library);
+ *   - `err` (nullable) is a device int32 flag; kernels OR in SMOE_ERRBIT_*
+ *     bits for data-dependent failures the reference raises on (the Python
+ *     mirror reads it and raises the reference's exception class);
+ *   - the return value reports argument/launch errors immediately.
+ *   - no CPU fallback: if the device is not an sm_100 part the calls return
+ *     SMOE_ERR_CUDA.
+ */
+#ifndef SMOE_H_
+#define SMOE_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (return values) ------------------------------------- */
+#define SMOE_OK                 0
+#define SMOE_ERR_INVALID_ARG    1   /* bad size / null pointer               */
+#define SMOE_ERR_LENGTH         2   /* scheduler.py:129-130, :155-156        */
+#define SMOE_ERR_UNSUPPORTED    3   /* shape outside the kernels' envelope    */
+#define SMOE_ERR_CUDA           4   /* launch / runtime failure               */
+#define SMOE_ERR_CLUSTERS       5   /* scheduler.py:37-38                     */
+#define SMOE_ERR_GATE_WIDTH     6   /* scheduler.py:217-218                   */
+
+/* ---- data-dependent error bits written to *err ------------------------- */
+#define SMOE_ERRBIT_DEVICE_RANGE   1  /* scheduler.py:131-132 SchedulerError */
+#define SMOE_ERRBIT_EXPERT_LABEL   2  /* scheduler.py:204-206 SchedulerError */
+#define SMOE_ERRBIT_TOKEN_RANGE    4  /* numpy IndexError on labels[tokens]  */
+#define SMOE_ERRBIT_HISTORY_RANGE  8  /* numpy IndexError on confidence[rows]*/
+#define SMOE_ERRBIT_INDEX_RANGE   16  /* numpy IndexError on a fancy index   */
+#define SMOE_ERRBIT_CAPACITY      32  /* a layer buffer would overflow        */
+
+#define SMOE_MAX_SHARDS 16          /* EP degree G supported by the layer    */
+#define SMOE_MAX_PLAN_DEVICES 1024  /* n_devices supported by rebatch plan   */
+
+const char* smoe_version(void);
+const char* smoe_status_string(int status);
+/* 1 when the current device is sm_100 (B200) and the kernels can run. */
+int smoe_device_ok(void);
+
+/* ======================================================================= *
+ *  Scheduler (reference: scheduler.py)                                     *
+ * ======================================================================= */
+
+/* lookup_devices (scheduler.py:82-98).
+ *   dev[i] = a_best[row_i] if hist && a_conf[row_i] > t_conf[tok_i] (strict,
+ *   float32) else t_labels[tok_i];  row_i = base-E code of hist[i, :]
+ *   (oldest digit most significant, predictor.py:149-154).
+ * tokens int64[n]; hist int64[n, hist_len] row-major or NULL; negative ids
+ * wrap like numpy (id + vocab); a_best/a_conf have n_clusters^hist_len rows
+ * (the reference's DeviceNGramTable.best / .confidence, predictor.py:72-78)
+ * and a_rows = n_clusters^ngram_n rows.  Like the vectorised reference, the
+ * history width is not checked against the table depth: a row code outside
+ * [-a_rows, a_rows) sets SMOE_ERRBIT_HISTORY_RANGE (numpy IndexError).
+ * Out-of-range token ids set SMOE_ERRBIT_TOKEN_RANGE. */
+int smoe_lookup_devices(const int64_t* tokens, int64_t n,
+                        const int64_t* hist, int32_t hist_len,
+                        const int16_t* t_labels, const float* t_conf, int64_t vocab,
+                        const int16_t* a_best, const float* a_conf,
+                        int64_t a_rows, int32_t n_clusters,
+                        int64_t* dev_out, int32_t* err, void* stream);
+
+/* Workspace bytes needed by smoe_rebatch_plan / smoe_lookup_plan. */
+size_t smoe_plan_workspace_bytes(int64_t n, int32_t n_devices);
+
+/* rebatch_tokens index half (scheduler.py:119-149): stable device partition
+ * padded to the largest group.
+ *   group = max_d #{i : dev[i] = d}                (scheduler.py:134-135)
+ *   inverse[i] = dev[i]*group + #{j < i : dev[j] = dev[i]}
+ *   forward[inverse[i]] = i, every other slot of [0, G*group) = -1
+ * devices int64[n]; forward must hold n_devices*n entries (only the first
+ * n_devices*group are written); counts int32[n_devices]; group int64[1].
+ * Labels outside [0, n_devices) set SMOE_ERRBIT_DEVICE_RANGE. */
+int smoe_rebatch_plan(const int64_t* devices, int64_t n, int32_t n_devices,
+                      int64_t* forward, int64_t* inverse, int32_t* counts,
+                      int64_t* group, int32_t* err,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* lookup_devices fused with the rebatch plan (K1 of DESIGN.md): the device
+ * labels never round-trip through HBM as int64 unless dev_out != NULL. */
+int smoe_lookup_plan(const int64_t* tokens, int64_t n,
+                     const int64_t* hist, int32_t hist_len,
+                     const int16_t* t_labels, const float* t_conf, int64_t vocab,
+                     const int16_t* a_best, const float* a_conf,
+                     int64_t a_rows, int32_t n_clusters,
+                     int64_t* dev_out, int64_t* forward, int64_t* inverse,
+                     int32_t* counts, int64_t* group, int32_t* err,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* Row gather, the data half of rebatch_tokens / resume_tokens
+ * (scheduler.py:145-146, :157):  dst[i, :] = src[idx[i], :], or pad_value in
+ * every element when idx[i] < 0 and pad_negative != 0.  With pad_negative == 0
+ * negative indices wrap like numpy.  elem_bytes in {1,2,4,8}; rows are
+ * row_elems elements.  idx out of range sets SMOE_ERRBIT_INDEX_RANGE. */
+int smoe_gather_rows(const void* src, int64_t n_src, int32_t elem_bytes,
+                     int64_t row_elems, const int64_t* idx, int64_t n_out,
+                     int32_t pad_negative, int64_t pad_value, void* dst,
+                     int32_t* err, void* stream);
+
+/* gate_permutation (scheduler.py:200-210): new_to_old = stable argsort of
+ * the expert cluster labels, old_to_new its inverse.  labels int64[N]. */
+int smoe_gate_permutation(const int64_t* labels, int32_t n_experts,
+                          int32_t n_clusters, int64_t* new_to_old,
+                          int64_t* old_to_new, int32_t* err, void* stream);
+
+/* apply_expert_shuffle (scheduler.py:213-219): dst[r, i] = src[r, perm[i]]
+ * over `rows` rows of `width` elements (elem_bytes in {1,2,4,8}). */
+int smoe_permute_columns(const void* src, int64_t rows, int32_t width,
+                         int32_t elem_bytes, const int64_t* perm, void* dst,
+                         void* stream);
+
+/* remap_topk (scheduler.py:222-224): dst[i] = table[idx[i]] (numpy wrap for
+ * negative idx; out of range sets SMOE_ERRBIT_INDEX_RANGE). */
+int smoe_remap_index(const int64_t* idx, int64_t count, const int64_t* table,
+                     int64_t table_len, int64_t* dst, int32_t* err,
+                     void* stream);
+
+/* Event counting of simulate_layer (comm.py:214):
+ *   local = sum_{i<occ, s<k} [expert_dev[experts[i, s]] == token_dev[i]]
+ * experts int64[occ, k]; local_out int64[1] (overwritten). */
+int smoe_count_local(const int64_t* experts, int64_t occ, int32_t k,
+                     const int64_t* expert_dev, int32_t n_experts,
+                     const int64_t* token_dev, int64_t* local_out,
+                     int32_t* err, void* stream);
+
+/* ======================================================================= *
+ *  MoE layer (Algorithm 2; no reference code)          *
+ * ======================================================================= */
+
+typedef struct smoe_layer smoe_layer;   /* opaque */
+
+typedef struct {
+  int32_t n_shards;      /* G: EP degree = token groups = expert clusters    */
+  int32_t shard_begin;   /* first shard resident in this process             */
+  int32_t shard_count;   /* shards resident in this process (same GPU)       */
+  int32_t n_experts;     /* N routed experts                                 */
+  int32_t top_k;         /* k                                                */
+  int32_t hidden;        /* d                                                */
+  int32_t ffn;           /* f (SwiGLU intermediate)                          */
+  int32_t renormalize;   /* 1: top-k weights renormalised to sum 1           */
+  int64_t max_tokens;    /* n capacity per forward                           */
+  int64_t expert_rows;   /* row capacity of each shard's expert input buffer */
+  int32_t world_size;    /* processes taking part (1 = all shards local)     */
+  int32_t world_rank;
+} smoe_layer_config;
+
+/* Buffer slots a host binds with smoe_layer_bind(). "peer" slots are bound
+ * once per shard g in [0, G) (remote shards: IPC-mapped pointers); "local"
+ * slots once per resident shard (index = g - shard_begin) or once (index 0). */
+enum {
+  /* peer, per shard */
+  SMOE_BUF_PARTIAL = 0,   /* bf16 [max_tokens, d]: this rank's attention-TP partial */
+  SMOE_BUF_XIN,           /* bf16 [expert_rows, d]: expert input rows (dispatch dst) */
+  SMOE_BUF_XMETA,         /* int64 [expert_rows]: (src shard << 40) | pair slot      */
+  SMOE_BUF_YPAIR,         /* bf16 [max_tokens*k, d]: expert outputs per (token,slot) */
+  SMOE_BUF_OUT,           /* bf16 [max_tokens, d]: layer output, original order      */
+  SMOE_BUF_COUNTS,        /* int32 [G, N]: pair counts source shard x expert slot    */
+  SMOE_BUF_SIGNAL,        /* uint32 [64]: cross-process barrier pad (per process)    */
+  /* local, per resident shard */
+  SMOE_BUF_HS,            /* bf16 [max_tokens, d]: SRS output (this shard's group)   */
+  SMOE_BUF_TOPK_IDS,      /* int32 [max_tokens, k]: expert slot (s-EG order)         */
+  SMOE_BUF_TOPK_W,        /* f32  [max_tokens, k]: combine weights                   */
+  SMOE_BUF_PAIR_RANK,     /* int32 [max_tokens, k]: rank inside (shard, slot)        */
+  SMOE_BUF_HMID,          /* bf16 [expert_rows, f]: SwiGLU activations               */
+  /* local, once */
+  SMOE_BUF_FORWARD,       /* int64 [G*max_tokens]                                    */
+  SMOE_BUF_INVERSE,       /* int64 [max_tokens]                                      */
+  SMOE_BUF_DEV,           /* int64 [max_tokens]                                      */
+  SMOE_BUF_PLAN_COUNTS,   /* int32 [G]                                               */
+  SMOE_BUF_GROUP,         /* int64 [1]                                               */
+  SMOE_BUF_STATS,         /* int64 [16]: see SMOE_STAT_*                             */
+  SMOE_BUF_ERR,           /* int32 [1]                                               */
+  SMOE_BUF_WORKSPACE,     /* bytes: smoe_layer_workspace_bytes()                     */
+  SMOE_BUF_PROBLEMS,      /* bytes: grouped-GEMM problem table, 64 KiB               */
+  SMOE_BUF_EPOCH,         /* uint32 [1]: barrier epoch (device)                      */
+  SMOE_BUF__COUNT
+};
+
+/* stats written by the layer (int64 each). */
+enum {
+  SMOE_STAT_LOCAL_PAIRS = 0,   /* (token, expert) pairs whose expert is on the token's shard */
+  SMOE_STAT_REMOTE_PAIRS,      /* pairs crossing shards (the A2A events, comm.py:214-216)   */
+  SMOE_STAT_SRS_ROWS,          /* rows reduced by SRS (real rows, no pads)                 */
+  SMOE_STAT_GROUP,             /* max group (scheduler.py:135)                              */
+  SMOE_STAT__COUNT = 16
+};
+
+size_t smoe_layer_workspace_bytes(const smoe_layer_config* cfg);
+
+int smoe_layer_create(const smoe_layer_config* cfg, smoe_layer** out);
+void smoe_layer_destroy(smoe_layer* layer);
+/* Bind a device buffer (see SMOE_BUF_*). */
+int smoe_layer_bind(smoe_layer* layer, int32_t slot, int32_t index, void* ptr);
+
+/* Lookup tables (predictor.py:39-82) and the s-EG expert placement
+ * (scheduler.py:200-224).  slot_owner[N]: cluster (= shard) that owns expert
+ * slot e' in the cluster-contiguous order, i.e. labels[new_to_old[e']]. */
+int smoe_layer_set_tables(smoe_layer* layer,
+                          const int16_t* t_labels, const float* t_conf,
+                          int64_t vocab, const int16_t* a_best,
+                          const float* a_conf, int64_t a_rows,
+                          int32_t hist_len, const int32_t* slot_owner_h);
+
+/* Weights, all bf16, expert slots in s-EG order:
+ *   w_gate  [N, d]          gate rows already permuted by new_to_old
+ *   b_gate  f32 [N] or NULL
+ *   w13     [L, 2f, d]      L = experts owned by the resident shards, packed
+ *                           by smoe_pack_w13 (gate/up interleaved per 128 rows)
+ *   w2      [L, d, f]       down projection                                  */
+int smoe_layer_set_weights(smoe_layer* layer, const void* w_gate,
+                           const float* b_gate, const void* w13,
+                           const void* w2);
+
+/* Pack per-expert gate_proj [f, d] and up_proj [f, d] (both bf16, expert e at
+ * w1[e], w3[e]) into the w13 layout the SwiGLU GEMM reads. */
+int smoe_pack_w13(const void* w1, const void* w3, int32_t n_local_experts,
+                  int32_t ffn, int32_t hidden, void* w13, void* stream);
+
+/* Stages of the forward (run in this order by smoe_layer_forward):           */
+enum {
+  SMOE_STAGE_PLAN = 0,    /* K1 lookup + stable partition plan               */
+  SMOE_STAGE_SRS,         /* K3 shuffled reduce-scatter (permute fused)      */
+  SMOE_STAGE_GATE,        /* K4 gate GEMV + softmax + top-k + locality       */
+  SMOE_STAGE_ROUTE,       /* K5a per-shard stable pair ranks + count publish */
+  SMOE_STAGE_DISPATCH,    /* K5b A2A dispatch: remote rows only cross shards */
+  SMOE_STAGE_EXPERT_UP,   /* K6a tcgen05 grouped GEMM + SwiGLU epilogue      */
+  SMOE_STAGE_EXPERT_DOWN, /* K6b tcgen05 grouped GEMM + A2A-combine epilogue */
+  SMOE_STAGE_COMBINE_SAG, /* K8 weighted combine + shuffled all-gather       */
+  SMOE_STAGE__COUNT
+};
+
+/* Run one stage / the whole layer.  tokens int64[n] and hist (int64[n,
+ * hist_len] or NULL) are replicated on every process, as in attention TP. */
+int smoe_layer_stage(smoe_layer* layer, int32_t stage, const int64_t* tokens,
+                     const int64_t* hist, int64_t n, void* stream);
+int smoe_layer_forward(smoe_layer* layer, const int64_t* tokens,
+                       const int64_t* hist, int64_t n, void* stream);
+
+/* Cross-process barrier over the bound SIGNAL pads (no-op if world_size 1). */
+int smoe_layer_barrier(smoe_layer* layer, void* stream);
+
+/* ======================================================================= *
+ *  Grouped GEMM (K6) — exposed for tests and microbenchmarks                *
+ * ======================================================================= */
+/* For problem p: C[c_off_p + i, :] = epilogue(A[a_off_p + i, :K] . B_p^T)
+ * for i < m_p, with B_p = B[b_index_p * N_b : (b_index_p+1) * N_b, :K].
+ * problems: device int64[num_problems, 4] = {a_off, m, b_index, c_off}.
+ * epilogue 0: bf16 store, C row stride ldc (N_b columns);
+ * epilogue 1: SwiGLU, B packed by smoe_pack_w13: C has N_b/2 columns.     */
+int smoe_grouped_gemm(const void* A, int64_t a_rows, int64_t K,
+                      const void* B, int64_t b_rows, int64_t n_b,
+                      const int64_t* problems, int32_t num_problems,
+                      int32_t epilogue, void* C, int64_t c_rows, int64_t ldc,
+                      void* stream);
+
+/* ======================================================================= *
+ *  CUDA IPC helpers (multi-process shard tables)                           *
+ * ======================================================================= */
+/* cudaMalloc'd buffers (IPC handles then cover exactly the buffer). */
+int smoe_device_alloc(size_t bytes, void** dev_ptr_out_h);
+int smoe_device_free(void* dev_ptr);
+int smoe_ipc_handle(void* dev_ptr, void* handle_out_h /* 64 bytes */);
+int smoe_ipc_open(const void* handle_h, void** dev_ptr_out_h);
+int smoe_ipc_close(void* dev_ptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMOE_H_ */

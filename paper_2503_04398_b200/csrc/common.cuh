@@ -1,0 +1,88 @@
+// common.cuh — shared device helpers for the smoe sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/smoe.h"
+
+#define SMOE_CUDA_TRY(expr)                                   \
+  do {                                                        \
+    cudaError_t _e = (expr);                                  \
+    if (_e != cudaSuccess) { return SMOE_ERR_CUDA; }          \
+  } while (0)
+
+#define SMOE_LAUNCH_CHECK() SMOE_CUDA_TRY(cudaGetLastError())
+
+namespace smoe {
+
+constexpr int kWarp = 32;
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Number of SMs on the current device (cached per process).
+int num_sms();
+
+__device__ __forceinline__ void set_err(int32_t* err, int32_t bit) {
+  if (err) atomicOr(err, bit);
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---- bf16 helpers (round-to-nearest-even, matches torch / oracle) -------
+__device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// ---- 128-bit global memory access --------------------------------------
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ld_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void st_na_v4(void* p, uint4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+// fp32 accumulate of 8 bf16 values held in a uint4
+__device__ __forceinline__ void acc_bf16x8(float (&a)[8], uint4 v) {
+  a[0] += bf16_lo(v.x); a[1] += bf16_hi(v.x);
+  a[2] += bf16_lo(v.y); a[3] += bf16_hi(v.y);
+  a[4] += bf16_lo(v.z); a[5] += bf16_hi(v.z);
+  a[6] += bf16_lo(v.w); a[7] += bf16_hi(v.w);
+}
+__device__ __forceinline__ void set_bf16x8(float (&a)[8], uint4 v) {
+  a[0] = bf16_lo(v.x); a[1] = bf16_hi(v.x);
+  a[2] = bf16_lo(v.y); a[3] = bf16_hi(v.y);
+  a[4] = bf16_lo(v.z); a[5] = bf16_hi(v.z);
+  a[6] = bf16_lo(v.w); a[7] = bf16_hi(v.w);
+}
+__device__ __forceinline__ uint4 pack_bf16x8(const float (&a)[8]) {
+  return make_uint4(pack_bf16x2(a[0], a[1]), pack_bf16x2(a[2], a[3]),
+                    pack_bf16x2(a[4], a[5]), pack_bf16x2(a[6], a[7]));
+}
+
+}  // namespace smoe

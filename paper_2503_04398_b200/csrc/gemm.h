@@ -1,0 +1,42 @@
+// gemm.h — host interface of the tcgen05 grouped GEMM (K6).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "../../include/smoe.h"
+
+namespace smoe {
+
+enum GemmEpilogue : int32_t {
+  kEpiStore = 0,    // C[c_off + i, n] = bf16(acc)
+  kEpiSwiGLU = 1,   // C[c_off + i, n'] = bf16(silu(acc_gate) * acc_up), B packed by pack_w13
+  kEpiScatter = 2,  // row i goes to dst_base[meta >> 40] + (meta & mask) * ldd  (A2A combine)
+};
+
+constexpr int kGemmBM = 128;
+constexpr int kGemmBN = 256;
+constexpr int kGemmBK = 64;
+constexpr int kGemmMaxProblems = 256;
+constexpr int64_t kMetaSlotMask = (int64_t(1) << 40) - 1;
+
+struct GemmArgs {
+  const int64_t* problems;   // [P, 4] {a_off, m, b_index, c_off}
+  int32_t num_problems;
+  int32_t num_k_blocks;      // K / 64
+  int32_t n_tiles_n;         // n_b / 256
+  int32_t n_b;               // rows of B per problem (output columns before SwiGLU)
+  char* c;                   // store / swiglu output
+  int64_t ldc;               // elements
+  const int64_t* meta;       // scatter: per A row
+  char* dst_base[SMOE_MAX_SHARDS];
+  int64_t ldd;               // elements
+};
+
+// Encodes a 2D bf16 K-major tensor map (rows x cols, box 64 x box_rows, 128B swizzle).
+int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols,
+                   int32_t box_rows);
+
+int launch_grouped_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap_b,
+                        const GemmArgs& args, int32_t epilogue, cudaStream_t stream);
+
+}  // namespace smoe

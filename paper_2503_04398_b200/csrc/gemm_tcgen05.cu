@@ -1,0 +1,465 @@
+// gemm_tcgen05.cu — K6: persistent, warp-specialised grouped GEMM for the
+// expert FFN on sm_100a (TMA -> SMEM -> tcgen05.mma -> TMEM -> epilogue).
+//
+// The expert FFN is not in the reference; it is the
+// one dense contraction of the layer.  One launch covers every (shard,
+// expert) problem resident on this GPU: problem p multiplies rows
+// [a_off_p, a_off_p + m_p) of the expert-input buffer by expert b_index_p's
+// weight block.  Row counts live in device memory (written by the dispatch
+// stage), so the launch needs no host synchronisation and is graph-capturable.
+//
+// CTA layout (256 threads, 1 CTA per SM, persistent over tiles):
+//   warp 0 lane 0  TMA producer: A tile 128x64 + B tile 256x64 per k-block,
+//                  4-stage mbarrier ring (full/empty)
+//   warp 1 lane 0  MMA issuer: tcgen05.mma.cta_group::1.kind::f16,
+//                  M=128 N=256 K=16, fp32 accumulator in TMEM; two
+//                  accumulator buffers (2 x 256 columns) so the epilogue of
+//                  tile t overlaps the MMAs of tile t+1
+//   warp 2         TMEM allocator (512 columns)
+//   warps 4..7     epilogue: tcgen05.ld 32x32b -> registers -> bf16 ->
+//                  swizzled SMEM staging -> coalesced 16 B row stores
+//                  (plain, SwiGLU-fused, or scattered to peer shards: the
+//                  A2A combine is fused into the down-projection epilogue)
+#include "common.cuh"
+#include "gemm.h"
+#include <algorithm>
+
+namespace smoe {
+
+constexpr int kStages = 4;
+constexpr int kThreads = 256;
+constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2;    // 16 KiB
+constexpr uint32_t kBBytes = kGemmBN * kGemmBK * 2;    // 32 KiB
+constexpr uint32_t kStageBytes = kABytes + kBBytes;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kStagingBytes = 4 * 32 * 64;        // 4 epilogue warps x 32 rows x 64 B
+constexpr size_t kGemmSmem = 1024 /*align slack*/ + kStages * kStageBytes + kStagingBytes +
+                             1024 /*barriers*/ + kGemmMaxProblems * 32 + 4 * (kGemmMaxProblems + 1);
+
+// instruction descriptor: D f32, A/B bf16, K-major both, N=256, M=128
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) |
+                            (uint32_t(kGemmBN >> 3) << 17) | (uint32_t(kGemmBM >> 4) << 24);
+
+// ---------------------------------------------------------------- PTX glue
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n"
+      "DONE:\n\t}" :: "r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];"
+      :: "r"(dst), "l"(map), "r"(bar), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               :: "r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      :: "r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// K-major, 128B-swizzled operand tile: 8-row core groups 1024 B apart.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+#define SMOE_TMEM_LD32(taddr, r)                                                              \
+  asm volatile(                                                                               \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"      \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),   \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),            \
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),         \
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),         \
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),         \
+        "=r"(r[31])                                                                           \
+      : "r"(taddr))
+
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- tiles
+struct SmemProblems {
+  int64_t a_off[kGemmMaxProblems];
+  int64_t c_off[kGemmMaxProblems];
+  int32_t m[kGemmMaxProblems];
+  int32_t b_idx[kGemmMaxProblems];
+  int32_t tile_prefix[kGemmMaxProblems + 1];
+};
+
+struct TileCoord {
+  int32_t p, m_blk, n_blk;
+};
+
+// Tiles are enumerated problem-major; inside a problem m-blocks vary fastest
+// so the CTAs of one wave share a weight tile (n-block) and sweep the
+// problem's A rows, which stay L2-resident.
+__device__ __forceinline__ TileCoord decode_tile(const SmemProblems& sp, int32_t np,
+                                                 int32_t n_tiles_n, int32_t t, int32_t& cursor) {
+  while (cursor + 1 < np && sp.tile_prefix[cursor + 1] <= t) ++cursor;
+  const int32_t local = t - sp.tile_prefix[cursor];
+  const int32_t mt = (sp.m[cursor] + kGemmBM - 1) / kGemmBM;
+  TileCoord c;
+  c.p = cursor;
+  c.m_blk = local % mt;
+  c.n_blk = local / mt;
+  (void)n_tiles_n;
+  return c;
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                    const __grid_constant__ CUtensorMap tmap_b, const GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + kStages * kABytes;
+  uint8_t* staging = smem + kStages * kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + kStagingBytes);
+  // bars: full[kStages], empty[kStages], tfull[2], tempty[2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  SmemProblems& sp = *reinterpret_cast<SmemProblems*>(bars + 2 * kStages + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t np = args.num_problems;
+
+  // ---- problem table -> shared, tile prefix
+  for (int p = threadIdx.x; p < np; p += kThreads) {
+    const int64_t* q = args.problems + 4 * p;
+    sp.a_off[p] = q[0];
+    sp.m[p] = (int32_t)q[1];
+    sp.b_idx[p] = (int32_t)q[2];
+    sp.c_off[p] = q[3];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t acc = 0;
+    for (int p = 0; p < np; ++p) {
+      sp.tile_prefix[p] = acc;
+      const int32_t m = sp.m[p] > 0 ? sp.m[p] : 0;
+      acc += ((m + kGemmBM - 1) / kGemmBM) * args.n_tiles_n;
+    }
+    sp.tile_prefix[np] = acc;
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(smem_addr(&bars[s]), 1);
+      mbar_init(smem_addr(&bars[kStages + s]), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(smem_addr(&bars[2 * kStages + a]), 1);
+      mbar_init(smem_addr(&bars[2 * kStages + 2 + a]), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&tmap_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&tmap_b) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_addr(tmem_holder)), "r"(kTmemCols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int32_t total_tiles = sp.tile_prefix[np];
+  const uint32_t full0 = smem_addr(&bars[0]);
+  const uint32_t empty0 = smem_addr(&bars[kStages]);
+  const uint32_t tfull0 = smem_addr(&bars[2 * kStages]);
+  const uint32_t tempty0 = smem_addr(&bars[2 * kStages + 2]);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      int32_t stage = 0;
+      uint32_t phase = 0;
+      int32_t cursor = 0;
+      for (int32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const TileCoord tc = decode_tile(sp, np, args.n_tiles_n, t, cursor);
+        const int32_t a_row = (int32_t)(sp.a_off[tc.p] + (int64_t)tc.m_blk * kGemmBM);
+        const int32_t b_row = sp.b_idx[tc.p] * args.n_b + tc.n_blk * kGemmBN;
+        for (int32_t kb = 0; kb < args.num_k_blocks; ++kb) {
+          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          const uint32_t fb = full0 + 8 * stage;
+          mbar_expect_tx(fb, kStageBytes);
+          tma_load_2d(smem_addr(smem_a + stage * kABytes), &tmap_a, fb, kb * kGemmBK, a_row);
+          tma_load_2d(smem_addr(smem_b + stage * kBBytes), &tmap_b, fb, kb * kGemmBK, b_row);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer =====
+      int32_t stage = 0;
+      uint32_t phase = 0;
+      uint32_t acc = 0, acc_phase = 0;
+      for (int32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kGemmBN;
+        for (int32_t kb = 0; kb < args.num_k_blocks; ++kb) {
+          mbar_wait(full0 + 8 * stage, phase);
+          tc_fence_after();
+          const uint64_t ad = sdesc(smem_addr(smem_a + stage * kABytes));
+          const uint64_t bd = sdesc(smem_addr(smem_b + stage * kBBytes));
+#pragma unroll
+          for (int k = 0; k < kGemmBK / 16; ++k)   // +32 B per K=16 step inside the swizzle atom
+            tc_mma(d_tmem, ad + 2 * k, bd + 2 * k, kIdesc, (kb | k) != 0);
+          tc_commit(empty0 + 8 * stage);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(tfull0 + 8 * acc);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue =====
+    const int ew = warp - 4;                          // TMEM lane quarter
+    uint8_t* stg = staging + ew * (32 * 64);
+    uint32_t acc = 0, acc_phase = 0;
+    int32_t cursor = 0;
+    for (int32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      const TileCoord tc = decode_tile(sp, np, args.n_tiles_n, t, cursor);
+      const int32_t m = sp.m[tc.p];
+      const int32_t row0 = tc.m_blk * kGemmBM + ew * 32;   // first row of this warp
+      // per-lane destination row pointer (lane l <-> row row0 + l)
+      char* my_row = nullptr;
+      {
+        const int32_t r = row0 + lane;
+        if (r < m) {
+          if (EPI == kEpiScatter) {
+            const int64_t meta = __ldg(args.meta + sp.a_off[tc.p] + r);
+            const int32_t shard = (int32_t)(meta >> 40);
+            my_row = args.dst_base[shard] + ((meta & kMetaSlotMask) * args.ldd +
+                                              (int64_t)tc.n_blk * kGemmBN) * 2;
+          } else {
+            const int64_t ncols = (EPI == kEpiSwiGLU) ? kGemmBN / 2 : kGemmBN;
+            my_row = args.c + ((sp.c_off[tc.p] + r) * args.ldc + (int64_t)tc.n_blk * ncols) * 2;
+          }
+        }
+      }
+      mbar_wait(tfull0 + 8 * acc, acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + acc * kGemmBN + ((uint32_t)(ew * 32) << 16);
+      constexpr int kChunks = (EPI == kEpiSwiGLU) ? 4 : 8;   // 32 output columns per chunk
+#pragma unroll 1
+      for (int ch = 0; ch < kChunks; ++ch) {
+        uint32_t packed[16];
+        if (EPI == kEpiSwiGLU) {
+          uint32_t g[32], u[32];
+          SMOE_TMEM_LD32(tbase + ch * 32, g);
+          SMOE_TMEM_LD32(tbase + 128 + ch * 32, u);
+          tmem_wait_ld();
+          if (ch == kChunks - 1) { tc_fence_before(); mbar_arrive(tempty0 + 8 * acc); }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float g0 = __uint_as_float(g[2 * j]), g1 = __uint_as_float(g[2 * j + 1]);
+            const float u0 = __uint_as_float(u[2 * j]), u1 = __uint_as_float(u[2 * j + 1]);
+            const float h0 = g0 / (1.0f + __expf(-g0)) * u0;
+            const float h1 = g1 / (1.0f + __expf(-g1)) * u1;
+            packed[j] = pack_bf16x2(h0, h1);
+          }
+        } else {
+          uint32_t v[32];
+          SMOE_TMEM_LD32(tbase + ch * 32, v);
+          tmem_wait_ld();
+          if (ch == kChunks - 1) { tc_fence_before(); mbar_arrive(tempty0 + 8 * acc); }
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            packed[j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+        }
+        // stage row `lane` (64 B = 4 x 16 B chunks, XOR-swizzled against bank conflicts)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int pq = q ^ ((lane >> 1) & 3);
+          *reinterpret_cast<uint4*>(stg + lane * 64 + pq * 16) =
+              make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+        }
+        __syncwarp();
+        // coalesced stores: 8 rows x 64 B per instruction
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int r = it * 8 + (lane >> 2);
+          const int q = lane & 3;
+          const unsigned long long rp =
+              __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), r);
+          if (rp) {
+            const uint4 val =
+                *reinterpret_cast<const uint4*>(stg + r * 64 + ((q ^ ((r >> 1) & 3)) * 16));
+            st_v4(reinterpret_cast<char*>(rp) + ch * 64 + q * 16, val);
+          }
+        }
+        __syncwarp();
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
+                 :: "r"(tmem_base), "r"(kTmemCols) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols,
+                   int32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return SMOE_ERR_CUDA;
+  if (rows <= 0 || cols <= 0 || (cols * 2) % 16 != 0 || ((uintptr_t)base % 16) != 0)
+    return SMOE_ERR_INVALID_ARG;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kGemmBK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? SMOE_OK : SMOE_ERR_CUDA;
+}
+
+template <int EPI>
+static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args,
+                       cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    SMOE_CUDA_TRY(cudaFuncSetAttribute(grouped_gemm_kernel<EPI>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kGemmSmem));
+    attr_set = true;
+  }
+  grouped_gemm_kernel<EPI><<<num_sms(), kThreads, kGemmSmem, st>>>(a, b, args);
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
+int launch_grouped_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args,
+                        int32_t epilogue, cudaStream_t st) {
+  if (args.num_problems <= 0) return SMOE_OK;
+  if (args.num_problems > kGemmMaxProblems) return SMOE_ERR_UNSUPPORTED;
+  switch (epilogue) {
+    case kEpiStore: return launch_impl<kEpiStore>(a, b, args, st);
+    case kEpiSwiGLU: return launch_impl<kEpiSwiGLU>(a, b, args, st);
+    case kEpiScatter: return launch_impl<kEpiScatter>(a, b, args, st);
+    default: return SMOE_ERR_INVALID_ARG;
+  }
+}
+
+// w13[e, blk*256 + r]      = w1[e, blk*128 + r]        r < 128  (gate)
+// w13[e, blk*256 + 128 + r] = w3[e, blk*128 + r]       r < 128  (up)
+__global__ void pack_w13_kernel(const uint4* __restrict__ w1, const uint4* __restrict__ w3,
+                                int64_t n_rows_out, int32_t ffn, int64_t row_vecs,
+                                uint4* __restrict__ w13) {
+  const int64_t total = n_rows_out * row_vecs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t orow = i / row_vecs, v = i - orow * row_vecs;
+    const int64_t e = orow / (2 * ffn), r = orow - e * 2 * ffn;
+    const int64_t blk = r / 256, rr = r - blk * 256;
+    const int64_t src_row = e * ffn + blk * 128 + (rr & 127);
+    w13[i] = (rr < 128 ? w1 : w3)[src_row * row_vecs + v];
+  }
+}
+
+}  // namespace smoe
+
+using namespace smoe;
+
+extern "C" int smoe_pack_w13(const void* w1, const void* w3, int32_t n_local_experts,
+                             int32_t ffn, int32_t hidden, void* w13, void* stream) {
+  if (n_local_experts <= 0 || ffn <= 0 || hidden <= 0 || !w1 || !w3 || !w13)
+    return SMOE_ERR_INVALID_ARG;
+  if (ffn % 128 != 0 || hidden % 8 != 0) return SMOE_ERR_UNSUPPORTED;
+  const int64_t rows = (int64_t)n_local_experts * 2 * ffn;
+  const int64_t vecs = hidden / 8;
+  const int blocks = (int)std::min<int64_t>(ceil_div(rows * vecs, 256), 148 * 32);
+  pack_w13_kernel<<<blocks, 256, 0, as_stream(stream)>>>(
+      static_cast<const uint4*>(w1), static_cast<const uint4*>(w3), rows, ffn, vecs,
+      static_cast<uint4*>(w13));
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
+extern "C" int smoe_grouped_gemm(const void* A, int64_t a_rows, int64_t K, const void* B,
+                                 int64_t b_rows, int64_t n_b, const int64_t* problems,
+                                 int32_t num_problems, int32_t epilogue, void* C, int64_t c_rows,
+                                 int64_t ldc, void* stream) {
+  (void)c_rows;
+  if (!A || !B || !C || !problems || num_problems <= 0) return SMOE_ERR_INVALID_ARG;
+  if (K % kGemmBK != 0 || n_b % kGemmBN != 0) return SMOE_ERR_UNSUPPORTED;
+  if (epilogue != kEpiStore && epilogue != kEpiSwiGLU) return SMOE_ERR_INVALID_ARG;
+  CUtensorMap ta, tb;
+  int rc = make_tmap_bf16(&ta, A, a_rows, K, kGemmBM);
+  if (rc) return rc;
+  rc = make_tmap_bf16(&tb, B, b_rows, K, kGemmBN);
+  if (rc) return rc;
+  GemmArgs args{};
+  args.problems = problems;
+  args.num_problems = num_problems;
+  args.num_k_blocks = (int32_t)(K / kGemmBK);
+  args.n_tiles_n = (int32_t)(n_b / kGemmBN);
+  args.n_b = (int32_t)n_b;
+  args.c = static_cast<char*>(C);
+  args.ldc = ldc;
+  return launch_grouped_gemm(ta, tb, args, epilogue, as_stream(stream));
+}

@@ -1,0 +1,325 @@
+// layer.cu — host runtime of the speculative MoE layer (C-ABI handle).
+//
+// Owns the shard tables, the TMA descriptors of the two expert GEMMs and the
+// small device-side placement tables, and sequences the stages of Algorithm 2
+// on one stream.  With world_size > 1 a cross-process
+// barrier over NVLink-mapped signal pads separates the stages whose inputs are
+// written by other processes (after ROUTE, DISPATCH, EXPERT_DOWN, COMBINE_SAG).
+#include "common.cuh"
+#include "gemm.h"
+#include "layer_kernels.cuh"
+
+#include <cstring>
+#include <vector>
+#include <algorithm>
+
+using namespace smoe;
+
+struct smoe_layer {
+  smoe_layer_config cfg;
+  void* buf[SMOE_BUF__COUNT][SMOE_MAX_SHARDS];
+  // tables
+  const int16_t* t_labels = nullptr;
+  const float* t_conf = nullptr;
+  int64_t vocab = 0;
+  const int16_t* a_best = nullptr;
+  const float* a_conf = nullptr;
+  int64_t a_rows = 0;
+  int32_t hist_len = 0;
+  std::vector<int32_t> slot_owner_h, slot_first_h;
+  int32_t* slot_owner_d = nullptr;   // [N]
+  int32_t* slot_first_d = nullptr;   // [G + 1]
+  int32_t local_slots = 0;           // expert slots owned by the resident shards
+  // weights
+  const void* w_gate = nullptr;
+  const float* b_gate = nullptr;
+  const void* w13 = nullptr;
+  const void* w2 = nullptr;
+  // GEMM descriptors
+  bool maps_ready = false;
+  CUtensorMap map_x, map_w13, map_h, map_w2;
+};
+
+static bool valid_cfg(const smoe_layer_config* c) {
+  return c && c->n_shards >= 1 && c->n_shards <= SMOE_MAX_SHARDS && c->shard_begin >= 0 &&
+         c->shard_count >= 1 && c->shard_begin + c->shard_count <= c->n_shards &&
+         c->n_experts >= 1 && c->top_k >= 1 && c->top_k <= c->n_experts && c->hidden > 0 &&
+         c->ffn > 0 && c->max_tokens > 0 && c->expert_rows > 0 && c->world_size >= 1 &&
+         c->world_rank >= 0 && c->world_rank < c->world_size;
+}
+
+extern "C" size_t smoe_layer_workspace_bytes(const smoe_layer_config* cfg) {
+  if (!cfg) return 0;
+  return smoe_plan_workspace_bytes(cfg->max_tokens, cfg->n_shards);
+}
+
+extern "C" int smoe_layer_create(const smoe_layer_config* cfg, smoe_layer** out) {
+  if (!valid_cfg(cfg) || !out) return SMOE_ERR_INVALID_ARG;
+  if (cfg->hidden % kGemmBN != 0 || cfg->ffn % 128 != 0 || (2 * cfg->ffn) % kGemmBN != 0 ||
+      cfg->n_experts > 64 || cfg->top_k > 8)
+    return SMOE_ERR_UNSUPPORTED;
+  smoe_layer* L = new smoe_layer();
+  L->cfg = *cfg;
+  std::memset(L->buf, 0, sizeof(L->buf));
+  if (cudaMalloc(&L->slot_owner_d, sizeof(int32_t) * cfg->n_experts) != cudaSuccess ||
+      cudaMalloc(&L->slot_first_d, sizeof(int32_t) * (cfg->n_shards + 1)) != cudaSuccess) {
+    delete L;
+    return SMOE_ERR_CUDA;
+  }
+  *out = L;
+  return SMOE_OK;
+}
+
+extern "C" void smoe_layer_destroy(smoe_layer* L) {
+  if (!L) return;
+  cudaFree(L->slot_owner_d);
+  cudaFree(L->slot_first_d);
+  delete L;
+}
+
+extern "C" int smoe_layer_bind(smoe_layer* L, int32_t slot, int32_t index, void* ptr) {
+  if (!L || slot < 0 || slot >= SMOE_BUF__COUNT || index < 0 || index >= SMOE_MAX_SHARDS)
+    return SMOE_ERR_INVALID_ARG;
+  L->buf[slot][index] = ptr;
+  L->maps_ready = false;
+  return SMOE_OK;
+}
+
+extern "C" int smoe_layer_set_tables(smoe_layer* L, const int16_t* t_labels, const float* t_conf,
+                                     int64_t vocab, const int16_t* a_best, const float* a_conf,
+                                     int64_t a_rows, int32_t hist_len,
+                                     const int32_t* slot_owner_h) {
+  if (!L || !t_labels || !t_conf || vocab <= 0 || !slot_owner_h) return SMOE_ERR_INVALID_ARG;
+  const int N = L->cfg.n_experts, G = L->cfg.n_shards;
+  std::vector<int32_t> owner(slot_owner_h, slot_owner_h + N);
+  // s-EG order: every cluster's slots are contiguous and clusters ascend
+  for (int e = 0; e < N; ++e) {
+    if (owner[e] < 0 || owner[e] >= G) return SMOE_ERR_CLUSTERS;
+    if (e && owner[e] < owner[e - 1]) return SMOE_ERR_INVALID_ARG;
+  }
+  std::vector<int32_t> first(G + 1, N);
+  for (int e = N - 1; e >= 0; --e) first[owner[e]] = e;
+  for (int g = G - 1; g >= 0; --g) first[g] = std::min(first[g], first[g + 1]);
+  L->t_labels = t_labels; L->t_conf = t_conf; L->vocab = vocab;
+  L->a_best = a_best; L->a_conf = a_conf; L->a_rows = a_rows; L->hist_len = hist_len;
+  L->slot_owner_h = owner;
+  L->slot_first_h = first;
+  L->local_slots = first[L->cfg.shard_begin + L->cfg.shard_count] - first[L->cfg.shard_begin];
+  SMOE_CUDA_TRY(cudaMemcpy(L->slot_owner_d, owner.data(), sizeof(int32_t) * N,
+                           cudaMemcpyHostToDevice));
+  SMOE_CUDA_TRY(cudaMemcpy(L->slot_first_d, first.data(), sizeof(int32_t) * (G + 1),
+                           cudaMemcpyHostToDevice));
+  L->maps_ready = false;
+  return SMOE_OK;
+}
+
+extern "C" int smoe_layer_set_weights(smoe_layer* L, const void* w_gate, const float* b_gate,
+                                      const void* w13, const void* w2) {
+  if (!L || !w_gate || !w13 || !w2) return SMOE_ERR_INVALID_ARG;
+  L->w_gate = w_gate; L->b_gate = b_gate; L->w13 = w13; L->w2 = w2;
+  L->maps_ready = false;
+  return SMOE_OK;
+}
+
+static ShardPtrs local_ptrs(const smoe_layer* L, int slot) {
+  ShardPtrs p{};
+  for (int i = 0; i < L->cfg.shard_count; ++i) p.p[i] = static_cast<char*>(L->buf[slot][i]);
+  return p;
+}
+// Per-shard ("peer") slot, restricted to the resident shards (index = local).
+static ShardPtrs resident_ptrs(const smoe_layer* L, int slot) {
+  ShardPtrs p{};
+  for (int i = 0; i < L->cfg.shard_count; ++i)
+    p.p[i] = static_cast<char*>(L->buf[slot][L->cfg.shard_begin + i]);
+  return p;
+}
+static ShardPtrs peer_ptrs(const smoe_layer* L, int slot) {
+  ShardPtrs p{};
+  for (int g = 0; g < L->cfg.n_shards; ++g) p.p[g] = static_cast<char*>(L->buf[slot][g]);
+  return p;
+}
+// Distinct pointers among the per-shard bindings of `slot` (one per process).
+static ShardPtrs distinct_ptrs(const smoe_layer* L, int slot, int32_t* count) {
+  ShardPtrs p{};
+  int n = 0;
+  for (int g = 0; g < L->cfg.n_shards; ++g) {
+    char* q = static_cast<char*>(L->buf[slot][g]);
+    bool seen = false;
+    for (int i = 0; i < n; ++i) seen |= (p.p[i] == q);
+    if (!seen) p.p[n++] = q;
+  }
+  *count = n;
+  return p;
+}
+
+static int check_bound(const smoe_layer* L) {
+  const auto& c = L->cfg;
+  for (int g = 0; g < c.n_shards; ++g)
+    for (int s : {SMOE_BUF_PARTIAL, SMOE_BUF_XIN, SMOE_BUF_XMETA, SMOE_BUF_YPAIR, SMOE_BUF_OUT,
+                  SMOE_BUF_COUNTS})
+      if (!L->buf[s][g]) return SMOE_ERR_INVALID_ARG;
+  for (int i = 0; i < c.shard_count; ++i)
+    for (int s : {SMOE_BUF_HS, SMOE_BUF_TOPK_IDS, SMOE_BUF_TOPK_W, SMOE_BUF_PAIR_RANK})
+      if (!L->buf[s][i]) return SMOE_ERR_INVALID_ARG;
+  for (int s : {SMOE_BUF_HMID, SMOE_BUF_FORWARD, SMOE_BUF_INVERSE, SMOE_BUF_DEV,
+                SMOE_BUF_PLAN_COUNTS, SMOE_BUF_GROUP, SMOE_BUF_STATS, SMOE_BUF_ERR,
+                SMOE_BUF_WORKSPACE, SMOE_BUF_PROBLEMS})
+    if (!L->buf[s][0]) return SMOE_ERR_INVALID_ARG;
+  if (c.world_size > 1) {
+    for (int g = 0; g < c.n_shards; ++g)
+      if (!L->buf[SMOE_BUF_SIGNAL][g]) return SMOE_ERR_INVALID_ARG;
+    if (!L->buf[SMOE_BUF_EPOCH][0]) return SMOE_ERR_INVALID_ARG;
+  }
+  // the resident shards' expert inputs / metadata must form one arena
+  // (one TMA descriptor covers all local problems)
+  const int64_t xs = c.expert_rows * (int64_t)c.hidden * 2, ms = c.expert_rows * 8;
+  for (int i = 1; i < c.shard_count; ++i) {
+    const int g0 = c.shard_begin;
+    if (static_cast<char*>(L->buf[SMOE_BUF_XIN][g0 + i]) !=
+            static_cast<char*>(L->buf[SMOE_BUF_XIN][g0]) + i * xs ||
+        static_cast<char*>(L->buf[SMOE_BUF_XMETA][g0 + i]) !=
+            static_cast<char*>(L->buf[SMOE_BUF_XMETA][g0]) + i * ms)
+      return SMOE_ERR_INVALID_ARG;
+  }
+  return SMOE_OK;
+}
+
+static int ensure_maps(smoe_layer* L) {
+  if (L->maps_ready) return SMOE_OK;
+  int rc = check_bound(L);
+  if (rc) return rc;
+  if (!L->w13 || !L->w2 || !L->w_gate || !L->t_labels) return SMOE_ERR_INVALID_ARG;
+  const auto& c = L->cfg;
+  const int64_t rows = c.expert_rows * c.shard_count;
+  const int64_t nl = std::max<int32_t>(L->local_slots, 1);
+  if ((rc = make_tmap_bf16(&L->map_x, L->buf[SMOE_BUF_XIN][c.shard_begin], rows, c.hidden,
+                           kGemmBM)))
+    return rc;
+  if ((rc = make_tmap_bf16(&L->map_w13, L->w13, nl * 2 * c.ffn, c.hidden, kGemmBN))) return rc;
+  if ((rc = make_tmap_bf16(&L->map_h, L->buf[SMOE_BUF_HMID][0], rows, c.ffn, kGemmBM))) return rc;
+  if ((rc = make_tmap_bf16(&L->map_w2, L->w2, nl * c.hidden, c.ffn, kGemmBN))) return rc;
+  L->maps_ready = true;
+  return SMOE_OK;
+}
+
+static LocalRows local_rows(const smoe_layer* L) {
+  LocalRows lr{};
+  lr.counts = static_cast<const int32_t*>(L->buf[SMOE_BUF_PLAN_COUNTS][0]);
+  lr.group = static_cast<const int64_t*>(L->buf[SMOE_BUF_GROUP][0]);
+  lr.forward = static_cast<const int64_t*>(L->buf[SMOE_BUF_FORWARD][0]);
+  lr.shard_begin = L->cfg.shard_begin;
+  lr.shard_count = L->cfg.shard_count;
+  lr.n_shards = L->cfg.n_shards;
+  return lr;
+}
+
+extern "C" int smoe_layer_barrier(smoe_layer* L, void* stream) {
+  if (!L) return SMOE_ERR_INVALID_ARG;
+  if (L->cfg.world_size <= 1) return SMOE_OK;
+  // signal pads are bound per shard; pick one per process (shards are
+  // distributed contiguously: process r owns shards [r*spp, (r+1)*spp))
+  ShardPtrs sig{};
+  const int spp = L->cfg.n_shards / L->cfg.world_size;
+  for (int r = 0; r < L->cfg.world_size; ++r)
+    sig.p[r] = static_cast<char*>(L->buf[SMOE_BUF_SIGNAL][r * spp]);
+  return launch_barrier(sig, L->cfg.world_size, L->cfg.world_rank,
+                        static_cast<uint32_t*>(L->buf[SMOE_BUF_SIGNAL][L->cfg.shard_begin]),
+                        static_cast<uint32_t*>(L->buf[SMOE_BUF_EPOCH][0]), as_stream(stream));
+}
+
+extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
+                                const int64_t* hist, int64_t n, void* stream) {
+  if (!L || n < 0 || n > L->cfg.max_tokens) return SMOE_ERR_INVALID_ARG;
+  int rc = ensure_maps(L);
+  if (rc) return rc;
+  const auto& c = L->cfg;
+  cudaStream_t st = as_stream(stream);
+  const LocalRows lr = local_rows(L);
+  int64_t* stats = static_cast<int64_t*>(L->buf[SMOE_BUF_STATS][0]);
+  int32_t* err = static_cast<int32_t*>(L->buf[SMOE_BUF_ERR][0]);
+  switch (stage) {
+    case SMOE_STAGE_PLAN: {
+      if (n > 0 && !tokens) return SMOE_ERR_INVALID_ARG;
+      SMOE_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(int64_t) * SMOE_STAT__COUNT, st));
+      SMOE_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
+      return smoe_lookup_plan(tokens, n, hist, L->hist_len, L->t_labels, L->t_conf, L->vocab,
+                              L->a_best, L->a_conf, L->a_rows, c.n_shards,
+                              static_cast<int64_t*>(L->buf[SMOE_BUF_DEV][0]),
+                              static_cast<int64_t*>(L->buf[SMOE_BUF_FORWARD][0]),
+                              static_cast<int64_t*>(L->buf[SMOE_BUF_INVERSE][0]),
+                              static_cast<int32_t*>(L->buf[SMOE_BUF_PLAN_COUNTS][0]),
+                              static_cast<int64_t*>(L->buf[SMOE_BUF_GROUP][0]), err,
+                              L->buf[SMOE_BUF_WORKSPACE][0], smoe_layer_workspace_bytes(&c),
+                              stream);
+    }
+    case SMOE_STAGE_SRS:
+      return launch_srs(lr, peer_ptrs(L, SMOE_BUF_PARTIAL), c.hidden, local_ptrs(L, SMOE_BUF_HS),
+                        n, st);
+    case SMOE_STAGE_GATE:
+      return launch_gate(lr, local_ptrs(L, SMOE_BUF_HS), c.hidden, L->w_gate, L->b_gate,
+                         c.n_experts, c.top_k, c.renormalize, L->slot_owner_d,
+                         local_ptrs(L, SMOE_BUF_TOPK_IDS), local_ptrs(L, SMOE_BUF_TOPK_W), stats,
+                         n, st);
+    case SMOE_STAGE_ROUTE: {
+      int32_t nb = 0;
+      ShardPtrs cb = distinct_ptrs(L, SMOE_BUF_COUNTS, &nb);
+      rc = launch_route(lr, c.n_experts, c.top_k, local_ptrs(L, SMOE_BUF_TOPK_IDS),
+                        local_ptrs(L, SMOE_BUF_PAIR_RANK), cb, nb, st);
+      if (rc) return rc;
+      return smoe_layer_barrier(L, stream);
+    }
+    case SMOE_STAGE_DISPATCH: {
+      rc = launch_dispatch(lr, c.n_experts, c.top_k, c.hidden,
+                           static_cast<const int32_t*>(L->buf[SMOE_BUF_COUNTS][c.shard_begin]),
+                           L->slot_owner_d, L->slot_first_d, local_ptrs(L, SMOE_BUF_HS),
+                           local_ptrs(L, SMOE_BUF_TOPK_IDS), local_ptrs(L, SMOE_BUF_PAIR_RANK),
+                           peer_ptrs(L, SMOE_BUF_XIN), peer_ptrs(L, SMOE_BUF_XMETA),
+                           c.expert_rows, static_cast<int64_t*>(L->buf[SMOE_BUF_PROBLEMS][0]),
+                           err, n, st);
+      if (rc) return rc;
+      return smoe_layer_barrier(L, stream);
+    }
+    case SMOE_STAGE_EXPERT_UP: {
+      GemmArgs a{};
+      a.problems = static_cast<const int64_t*>(L->buf[SMOE_BUF_PROBLEMS][0]);
+      a.num_problems = L->local_slots;
+      a.num_k_blocks = c.hidden / kGemmBK;
+      a.n_tiles_n = 2 * c.ffn / kGemmBN;
+      a.n_b = 2 * c.ffn;
+      a.c = static_cast<char*>(L->buf[SMOE_BUF_HMID][0]);
+      a.ldc = c.ffn;
+      return launch_grouped_gemm(L->map_x, L->map_w13, a, kEpiSwiGLU, st);
+    }
+    case SMOE_STAGE_EXPERT_DOWN: {
+      GemmArgs a{};
+      a.problems = static_cast<const int64_t*>(L->buf[SMOE_BUF_PROBLEMS][0]);
+      a.num_problems = L->local_slots;
+      a.num_k_blocks = c.ffn / kGemmBK;
+      a.n_tiles_n = c.hidden / kGemmBN;
+      a.n_b = c.hidden;
+      a.meta = static_cast<const int64_t*>(L->buf[SMOE_BUF_XMETA][c.shard_begin]);
+      for (int g = 0; g < c.n_shards; ++g) a.dst_base[g] = static_cast<char*>(L->buf[SMOE_BUF_YPAIR][g]);
+      a.ldd = c.hidden;
+      rc = launch_grouped_gemm(L->map_h, L->map_w2, a, kEpiScatter, st);
+      if (rc) return rc;
+      return smoe_layer_barrier(L, stream);
+    }
+    case SMOE_STAGE_COMBINE_SAG: {
+      rc = launch_combine_sag(lr, c.top_k, c.hidden, resident_ptrs(L, SMOE_BUF_YPAIR),
+                              local_ptrs(L, SMOE_BUF_TOPK_W), peer_ptrs(L, SMOE_BUF_OUT), n, st);
+      if (rc) return rc;
+      return smoe_layer_barrier(L, stream);
+    }
+    default:
+      return SMOE_ERR_INVALID_ARG;
+  }
+}
+
+extern "C" int smoe_layer_forward(smoe_layer* L, const int64_t* tokens, const int64_t* hist,
+                                  int64_t n, void* stream) {
+  for (int s = 0; s < SMOE_STAGE__COUNT; ++s) {
+    int rc = smoe_layer_stage(L, s, tokens, hist, n, stream);
+    if (rc) return rc;
+  }
+  return SMOE_OK;
+}

@@ -1,0 +1,465 @@
+// layer_kernels.cu — the non-GEMM stages of the speculative MoE layer.
+//
+// Algorithm 2 of the paper over G shards ("virtual
+// ranks").  Shard g owns token group g (slots [g*group, g*group+count_g) of
+// the plan, scheduler.py:119-149) and the experts of cluster g in the s-EG
+// order (scheduler.py:200-224).  Buffers that other shards read or write are
+// addressed through per-shard pointer tables (ShardPtrs): local pointers when
+// shards share a GPU, CUDA-IPC mappings over NVLink when they do not.  The
+// kernels therefore do the collective's data movement themselves:
+//
+//   K3 srs_kernel          shuffled reduce-scatter: gather row forward[s] from
+//                          every shard's partial, fp32 sum in shard order,
+//                          bf16 out (the permutation rides on the reduction)
+//   K4 gate_kernel         logits = h . Wg^T (+b), top-k (ties -> lowest slot),
+//                          softmax weights, local/remote event counts
+//   K5a route_kernel       stable rank of each (token, slot) pair inside its
+//                          expert slot; publishes the shard's count row
+//   K5b dispatch_kernel    A2A dispatch: pair rows land in the owner's expert
+//                          input buffer (a peer store only when remote)
+//   K8 combine_sag_kernel  weighted sum of the k expert outputs, then the
+//                          shuffled all-gather: one store per shard straight
+//                          to the token's original position (resume fused)
+#include "layer_kernels.cuh"
+#include <algorithm>
+
+namespace smoe {
+
+static int grid_cap(int64_t blocks, int per_sm) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)num_sms() * per_sm));
+}
+
+// Shared-memory view of the local shards' row counts.
+struct RowMap {
+  int32_t cnt[SMOE_MAX_SHARDS];
+  int32_t total;
+  int64_t group;
+};
+
+__device__ __forceinline__ void load_rowmap(RowMap& rm, const LocalRows& lr) {
+  if (threadIdx.x == 0) {
+    int32_t t = 0;
+    for (int i = 0; i < lr.shard_count; ++i) {
+      rm.cnt[i] = lr.counts[lr.shard_begin + i];
+      t += rm.cnt[i];
+    }
+    rm.total = t;
+    rm.group = *lr.group;
+  }
+  __syncthreads();
+}
+
+// q in [0, total) -> (local shard index, row inside the group)
+__device__ __forceinline__ void decode_row(const RowMap& rm, int32_t shard_count, int64_t q,
+                                           int32_t& gl, int64_t& j) {
+  gl = 0;
+  while (gl + 1 < shard_count && q >= rm.cnt[gl]) { q -= rm.cnt[gl]; ++gl; }
+  j = q;
+}
+
+// ------------------------------------------------------------------ K3 SRS
+__global__ void __launch_bounds__(256)
+srs_kernel(LocalRows lr, ShardPtrs partials, int64_t d, ShardPtrs hs) {
+  __shared__ RowMap rm;
+  load_rowmap(rm, lr);
+  const int lane = threadIdx.x & 31;
+  const int G = lr.n_shards;
+  const int64_t vecs = d / 8;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t q = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); q < rm.total;
+       q += nwarps) {
+    int32_t gl; int64_t j;
+    decode_row(rm, lr.shard_count, q, gl, j);
+    const int64_t g = lr.shard_begin + gl;
+    const int64_t src = lr.forward[g * rm.group + j];
+    const int64_t row_off = src * d * 2;
+    char* out = hs.p[gl] + j * d * 2;
+    for (int64_t v = lane; v < vecs; v += 32) {
+      uint4 x[SMOE_MAX_SHARDS];
+#pragma unroll
+      for (int r = 0; r < SMOE_MAX_SHARDS; ++r)
+        if (r < G) x[r] = ld_nc_v4(partials.p[r] + row_off + v * 16);
+      float a[8];
+      set_bf16x8(a, x[0]);
+#pragma unroll
+      for (int r = 1; r < SMOE_MAX_SHARDS; ++r)
+        if (r < G) acc_bf16x8(a, x[r]);
+      st_v4(out + v * 16, pack_bf16x8(a));
+    }
+  }
+}
+
+int launch_srs(const LocalRows& lr, const ShardPtrs& partials, int64_t d, const ShardPtrs& hs,
+               int64_t n_rows_bound, cudaStream_t st) {
+  if (d % 8) return SMOE_ERR_UNSUPPORTED;
+  if (n_rows_bound <= 0) return SMOE_OK;
+  srs_kernel<<<grid_cap(ceil_div(n_rows_bound, 8), 16), 256, 0, st>>>(lr, partials, d, hs);
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
+// ------------------------------------------------------------------ K4 gate
+constexpr int kGateRows = 32;
+constexpr int kGateKC = 128;                 // hidden elements per smem chunk
+constexpr int kGateWords = kGateKC / 2;      // bf16x2 words per row chunk
+constexpr int kGatePad = kGateWords + 1;     // conflict-free row stride (words)
+constexpr int kGateMaxN = 64;
+constexpr int kGateMaxK = 8;
+
+__global__ void __launch_bounds__(256)
+gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ w_gate,
+            const float* __restrict__ b_gate, int32_t N, int32_t k, int32_t renorm,
+            const int32_t* __restrict__ slot_owner, ShardPtrs topk_ids, ShardPtrs topk_w,
+            int64_t* stats) {
+  __shared__ RowMap rm;
+  __shared__ uint32_t s_h[kGateRows * kGatePad];
+  __shared__ uint32_t s_w[kGateMaxN * kGatePad];
+  __shared__ float s_logit[kGateRows * (kGateMaxN + 1)];
+  __shared__ int32_t s_gl[kGateRows];
+  __shared__ int64_t s_j[kGateRows];
+  __shared__ unsigned long long s_local, s_remote;
+  load_rowmap(rm, lr);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t words = d / 2;
+  for (int64_t rb = blockIdx.x; rb * kGateRows < rm.total; rb += gridDim.x) {
+    if (tid < kGateRows) {
+      const int64_t q = rb * kGateRows + tid;
+      int32_t gl = -1; int64_t j = 0;
+      if (q < rm.total) decode_row(rm, lr.shard_count, q, gl, j);
+      s_gl[tid] = gl;
+      s_j[tid] = j;
+    }
+    if (tid == 0) { s_local = 0; s_remote = 0; }
+    float acc[kGateMaxN * kGateRows / 256];
+#pragma unroll
+    for (int i = 0; i < kGateMaxN * kGateRows / 256; ++i) acc[i] = 0.f;
+    __syncthreads();
+    for (int64_t kc = 0; kc < words; kc += kGateWords) {
+      // stage H rows and W rows of this chunk (32-bit words, coalesced)
+      for (int e = tid; e < kGateRows * kGateWords; e += 256) {
+        const int r = e / kGateWords, w = e - r * kGateWords;
+        uint32_t v = 0;
+        if (s_gl[r] >= 0 && kc + w < words)
+          v = reinterpret_cast<const uint32_t*>(hs.p[s_gl[r]] + s_j[r] * d * 2)[kc + w];
+        s_h[r * kGatePad + w] = v;
+      }
+      for (int e = tid; e < N * kGateWords; e += 256) {
+        const int r = e / kGateWords, w = e - r * kGateWords;
+        s_w[r * kGatePad + w] = (kc + w < words) ? __ldg(w_gate + r * words + kc + w) : 0u;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < kGateMaxN * kGateRows / 256; ++i) {
+        const int o = tid + 256 * i;
+        if (o < kGateRows * N) {
+          const int r = o / N, e = o - r * N;
+          const uint32_t* hr = s_h + r * kGatePad;
+          const uint32_t* wr = s_w + e * kGatePad;
+          float a = acc[i];
+#pragma unroll 8
+          for (int w = 0; w < kGateWords; ++w) {
+            const uint32_t hv = hr[w], wv = wr[w];
+            a = fmaf(bf16_lo(hv), bf16_lo(wv), a);
+            a = fmaf(bf16_hi(hv), bf16_hi(wv), a);
+          }
+          acc[i] = a;
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < kGateMaxN * kGateRows / 256; ++i) {
+      const int o = tid + 256 * i;
+      if (o < kGateRows * N) {
+        const int r = o / N, e = o - r * N;
+        s_logit[r * (kGateMaxN + 1) + e] = acc[i] + (b_gate ? __ldg(b_gate + e) : 0.f);
+      }
+    }
+    __syncthreads();
+    // top-k + softmax, one warp per row
+    unsigned long long my_local = 0, my_remote = 0;
+    for (int r = warp; r < kGateRows; r += 8) {
+      const int32_t gl = s_gl[r];
+      if (gl < 0) continue;
+      const float* lg = s_logit + r * (kGateMaxN + 1);
+      float v0 = lane < N ? lg[lane] : -INFINITY;
+      float v1 = lane + 32 < N ? lg[lane + 32] : -INFINITY;
+      float mx = fmaxf(v0, v1);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      float ex = (lane < N ? __expf(v0 - mx) : 0.f) + (lane + 32 < N ? __expf(v1 - mx) : 0.f);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ex += __shfl_xor_sync(0xffffffffu, ex, o);
+      const float inv = 1.0f / ex;
+      int sel_e[kGateMaxK];
+      float sel_p[kGateMaxK];
+      float psum = 0.f;
+      for (int s = 0; s < k; ++s) {
+        // candidate: larger value wins, ties -> lower index (stable argsort of -logits)
+        float bv; int bi;
+        if (v1 > v0) { bv = v1; bi = lane + 32; } else { bv = v0; bi = lane; }
+        if (bv == -INFINITY) bi = 1 << 20;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+        }
+        sel_e[s] = bi;
+        sel_p[s] = __expf(bv - mx) * inv;
+        psum += sel_p[s];
+        if (bi == lane) v0 = -INFINITY;
+        if (bi == lane + 32) v1 = -INFINITY;
+      }
+      if (lane == 0) {
+        const int64_t g = lr.shard_begin + gl;
+        int32_t* ids = reinterpret_cast<int32_t*>(topk_ids.p[gl]) + s_j[r] * k;
+        float* wts = reinterpret_cast<float*>(topk_w.p[gl]) + s_j[r] * k;
+        const float scale = renorm ? 1.0f / psum : 1.0f;
+        for (int s = 0; s < k; ++s) {
+          ids[s] = sel_e[s];
+          wts[s] = sel_p[s] * scale;
+          if (slot_owner[sel_e[s]] == g) ++my_local; else ++my_remote;
+        }
+      }
+    }
+    if (lane == 0 && (my_local | my_remote)) {
+      atomicAdd(&s_local, my_local);
+      atomicAdd(&s_remote, my_remote);
+    }
+    __syncthreads();
+    if (tid == 0 && stats) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_LOCAL_PAIRS), s_local);
+      atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_REMOTE_PAIRS), s_remote);
+    }
+    __syncthreads();
+  }
+}
+
+int launch_gate(const LocalRows& lr, const ShardPtrs& hs, int64_t d, const void* w_gate,
+                const float* b_gate, int32_t N, int32_t k, int32_t renorm,
+                const int32_t* slot_owner, const ShardPtrs& topk_ids, const ShardPtrs& topk_w,
+                int64_t* stats, int64_t n_rows_bound, cudaStream_t st) {
+  if (N < 1 || N > kGateMaxN || k < 1 || k > kGateMaxK || k > N || d % 2) return SMOE_ERR_UNSUPPORTED;
+  if (n_rows_bound <= 0) return SMOE_OK;
+  gate_kernel<<<grid_cap(ceil_div(n_rows_bound, kGateRows), 4), 256, 0, st>>>(
+      lr, hs, d, static_cast<const uint32_t*>(w_gate), b_gate, N, k, renorm, slot_owner,
+      topk_ids, topk_w, stats);
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
+// ------------------------------------------------------------------ K5a route
+constexpr int kRouteThreads = 1024;
+
+__global__ void __launch_bounds__(kRouteThreads)
+route_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids, ShardPtrs pair_rank,
+             ShardPtrs count_bufs, int32_t n_count_bufs) {
+  __shared__ int32_t s_run[kGateMaxN];
+  __shared__ int32_t s_w[32 * kGateMaxN];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gl = blockIdx.x;
+  const int64_t g = lr.shard_begin + gl;
+  const int64_t P = (int64_t)lr.counts[g] * k;
+  const int32_t* ids = reinterpret_cast<const int32_t*>(topk_ids.p[gl]);
+  int32_t* rank = reinterpret_cast<int32_t*>(pair_rank.p[gl]);
+  for (int e = tid; e < N; e += kRouteThreads) s_run[e] = 0;
+  for (int e = tid; e < 32 * N; e += kRouteThreads) s_w[e] = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < P; base += kRouteThreads) {
+    const int64_t p = base + tid;
+    const int32_t e = p < P ? ids[p] : -1;
+    const uint32_t peers = __match_any_sync(0xffffffffu, e);
+    const int32_t rw = __popc(peers & lanemask_lt());
+    if (e >= 0 && lane == __ffs(peers) - 1) s_w[warp * N + e] = __popc(peers);
+    __syncthreads();
+    if (e >= 0) {
+      int32_t r = s_run[e] + rw;
+      for (int w = 0; w < warp; ++w) r += s_w[w * N + e];
+      rank[p] = r;
+    }
+    __syncthreads();
+    for (int ee = tid; ee < N; ee += kRouteThreads) {
+      int32_t s = 0;
+      for (int w = 0; w < 32; ++w) { s += s_w[w * N + ee]; s_w[w * N + ee] = 0; }
+      s_run[ee] += s;
+    }
+    __syncthreads();
+  }
+  // publish row g of the [G, N] count matrix to every process's copy
+  for (int e = tid; e < N * n_count_bufs; e += kRouteThreads) {
+    const int b = e / N, ee = e - b * N;
+    reinterpret_cast<int32_t*>(count_bufs.p[b])[g * N + ee] = s_run[ee];
+  }
+}
+
+int launch_route(const LocalRows& lr, int32_t N, int32_t k, const ShardPtrs& topk_ids,
+                 const ShardPtrs& pair_rank, const ShardPtrs& count_bufs, int32_t n_count_bufs,
+                 cudaStream_t st) {
+  if (N > kGateMaxN) return SMOE_ERR_UNSUPPORTED;
+  route_kernel<<<lr.shard_count, kRouteThreads, 0, st>>>(lr, N, k, topk_ids, pair_rank,
+                                                        count_bufs, n_count_bufs);
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
+// ------------------------------------------------------------------ K5b dispatch
+__global__ void __launch_bounds__(256)
+dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __restrict__ C,
+                const int32_t* __restrict__ slot_owner, const int32_t* __restrict__ slot_first,
+                ShardPtrs hs, ShardPtrs topk_ids, ShardPtrs pair_rank, ShardPtrs xin,
+                ShardPtrs xmeta, int64_t expert_rows, int64_t* problems, int32_t* err) {
+  __shared__ RowMap rm;
+  __shared__ int32_t s_M[kGateMaxN];
+  __shared__ int32_t s_seg[kGateMaxN];
+  __shared__ int32_t s_off[SMOE_MAX_SHARDS * kGateMaxN];
+  const int G = lr.n_shards;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int e = tid; e < N; e += blockDim.x) {
+    int32_t m = 0;
+    for (int s = 0; s < G; ++s) m += C[s * N + e];
+    s_M[e] = m;
+  }
+  load_rowmap(rm, lr);    // contains __syncthreads
+  for (int e = tid; e < N; e += blockDim.x) {
+    int32_t seg = 0;
+    for (int e2 = slot_first[slot_owner[e]]; e2 < e; ++e2) seg += s_M[e2];
+    s_seg[e] = seg;
+    int32_t run = seg;
+    for (int s = 0; s < G; ++s) { s_off[s * N + e] = run; run += C[s * N + e]; }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    // grouped-GEMM problem table: one problem per expert slot of the resident shards
+    const int32_t e0 = slot_first[lr.shard_begin];
+    const int32_t e1 = slot_first[lr.shard_begin + lr.shard_count];
+    for (int e = e0 + tid; e < e1; e += blockDim.x) {
+      const int32_t o = slot_owner[e];
+      int64_t m = s_M[e];
+      if (s_seg[e] + m > expert_rows) { set_err(err, SMOE_ERRBIT_CAPACITY); m = 0; }
+      const int64_t a_off = (int64_t)(o - lr.shard_begin) * expert_rows + s_seg[e];
+      int64_t* pr = problems + 4 * (e - e0);
+      pr[0] = a_off; pr[1] = m; pr[2] = e - e0; pr[3] = a_off;
+    }
+  }
+  const int64_t vecs = d / 8;
+  const int64_t total_pairs = (int64_t)rm.total * k;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t pq = blockIdx.x * (int64_t)(blockDim.x >> 5) + (tid >> 5); pq < total_pairs;
+       pq += nwarps) {
+    const int64_t q = pq / k;
+    const int32_t s = (int32_t)(pq - q * k);
+    int32_t gl; int64_t j;
+    decode_row(rm, lr.shard_count, q, gl, j);
+    const int32_t g = lr.shard_begin + gl;
+    const int32_t e = reinterpret_cast<const int32_t*>(topk_ids.p[gl])[j * k + s];
+    const int32_t o = slot_owner[e];
+    const int64_t pos =
+        (int64_t)s_off[g * N + e] + reinterpret_cast<const int32_t*>(pair_rank.p[gl])[j * k + s];
+    if (pos >= expert_rows) { if (lane == 0) set_err(err, SMOE_ERRBIT_CAPACITY); continue; }
+    const char* src = hs.p[gl] + j * d * 2;
+    char* dst = xin.p[o] + pos * d * 2;
+    for (int64_t v = lane; v < vecs; v += 32) st_v4(dst + v * 16, ld_nc_v4(src + v * 16));
+    if (lane == 0)
+      reinterpret_cast<int64_t*>(xmeta.p[o])[pos] = ((int64_t)g << 40) | (j * k + s);
+  }
+}
+
+int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
+                    const int32_t* counts_mat, const int32_t* slot_owner,
+                    const int32_t* slot_first, const ShardPtrs& hs, const ShardPtrs& topk_ids,
+                    const ShardPtrs& pair_rank, const ShardPtrs& xin, const ShardPtrs& xmeta,
+                    int64_t expert_rows, int64_t* problems, int32_t* err, int64_t n_rows_bound,
+                    cudaStream_t st) {
+  if (N > kGateMaxN || d % 8) return SMOE_ERR_UNSUPPORTED;
+  const int64_t blocks = std::max<int64_t>(1, ceil_div(n_rows_bound * k, 8));
+  dispatch_kernel<<<grid_cap(blocks, 16), 256, 0, st>>>(lr, N, k, d, counts_mat, slot_owner,
+                                                        slot_first, hs, topk_ids, pair_rank, xin,
+                                                        xmeta, expert_rows, problems, err);
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
+// ------------------------------------------------------------------ K8 combine + SAG
+__global__ void __launch_bounds__(256)
+combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtrs topk_w,
+                   ShardPtrs outs) {
+  __shared__ RowMap rm;
+  load_rowmap(rm, lr);
+  const int lane = threadIdx.x & 31;
+  const int G = lr.n_shards;
+  const int64_t vecs = d / 8;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t q = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); q < rm.total;
+       q += nwarps) {
+    int32_t gl; int64_t j;
+    decode_row(rm, lr.shard_count, q, gl, j);
+    const int64_t g = lr.shard_begin + gl;
+    const int64_t i = lr.forward[g * rm.group + j];    // original token position
+    const float* w = reinterpret_cast<const float*>(topk_w.p[gl]) + j * k;
+    float wk[kGateMaxK];
+#pragma unroll
+    for (int s = 0; s < kGateMaxK; ++s) wk[s] = s < k ? w[s] : 0.f;
+    const char* y = ypair.p[gl] + j * k * d * 2;
+    for (int64_t v = lane; v < vecs; v += 32) {
+      float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int s = 0; s < kGateMaxK; ++s) {
+        if (s < k) {
+          float t[8];
+          set_bf16x8(t, ld_nc_v4(y + ((int64_t)s * d + v * 8) * 2));
+#pragma unroll
+          for (int c = 0; c < 8; ++c) a[c] += wk[s] * t[c];
+        }
+      }
+      const uint4 o = pack_bf16x8(a);
+#pragma unroll
+      for (int r = 0; r < SMOE_MAX_SHARDS; ++r)
+        if (r < G) st_v4(outs.p[r] + (i * d + v * 8) * 2, o);
+    }
+  }
+}
+
+int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtrs& ypair,
+                       const ShardPtrs& topk_w, const ShardPtrs& outs, int64_t n_rows_bound,
+                       cudaStream_t st) {
+  if (k > kGateMaxK || d % 8) return SMOE_ERR_UNSUPPORTED;
+  if (n_rows_bound <= 0) return SMOE_OK;
+  combine_sag_kernel<<<grid_cap(ceil_div(n_rows_bound, 8), 16), 256, 0, st>>>(lr, k, d, ypair,
+                                                                             topk_w, outs);
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
+// ------------------------------------------------------------------ barrier
+__global__ void barrier_kernel(ShardPtrs signals, int32_t world, int32_t rank,
+                               uint32_t* my_signal, uint32_t* epoch) {
+  __shared__ uint32_t s_e;
+  if (threadIdx.x == 0) {
+    s_e = *epoch + 1;
+    *epoch = s_e;
+  }
+  __syncthreads();
+  const uint32_t e = s_e;
+  if ((int)threadIdx.x < world) {
+    __threadfence_system();
+    uint32_t* dst = reinterpret_cast<uint32_t*>(signals.p[threadIdx.x]) + rank;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(dst), "r"(e) : "memory");
+    uint32_t v = 0;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(my_signal + threadIdx.x)
+                   : "memory");
+    } while (v < e);
+  }
+  __syncthreads();
+}
+
+int launch_barrier(const ShardPtrs& signals, int32_t world, int32_t rank, uint32_t* my_signal,
+                   uint32_t* epoch, cudaStream_t st) {
+  if (world <= 1) return SMOE_OK;
+  barrier_kernel<<<1, 32, 0, st>>>(signals, world, rank, my_signal, epoch);
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
+}  // namespace smoe

@@ -1,0 +1,46 @@
+// layer_kernels.cuh — launch interface of the layer stages (K3, K4, K5, K8).
+#pragma once
+#include "common.cuh"
+
+namespace smoe {
+
+struct ShardPtrs {
+  char* p[SMOE_MAX_SHARDS];
+};
+
+struct LocalRows {
+  // local rows are the concatenation, over resident shards g, of the first
+  // counts[g] slots of group g (real tokens only, no pads)
+  const int32_t* counts;     // [G] plan counts
+  const int64_t* group;      // [1] max group
+  const int64_t* forward;    // [G * max_tokens]
+  int32_t shard_begin, shard_count, n_shards;
+};
+
+int launch_srs(const LocalRows& lr, const ShardPtrs& partials, int64_t d, const ShardPtrs& hs,
+               int64_t n_rows_bound, cudaStream_t st);
+
+int launch_gate(const LocalRows& lr, const ShardPtrs& hs, int64_t d, const void* w_gate,
+                const float* b_gate, int32_t N, int32_t k, int32_t renorm,
+                const int32_t* slot_owner, const ShardPtrs& topk_ids, const ShardPtrs& topk_w,
+                int64_t* stats, int64_t n_rows_bound, cudaStream_t st);
+
+int launch_route(const LocalRows& lr, int32_t N, int32_t k, const ShardPtrs& topk_ids,
+                 const ShardPtrs& pair_rank, const ShardPtrs& count_bufs, int32_t n_count_bufs,
+                 cudaStream_t st);
+
+int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
+                    const int32_t* counts_mat, const int32_t* slot_owner,
+                    const int32_t* slot_first, const ShardPtrs& hs, const ShardPtrs& topk_ids,
+                    const ShardPtrs& pair_rank, const ShardPtrs& xin, const ShardPtrs& xmeta,
+                    int64_t expert_rows, int64_t* problems, int32_t* err, int64_t n_rows_bound,
+                    cudaStream_t st);
+
+int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtrs& ypair,
+                       const ShardPtrs& topk_w, const ShardPtrs& outs, int64_t n_rows_bound,
+                       cudaStream_t st);
+
+int launch_barrier(const ShardPtrs& signals, int32_t world, int32_t rank, uint32_t* my_signal,
+                   uint32_t* epoch, cudaStream_t st);
+
+}  // namespace smoe

@@ -1,0 +1,313 @@
+"""The speculative-token-shuffling MoE layer (Algorithm 2).
+
+`SpecMoELayer(bundle, gate_w, w1, w3, w2, ...)` takes the offline solver's
+E/T/S tables (a `LookupBundle`, scheduler.py:24-38) and the expert weights in
+the ORIGINAL expert order, applies the s-EG placement (gate_permutation,
+scheduler.py:200-210) once at construction, and runs the forward:
+
+    plan (lookup + stable partition) -> SRS -> gate/top-k -> route ->
+    A2A dispatch (local pairs stay local) -> SwiGLU grouped GEMM (tcgen05) ->
+    down GEMM whose epilogue writes the A2A combine -> weighted combine + SAG
+
+G shards ("virtual ranks", G = the bundle's cluster count) are resident in
+this process; with a `ShardGroup` (dist.py) they are spread over processes /
+GPUs and the peer buffers are CUDA-IPC mappings.  Every stage is one or two
+kernels of libsmoe.so; there is no CPU fallback.
+
+Data layout in HBM (per shard g unless noted; n = max_tokens, k = top_k):
+    partial[g]  bf16 [n, d]        attention-TP partial sum (input)
+    hs[g]       bf16 [n, d]        SRS output, rows of group g in slot order
+    topk ids/w  i32/f32 [n, k]     s-EG expert slot and combine weight
+    xin[g]      bf16 [R, d]        expert-major input rows (R = expert_rows)
+    hmid        bf16 [L*R, f]      SwiGLU activations (L resident shards)
+    ypair[g]    bf16 [n*k, d]      expert output per (token, k-slot)
+    out[g]      bf16 [n, d]        layer output in original token order
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _dev, _native
+from .scheduler import LookupBundle, SchedulerError, device_tables, gate_permutation
+
+N = _native
+
+
+class SpecMoELayer:
+    def __init__(self, bundle, gate_w, w1, w3, w2, *, top_k: int, max_tokens: int,
+                 gate_b=None, renormalize: bool = True, expert_rows: int | None = None,
+                 group=None):
+        t = _dev.torch()
+        self.lib = N.lib()
+        self.bundle = bundle
+        self.G = int(bundle.token_table.n_clusters)
+        if self.G > N.MAX_SHARDS:
+            raise SchedulerError(f"{self.G} shards exceed the supported {N.MAX_SHARDS}")
+        gate_w = _dev.to_device(gate_w, t.bfloat16)
+        self.N, self.d = int(gate_w.shape[0]), int(gate_w.shape[1])
+        self.f = int(w1.shape[1])
+        self.k = int(top_k)
+        self.max_tokens = int(max_tokens)
+        self.expert_rows = int(expert_rows or self.max_tokens * self.k)
+        self.renormalize = bool(renormalize)
+        labels = np.asarray(bundle.expert_labels, dtype=np.int64)
+        if len(labels) != self.N:
+            raise SchedulerError("expert labels do not match the gate width")
+        self.group = group
+        world = group.world_size if group else 1
+        rank = group.rank if group else 0
+        if self.G % world:
+            raise SchedulerError("shards must divide evenly over processes")
+        spp = self.G // world
+        self.shard_begin, self.shard_count = rank * spp, spp
+        self.world, self.rank = world, rank
+
+        # ---- s-EG placement (scheduler.py:200-224), computed on the GPU
+        self.perm = gate_permutation(labels, self.G)
+        n2o = np.asarray(self.perm.new_to_old)
+        self.slot_owner = labels[n2o].astype(np.int32)          # cluster of each slot
+        first = np.searchsorted(self.slot_owner, np.arange(self.G + 1), side="left")
+        self.slot_first = first.astype(np.int64)
+        e0 = int(first[self.shard_begin])
+        e1 = int(first[self.shard_begin + self.shard_count])
+        self.local_slots = e1 - e0
+        if self.local_slots > 256:
+            raise SchedulerError("more than 256 resident experts per process")
+        n2o_t = t.as_tensor(n2o, device=gate_w.device)
+        self.w_gate = gate_w.index_select(0, n2o_t).contiguous()
+        self.b_gate = None
+        if gate_b is not None:
+            self.b_gate = _dev.to_device(gate_b, t.float32).index_select(0, n2o_t).contiguous()
+        local_ids = n2o_t[e0:e1]
+        w1l = _dev.to_device(w1, t.bfloat16).index_select(0, local_ids).contiguous()
+        w3l = _dev.to_device(w3, t.bfloat16).index_select(0, local_ids).contiguous()
+        self.w2 = _dev.to_device(w2, t.bfloat16).index_select(0, local_ids).contiguous()
+        self.w13 = t.empty((max(self.local_slots, 1), 2 * self.f, self.d), dtype=t.bfloat16,
+                           device=gate_w.device)
+        if self.local_slots:
+            N.check(self.lib.smoe_pack_w13(N.ptr(w1l), N.ptr(w3l), self.local_slots, self.f,
+                                           self.d, N.ptr(self.w13), N.stream_ptr()), "pack_w13")
+        del w1l, w3l
+
+        self.tables = device_tables(bundle)
+        self._alloc_buffers()
+        self._create_handle()
+
+    # ------------------------------------------------------------ buffers
+    def _alloc_buffers(self):
+        t = _dev.torch()
+        dev = self.w_gate.device
+        G, L, n, d, k, f, R = (self.G, self.shard_count, self.max_tokens, self.d, self.k,
+                               self.f, self.expert_rows)
+        bf = t.bfloat16
+        if self.group is None:
+            self.partial = t.zeros((G, n, d), dtype=bf, device=dev)
+            self.xin = t.empty((G, R, d), dtype=bf, device=dev)
+            self.xmeta = t.empty((G, R), dtype=t.int64, device=dev)
+            self.ypair = t.empty((G, n * k, d), dtype=bf, device=dev)
+            self.out = t.empty((G, n, d), dtype=bf, device=dev)
+            self.counts_mat = t.zeros((G, self.N), dtype=t.int32, device=dev)
+            peer = {"partial": [self.partial[g] for g in range(G)],
+                    "xin": [self.xin[g] for g in range(G)],
+                    "xmeta": [self.xmeta[g] for g in range(G)],
+                    "ypair": [self.ypair[g] for g in range(G)],
+                    "out": [self.out[g] for g in range(G)],
+                    "counts": [self.counts_mat] * G,
+                    "signal": [None] * G}
+        else:
+            peer = self.group.alloc_layer_buffers(self, dev)
+            self.partial = peer["partial_local"]
+            self.out = peer["out_local"]
+            self.counts_mat = peer["counts_local"]
+        self._peer = peer
+        self.hs = t.empty((L, n, d), dtype=bf, device=dev)
+        self.topk_ids = t.empty((L, n, k), dtype=t.int32, device=dev)
+        self.topk_w = t.empty((L, n, k), dtype=t.float32, device=dev)
+        self.pair_rank = t.empty((L, n, k), dtype=t.int32, device=dev)
+        self.hmid = t.empty((L * R, f), dtype=bf, device=dev)
+        self.forward_buf = t.empty(G * n, dtype=t.int64, device=dev)
+        self.inverse = t.empty(n, dtype=t.int64, device=dev)
+        self.dev = t.empty(n, dtype=t.int64, device=dev)
+        self.plan_counts = t.zeros(G, dtype=t.int32, device=dev)
+        self.group_t = t.zeros(1, dtype=t.int64, device=dev)
+        self.stats_t = t.zeros(N.STAT_COUNT, dtype=t.int64, device=dev)
+        self.err = t.zeros(1, dtype=t.int32, device=dev)
+        self.problems = t.zeros((256, 4), dtype=t.int64, device=dev)
+        self.epoch = t.zeros(1, dtype=t.int32, device=dev)
+
+    def _create_handle(self):
+        cfg = N.LayerConfig(n_shards=self.G, shard_begin=self.shard_begin,
+                            shard_count=self.shard_count, n_experts=self.N, top_k=self.k,
+                            hidden=self.d, ffn=self.f, renormalize=int(self.renormalize),
+                            max_tokens=self.max_tokens, expert_rows=self.expert_rows,
+                            world_size=self.world, world_rank=self.rank)
+        import ctypes as C
+        self._cfg = cfg
+        ws_bytes = int(self.lib.smoe_layer_workspace_bytes(C.byref(cfg)))
+        t = _dev.torch()
+        self.workspace = t.empty(max(ws_bytes, 256), dtype=t.uint8, device=self.w_gate.device)
+        h = C.c_void_p()
+        N.check(self.lib.smoe_layer_create(C.byref(cfg), C.byref(h)), "layer_create")
+        self._h = h
+        bind = lambda slot, i, x: N.check(  # noqa: E731
+            self.lib.smoe_layer_bind(h, slot, i, 0 if x is None else N.ptr(x) if
+                                     hasattr(x, "data_ptr") else int(x)), "layer_bind")
+        p = self._peer
+        for g in range(self.G):
+            bind(N.BUF_PARTIAL, g, p["partial"][g])
+            bind(N.BUF_XIN, g, p["xin"][g])
+            bind(N.BUF_XMETA, g, p["xmeta"][g])
+            bind(N.BUF_YPAIR, g, p["ypair"][g])
+            bind(N.BUF_OUT, g, p["out"][g])
+            bind(N.BUF_COUNTS, g, p["counts"][g])
+            if p["signal"][g] is not None:
+                bind(N.BUF_SIGNAL, g, p["signal"][g])
+        for i in range(self.shard_count):
+            bind(N.BUF_HS, i, self.hs[i])
+            bind(N.BUF_TOPK_IDS, i, self.topk_ids[i])
+            bind(N.BUF_TOPK_W, i, self.topk_w[i])
+            bind(N.BUF_PAIR_RANK, i, self.pair_rank[i])
+        for slot, x in ((N.BUF_HMID, self.hmid), (N.BUF_FORWARD, self.forward_buf),
+                        (N.BUF_INVERSE, self.inverse), (N.BUF_DEV, self.dev),
+                        (N.BUF_PLAN_COUNTS, self.plan_counts), (N.BUF_GROUP, self.group_t),
+                        (N.BUF_STATS, self.stats_t), (N.BUF_ERR, self.err),
+                        (N.BUF_WORKSPACE, self.workspace), (N.BUF_PROBLEMS, self.problems),
+                        (N.BUF_EPOCH, self.epoch)):
+            bind(slot, 0, x)
+        tb = self.tables
+        owner = (C.c_int32 * self.N)(*[int(x) for x in self.slot_owner])
+        N.check(self.lib.smoe_layer_set_tables(
+            h, N.ptr(tb.t_labels), N.ptr(tb.t_conf), tb.vocab, N.ptr(tb.a_best), N.ptr(tb.a_conf),
+            tb.a_rows, tb.ngram_n, owner), "layer_set_tables")
+        N.check(self.lib.smoe_layer_set_weights(h, N.ptr(self.w_gate), N.ptr(self.b_gate),
+                                                N.ptr(self.w13), N.ptr(self.w2)),
+                "layer_set_weights")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self.lib.smoe_layer_destroy(h)
+            except Exception:
+                pass
+
+    # ------------------------------------------------------------ forward
+    def partial_views(self, n: int):
+        """[L, n, d] views of the resident shards' partial-input buffers
+        (write the attention-TP partials here to avoid a copy)."""
+        if self.group is None:
+            return self.partial[:, :n]
+        return self.partial[:, :n]
+
+    def run_device(self, tokens_t, hist_t=None, stream=None, stages=None):
+        """Run the layer on device-resident inputs already in the partial
+        buffers; no host synchronisation (graph-capturable)."""
+        n = int(tokens_t.shape[0])
+        if n > self.max_tokens:
+            raise SchedulerError(f"{n} tokens exceed max_tokens={self.max_tokens}")
+        if hist_t is not None and hist_t.shape[1] != self.tables.ngram_n:
+            pass  # like the vectorised reference, any history width is accepted
+        sp = N.stream_ptr(stream)
+        hp = N.ptr(hist_t)
+        if stages is None:
+            N.check(self.lib.smoe_layer_forward(self._h, N.ptr(tokens_t), hp, n, sp),
+                    "layer_forward")
+        else:
+            for s in stages:
+                N.check(self.lib.smoe_layer_stage(self._h, s, N.ptr(tokens_t), hp, n, sp),
+                        f"layer stage {N.STAGE_NAMES[s]}")
+        return self.out_view(n)
+
+    def out_view(self, n: int, shard: int | None = None):
+        g = self.shard_begin if shard is None else shard
+        if self.group is None:
+            return self.out[g, :n]
+        return self.out[g - self.shard_begin, :n]
+
+    def forward(self, hidden_partials, token_ids, histories=None):
+        """Full layer from user tensors (host or device).
+
+        hidden_partials: [L, n, d] (one partial per resident shard) or [n, d]
+        when there is a single shard; token_ids int [n]; histories int [n, h].
+        Returns the layer output [n, d] (bf16) in the original token order,
+        on the device for torch inputs, as a host tensor otherwise.
+        """
+        t = _dev.torch()
+        host = not (isinstance(hidden_partials, t.Tensor) and hidden_partials.is_cuda)
+        tok = _dev.to_device(token_ids, t.int64).reshape(-1)
+        n = int(tok.numel())
+        hp = hidden_partials if isinstance(hidden_partials, t.Tensor) else t.as_tensor(
+            np.asarray(hidden_partials))
+        if hp.dim() == 2:
+            hp = hp.unsqueeze(0)
+        if hp.shape[0] != self.shard_count or hp.shape[1] != n or hp.shape[2] != self.d:
+            raise SchedulerError(f"partials must be [{self.shard_count}, {n}, {self.d}]")
+        self.partial_views(n).copy_(hp.to(t.bfloat16), non_blocking=True)
+        hist = None if histories is None else _dev.to_device(histories, t.int64)
+        out = self.run_device(tok, hist)
+        self.check_errors()
+        return out.cpu() if host else out
+
+    # ------------------------------------------------------------ results
+    def check_errors(self):
+        bits = int(self.err.item())
+        if bits & N.ERRBIT_CAPACITY:
+            raise SchedulerError("expert_rows capacity exceeded; raise expert_rows")
+        if bits & N.ERRBIT_DEVICE_RANGE:
+            raise SchedulerError("device label out of range")
+        if bits & (N.ERRBIT_TOKEN_RANGE | N.ERRBIT_HISTORY_RANGE):
+            raise IndexError("token id or history out of range")
+
+    def plan_indices(self, n: int):
+        """The ShuffleIndices of the last forward (bit-exact with
+        scheduler.rebatch_tokens on the looked-up devices)."""
+        from .scheduler import ShuffleIndices
+        group = int(self.group_t.item())
+        return ShuffleIndices(forward=self.forward_buf[: self.G * group].cpu().numpy(),
+                              inverse=self.inverse[:n].cpu().numpy(), group_size=group,
+                              n_devices=self.G)
+
+    def routing(self, n: int):
+        """Per original token: expert slots (s-EG order), ORIGINAL expert ids
+        and weights, gathered from the shards' top-k buffers."""
+        counts = self.plan_counts.cpu().numpy()
+        group = int(self.group_t.item())
+        fwd = self.forward_buf[: self.G * group].cpu().numpy()
+        slots = np.full((n, self.k), -1, dtype=np.int64)
+        wts = np.zeros((n, self.k), dtype=np.float32)
+        ids = self.topk_ids.cpu().numpy()
+        ws = self.topk_w.cpu().numpy()
+        for i in range(self.shard_count):
+            g = self.shard_begin + i
+            c = int(counts[g])
+            pos = fwd[g * group: g * group + c]
+            slots[pos] = ids[i, :c]
+            wts[pos] = ws[i, :c]
+        experts = np.where(slots >= 0, np.asarray(self.perm.new_to_old)[np.maximum(slots, 0)], -1)
+        return {"slots": slots, "experts": experts, "weights": wts}
+
+    def stats(self, n: int | None = None) -> dict:
+        """Locality and traffic of the last forward (mirrors the keys of
+        comm.simulate_layer, comm.py:223-227, plus per-stage bytes)."""
+        s = self.stats_t.cpu().numpy()
+        local, remote = int(s[N.STAT_LOCAL_PAIRS]), int(s[N.STAT_REMOTE_PAIRS])
+        counts = self.plan_counts.cpu().numpy().astype(np.int64)
+        cm = self.counts_mat.cpu().numpy().astype(np.int64)
+        group = int(self.group_t.item())
+        n = int(counts.sum()) if n is None else n
+        row = 2 * self.d
+        G = self.G
+        srs_bytes = int(counts.sum()) * (G - 1) * row      # rows pulled from other shards
+        sag_bytes = int(counts.sum()) * (G - 1) * row      # rows pushed to other shards
+        a2a = remote * row
+        return {
+            "local_tokens": local, "remote_tokens": remote,
+            "measured_alpha": local / max(local + remote, 1),
+            "group_size": group, "device_counts": counts.tolist(),
+            "pair_counts": cm.tolist(),
+            "bytes": {"srs": srs_bytes, "a2a_dispatch": a2a, "a2a_combine": a2a,
+                      "sag": sag_bytes,
+                      "srs_padded_model": G * group * (G - 1) * row,
+                      "reference_model_a2a": a2a},
+        }

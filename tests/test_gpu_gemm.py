@@ -1,0 +1,75 @@
+"""tcgen05 grouped GEMM (K6) against a torch fp32 reference of the same op."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2503_04398_b200 import _native as N
+
+
+def run_gemm(A, B, problems, n_b, epilogue, c_cols):
+    lib = N.lib()
+    C = torch.zeros((A.shape[0], c_cols), dtype=torch.bfloat16, device="cuda")
+    pt = torch.as_tensor(np.asarray(problems, dtype=np.int64), device="cuda")
+    N.check(lib.smoe_grouped_gemm(N.ptr(A), A.shape[0], A.shape[1], N.ptr(B), B.shape[0], n_b,
+                                  N.ptr(pt), len(problems), epilogue, N.ptr(C), C.shape[0],
+                                  c_cols, N.stream_ptr()), "grouped_gemm")
+    torch.cuda.synchronize()
+    return C
+
+
+def rel(a, b):
+    return (a.float() - b.float()).norm().item() / max(b.float().norm().item(), 1e-30)
+
+
+@pytest.mark.parametrize("M,K,NB", [(128, 64, 256), (128, 256, 256), (300, 512, 512),
+                                    (1000, 1024, 768)])
+def test_single_problem_store(M, K, NB):
+    torch.manual_seed(M + K)
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    B = torch.randn(NB, K, device="cuda").to(torch.bfloat16)
+    C = run_gemm(A, B, [[0, M, 0, 0]], NB, 0, NB)
+    ref = A.float() @ B.float().T
+    assert rel(C, ref) < 1e-2
+
+
+def test_grouped_ragged_store():
+    torch.manual_seed(1)
+    K, NB, E = 512, 256, 5
+    ms = [0, 1, 129, 256, 77]
+    offs = np.concatenate([[0], np.cumsum(ms)])[:-1]
+    A = torch.randn(int(sum(ms)) + 16, K, device="cuda").to(torch.bfloat16)
+    B = torch.randn(E * NB, K, device="cuda").to(torch.bfloat16)
+    probs = [[int(offs[e]), ms[e], e, int(offs[e])] for e in range(E)]
+    C = run_gemm(A, B, probs, NB, 0, NB)
+    for e in range(E):
+        if ms[e] == 0:
+            continue
+        a = A[offs[e]:offs[e] + ms[e]].float()
+        ref = a @ B[e * NB:(e + 1) * NB].float().T
+        assert rel(C[offs[e]:offs[e] + ms[e]], ref) < 1e-2, e
+    # rows not owned by any problem stay untouched
+    assert torch.count_nonzero(C[int(sum(ms)):]) == 0
+
+
+def test_swiglu_epilogue():
+    torch.manual_seed(2)
+    E, f, d = 3, 256, 512
+    ms = [200, 64, 333]
+    offs = np.concatenate([[0], np.cumsum(ms)])[:-1]
+    X = (torch.randn(int(sum(ms)), d, device="cuda") / 4).to(torch.bfloat16)
+    w1 = (torch.randn(E, f, d, device="cuda") / d ** 0.5).to(torch.bfloat16)
+    w3 = (torch.randn(E, f, d, device="cuda") / d ** 0.5).to(torch.bfloat16)
+    w13 = torch.empty(E, 2 * f, d, dtype=torch.bfloat16, device="cuda")
+    lib = N.lib()
+    N.check(lib.smoe_pack_w13(N.ptr(w1), N.ptr(w3), E, f, d, N.ptr(w13), N.stream_ptr()), "pack")
+    probs = [[int(offs[e]), ms[e], e, int(offs[e])] for e in range(E)]
+    H = run_gemm(X, w13.view(E * 2 * f, d), probs, 2 * f, 1, f)
+    for e in range(E):
+        x = X[offs[e]:offs[e] + ms[e]].float()
+        g = x @ w1[e].float().T
+        u = x @ w3[e].float().T
+        ref = torch.nn.functional.silu(g) * u
+        assert rel(H[offs[e]:offs[e] + ms[e]], ref) < 1e-2, e

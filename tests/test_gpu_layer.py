@@ -1,0 +1,87 @@
+"""Whole-layer parity: GPU SpecMoELayer vs the fp32 CPU oracle.
+
+Bit-exact: plan (forward/inverse/group/counts), routing (ordered top-k
+original expert ids), local/remote event counts, the SRS rows.
+Tolerance: layer output, relative Frobenius error <= 1e-2 (north_star)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import layer_ref
+from paper_2503_04398_b200 import SpecMoELayer, synth
+
+TOL = 1e-2
+
+
+def oracle_for(w):
+    b = w.bundle
+    return layer_ref.layer_forward(
+        partials=w.partials, tokens=w.tokens, hist=w.hist, t_labels=b.token_table.labels,
+        t_conf=b.token_table.confidence, a_best=b.ngram_table.best,
+        a_conf=b.ngram_table.confidence, n_clusters=w.cfg["G"], expert_labels=w.expert_labels,
+        gate_w=w.gate_w, w1=w.w1, w3=w.w3, w2=w.w2, k=w.cfg["k"])
+
+
+CASES = [
+    ("toy", 384, 0.2, {}),
+    ("toy", 1, 0.0, {}),
+    ("toy", 1000, 0.5, {"G": 8, "N": 16}),
+    ("toy", 700, 0.3, {"G": 8, "N": 64, "k": 6, "d": 512, "f": 256}),
+    ("toy", 500, 0.1, {"G": 4, "N": 64, "k": 8, "d": 256, "f": 384}),
+    ("toy", 300, 0.1, {"G": 1, "N": 8, "k": 2}),
+    ("toy", 512, 0.2, {"G": 8, "N": 8, "k": 1, "d": 4096, "f": 512}),
+]
+
+
+@pytest.mark.parametrize("name,n,eps,over", CASES)
+def test_layer_matches_oracle(name, n, eps, over):
+    w = synth.make_workload(name, n=n, eps=eps, seed=n, cfg_override=over)
+    G = w.cfg["G"]
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=w.cfg["k"],
+                         max_tokens=n + 7)
+    out = layer.forward(torch.from_numpy(w.partials), w.tokens, w.hist).float().numpy()
+    ref = oracle_for(w)
+    ix = layer.plan_indices(n)
+    assert ix.group_size == ref["group"]
+    assert np.array_equal(ix.forward, ref["forward"])
+    assert np.array_equal(ix.inverse, ref["inverse"])
+    assert np.array_equal(layer.plan_counts.cpu().numpy(), ref["counts"])
+    # SRS rows are bit-exact (fixed fp32 summation order, RNE to bf16)
+    hs = layer.hs.float().cpu().numpy()
+    for g in range(G):
+        c = int(ref["counts"][g])
+        assert np.array_equal(hs[g, :c], ref["h"][ref["forward"][g * ref["group"]:g * ref["group"] + c]])
+    r = layer.routing(n)
+    assert np.array_equal(r["experts"], ref["experts"])
+    assert np.allclose(r["weights"], ref["weights"], rtol=1e-4, atol=1e-6)
+    st = layer.stats()
+    assert st["local_tokens"] == ref["local"] and st["remote_tokens"] == ref["remote"]
+    err = np.linalg.norm(out - ref["out"]) / np.linalg.norm(ref["out"])
+    assert err <= TOL, err
+    # every shard's SAG copy is identical
+    for g in range(G):
+        assert torch.equal(layer.out[g, :n], layer.out[0, :n])
+
+
+def test_layer_repeatable_and_graph_capturable():
+    w = synth.make_workload("toy", n=256, eps=0.2, seed=5, cfg_override={"G": 4, "N": 16})
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=256)
+    tok = torch.as_tensor(w.tokens, device="cuda")
+    hist = torch.as_tensor(w.hist, device="cuda")
+    layer.partial_views(256).copy_(torch.from_numpy(w.partials).to(torch.bfloat16))
+    a = layer.run_device(tok, hist).clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        layer.run_device(tok, hist)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        layer.run_device(tok, hist)
+    layer.out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(layer.out_view(256), a)
