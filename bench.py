@@ -1,0 +1,379 @@
+"""MoE-layer tokens/sec of the speculative-token-shuffling layer on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl smoe|reference]
+                    [--config mixtral] [--tokens 16384] [--eps 0.2]
+
+A step is one MoE-layer forward (Algorithm 2: lookup/plan -> SRS -> gate ->
+A2A dispatch -> SwiGLU grouped GEMM -> down GEMM + A2A combine -> combine +
+SAG) over one batch of synthetic tokens.  The workload is BASELINE.json
+configs[1] (Mixtral-8x7B layer, 8 experts, top-2, hidden 4096, EP=8): the 8
+EP shards are spread over the N GPUs (all 8 on one GPU at N=1, peer buffers
+over CUDA IPC / NVLink at N>1), tokens_per_gpu fixed -> weak scaling.
+
+value   = tokens processed by all GPUs / device time (inputs resident in HBM)
+e2e     = same metric through SpecMoELayer.forward() with pinned HOST inputs:
+          H2D of the partials + ids every step, D2H of the layer output
+roofline: the SwiGLU expert GEMM (dominant kernel), CUDA-event timed in the
+          timed region, vs the measured bf16 peak in MEASURED_PEAKS.json
+cpu_baseline: the CPU oracle port (oracle/layer_ref) on a bounded sample of the
+          same workload, on this host's cores
+`--impl reference` times that CPU path alone (the reference is pure Python and
+ships no layer; its arithmetic is restated in oracle/).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="smoe", choices=["smoe", "reference"])
+    p.add_argument("--config", default="mixtral")
+    p.add_argument("--tokens", type=int, default=16384, help="tokens per GPU per step")
+    p.add_argument("--eps", type=float, default=0.2, help="planted routing noise")
+    p.add_argument("--ep", type=int, default=0, help="EP shards (default: config's 8)")
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU baseline work")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return {"hbm": d.get("hbm_gbs", 6650.0), "bf16": d.get("bf16_tflops", 1590.0),
+                "bf16_sustained": d.get("bf16_tflops_sustained", 1400.0), "src": "measured"}
+    return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0, "src": "fallback"}
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = ROOT / "gpurun_out" / f"clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.path.parent.mkdir(exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in self.path.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[3:7]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        load = [r for r in rows if r[2] > 250.0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in load for i, v in enumerate(r[3]) if v == "Active"})
+        return {"sm_mhz": float(np.median([r[0] for r in load])), "sm_max_mhz": rows[0][1],
+                "reasons": reasons, "samples": len(load)}
+
+
+def cpu_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return int(max(n)) if n else (os.cpu_count() or 1)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_sample(bundle, partials, tokens, hist, gate_w, w1, w3, w2, k, budget, n_max):
+    """Time the CPU oracle (oracle/layer_ref) on the first n_s tokens, n_s
+    calibrated so one call costs about `budget` seconds."""
+    from oracle import layer_ref
+    tab = bundle
+
+    def run(ns):
+        t0 = time.perf_counter()
+        layer_ref.layer_forward(partials=partials[:, :ns], tokens=tokens[:ns], hist=hist[:ns],
+                                t_labels=tab.token_table.labels,
+                                t_conf=tab.token_table.confidence, a_best=tab.ngram_table.best,
+                                a_conf=tab.ngram_table.confidence,
+                                n_clusters=tab.token_table.n_clusters,
+                                expert_labels=np.asarray(tab.expert_labels), gate_w=gate_w,
+                                w1=w1, w3=w3, w2=w2, k=k)
+        return time.perf_counter() - t0
+
+    ns = min(64, n_max)
+    t = run(ns)
+    ns2 = int(min(n_max, max(ns, ns * budget / max(t, 1e-3))))
+    if ns2 > ns:
+        t = run(ns2)
+        ns = ns2
+    return ns, t
+
+
+def host_copy_weights(w):
+    import torch
+    f = lambda x: x.float().cpu().numpy() if isinstance(x, torch.Tensor) else x  # noqa: E731
+    return f(w.gate_w), f(w.w1), f(w.w3), f(w.w2)
+
+
+def emit(line: dict):
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args, world, rank):
+    """CPU path of the reference, restated (oracle port): bounded sample per step."""
+    if rank != 0:
+        return
+    import torch
+    from paper_2503_04398_b200 import synth
+    torch.set_num_threads(os.cpu_count() or 1)
+    cfg = dict(synth.CONFIGS[args.config])
+    if args.ep:
+        cfg["G"] = args.ep
+    # generate a small sample of the same workload on the host (same generator)
+    steps = args.steps + args.warmup
+    per_step_budget = max(2.0, min(args.cpu_budget, 150.0 / max(steps, 1)))
+    w = synth.make_workload(args.config, n=256, eps=args.eps, seed=args.seed, device=False,
+                            cfg_override=cfg) if cfg["d"] * cfg["f"] * cfg["N"] < 2e9 else None
+    if w is None:
+        # big configs: numpy weight generation is slow; use torch's CPU RNG for the weights
+        w = _host_workload_torch(args, cfg)
+    gw, w1, w3, w2 = w.gate_w, w.w1, w.w3, w.w2
+    ns, _ = oracle_sample(w.bundle, w.partials, w.tokens, w.hist, gw, w1, w3, w2, cfg["k"],
+                          per_step_budget, len(w.tokens))
+    from oracle import layer_ref  # noqa: F401
+    times = []
+    for i in range(steps):
+        _, t = oracle_sample(w.bundle, w.partials, w.tokens, w.hist, gw, w1, w3, w2, cfg["k"],
+                             0.0, ns)
+        if i >= args.warmup:
+            times.append(t)
+    total = sum(times)
+    value = ns * len(times) / total
+    cores = cpu_threads()
+    emit({"impl": "reference", "metric": "moe_layer_tokens_per_sec", "value": value,
+          "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+          "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+          "vs_baseline": None, "dtype": "f32", "data": "synthetic (planted skew, host RNG)",
+          "config": {"workload": f"{args.config} MoE layer, EP={cfg['G']} shards, top-{cfg['k']}, "
+                                 f"hidden {cfg['d']}, CPU sample {ns} tokens/step",
+                     "tokens_per_step": ns, "eps": args.eps},
+          "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
+                           "sample": f"{ns} tokens of the {args.config} workload per step "
+                                     f"(oracle/layer_ref: lookup, plan, SRS over {cfg['G']} "
+                                     f"partials, fp32 gate, SwiGLU experts, combine)"},
+          "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                  "d2h_bytes_per_step": 0}})
+
+
+def _host_workload_torch(args, cfg):
+    import torch
+    from paper_2503_04398_b200 import synth
+    small = dict(cfg)
+    small["f"] = 128
+    w = synth.make_workload(args.config, n=256, eps=args.eps, seed=args.seed, device=False,
+                            cfg_override=small)
+    g = torch.Generator().manual_seed(args.seed)
+    N, f, d = cfg["N"], cfg["f"], cfg["d"]
+    bf = lambda x: x.to(torch.bfloat16).float().numpy()  # noqa: E731
+    w.w1 = bf(torch.randn((N, f, d), generator=g) / d ** 0.5)
+    w.w3 = bf(torch.randn((N, f, d), generator=g) / d ** 0.5)
+    w.w2 = bf(torch.randn((N, d, f), generator=g) / f ** 0.5)
+    w.cfg = cfg
+    return w
+
+
+# --------------------------------------------------------------------------- smoe arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    torch.cuda.set_device(local_rank)
+    from paper_2503_04398_b200 import SpecMoELayer, synth
+    from paper_2503_04398_b200 import _native as N
+
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        from paper_2503_04398_b200.dist import ShardGroup
+        group = ShardGroup.from_torch_distributed()
+
+    cfg = dict(synth.CONFIGS[args.config])
+    if args.ep:
+        cfg["G"] = args.ep
+    G, k, d, f = cfg["G"], cfg["k"], cfg["d"], cfg["f"]
+    n = args.tokens * world                      # weak scaling: tokens per GPU fixed
+    w = synth.make_workload(args.config, n=n, eps=args.eps, seed=args.seed, device=True,
+                            cfg_override=cfg)
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=k, max_tokens=n,
+                         group=group)
+    L = layer.shard_count
+    layer.partial_views(n).copy_(w.partials[layer.shard_begin:layer.shard_begin + L])
+    tok = torch.as_tensor(w.tokens, device="cuda")
+    hist = torch.as_tensor(w.hist, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # ---------------- device-resident timed region (value + roofline)
+    for _ in range(args.warmup):
+        layer.run_device(tok, hist)
+    torch.cuda.synchronize()
+    layer.check_errors()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pre = [N.STAGE_PLAN, N.STAGE_SRS, N.STAGE_GATE, N.STAGE_ROUTE, N.STAGE_DISPATCH]
+    barrier()
+    torch.cuda.synchronize()
+    with Clocks(local_rank) as clk:
+        start.record(stream)
+        for s in range(args.steps):
+            layer.run_device(tok, hist, stages=pre)
+            ev[s][0].record(stream)
+            layer.run_device(tok, hist, stages=[N.STAGE_EXPERT_UP])
+            ev[s][1].record(stream)
+            layer.run_device(tok, hist, stages=[N.STAGE_EXPERT_DOWN])
+            ev[s][2].record(stream)
+            layer.run_device(tok, hist, stages=[N.STAGE_COMBINE_SAG])
+            ev[s][3].record(stream)
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms_total = start.elapsed_time(end)
+    up_ms = np.mean([ev[s][0].elapsed_time(ev[s][1]) for s in range(args.steps)])
+    down_ms = np.mean([ev[s][1].elapsed_time(ev[s][2]) for s in range(args.steps)])
+    if world > 1:
+        t = torch.tensor([ms_total], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_total = float(t.item())
+    layer.check_errors()
+    st = layer.stats(n)
+    ms_step = ms_total / args.steps
+    value = n * args.steps / (ms_total / 1e3)
+    rows = st["local_tokens"] + st["remote_tokens"]           # (token, expert) pairs
+    local_rows = rows if world == 1 else None
+    pk = peaks()
+    up_flops = 2.0 * rows * d * (2 * f) / world
+    down_flops = 2.0 * rows * f * d / world
+    achieved = up_flops / (up_ms / 1e3) / 1e12
+    clocks = clk.summary()
+
+    # ---------------- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_p = w.partials[layer.shard_begin:layer.shard_begin + L].cpu().pin_memory()
+        host_tok = torch.from_numpy(w.tokens).pin_memory()
+        host_hist = torch.from_numpy(w.hist).pin_memory()
+        out_h = torch.empty((n, d), dtype=torch.bfloat16).pin_memory()
+        for _ in range(2):
+            layer.forward(host_p, host_tok, host_hist, out=out_h)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_start.record(stream)
+        ksteps = max(3, args.steps // 2)
+        for _ in range(ksteps):
+            layer.forward(host_p, host_tok, host_hist, out=out_h)
+        e_end.record(stream)
+        torch.cuda.synchronize()
+        e_ms = max(e_start.elapsed_time(e_end), 1e3 * (time.perf_counter() - t0))
+        if world > 1:
+            t = torch.tensor([e_ms], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e_ms = float(t.item())
+        h2d = host_p.numel() * 2 + host_tok.numel() * 8 + host_hist.numel() * 8
+        e2e = {"value": n * ksteps / (e_ms / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(out_h.numel() * 2),
+               "steps": ksteps, "api": "SpecMoELayer.forward(host pinned partials, ids, hist)"}
+
+    # ---------------- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        gw, w1, w3, w2 = host_copy_weights(w)
+        parts = w.partials.float().cpu().numpy()
+        ns, t = oracle_sample(w.bundle, parts, w.tokens, w.hist, gw, w1, w3, w2, k,
+                              args.cpu_budget, n)
+        cpu = {"value": ns / t, "unit": "tokens/s", "cores": cpu_threads(), "kind": "port",
+               "sample": f"first {ns} tokens of the step's batch through oracle/layer_ref "
+                         f"(lookup, plan, SRS over {G} partials, fp32 gate, SwiGLU, combine)"}
+
+    launches_per_step = 2 + 1 + 1 + 1 + 1 + 2 + 1 + (4 if world > 1 else 0)
+    if rank == 0:
+        emit({"metric": "moe_layer_tokens_per_sec", "value": value, "unit": "tokens/s",
+              "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+              "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+              "vs_baseline": None, "dtype": "bf16", "data": "synthetic (planted skew, seeded)",
+              "config": {"workload": f"{args.config} MoE layer (N={cfg['N']} experts, top-{k}, "
+                                     f"hidden {d}, ffn {f}), EP={G} shards over {world} GPU(s)",
+                         "tokens_per_gpu": args.tokens, "global_tokens": n, "eps": args.eps,
+                         "parallelism": f"ep{G}", "l2": "inputs larger than L2 "
+                         f"({G * n * d * 2 / 2**20:.0f} MiB partials, "
+                         f"{3 * cfg['N'] * d * f * 2 / 2**30:.1f} GiB weights)"},
+              "local_activation_rate": st["measured_alpha"],
+              "a2a_bytes_per_step": st["bytes"]["a2a_dispatch"] + st["bytes"]["a2a_combine"],
+              "stage_bytes": st["bytes"], "group_size": st["group_size"],
+              "stages_ms": {"expert_up": up_ms, "expert_down": down_ms,
+                            "rest": ms_step - up_ms - down_ms},
+              "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel<SwiGLU> (expert up)",
+                           "achieved": achieved, "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
+                           "frac": achieved / pk["bf16_sustained"], "traffic": None,
+                           "peak_src": pk["src"] + " sustained",
+                           "down_gemm_tflops": down_flops / (down_ms / 1e3) / 1e12,
+                           "layer_tflops": (up_flops + down_flops) / (ms_step / 1e3) / 1e12},
+              "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
+              "gpu_launches": launches_per_step * args.steps})
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

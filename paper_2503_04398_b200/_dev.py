@@ -51,13 +51,12 @@ def to_device(x, dtype=None):
         if y.device.type != "cuda":
             y = y.to(device())
         return y.contiguous()
-    a = np.asarray(x)
-    if dtype is None:
-        dtype = _np_to_torch_dtype(a.dtype)
-    elif a.dtype != np.dtype(str(dtype).replace("torch.", "")):
-        a = a.astype(str(dtype).replace("torch.", ""))
-    a = np.ascontiguousarray(a)
-    return t.from_numpy(a).to(device(), non_blocking=False)
+    a = np.ascontiguousarray(np.asarray(x))
+    _np_to_torch_dtype(a.dtype)            # rejects dtypes the device path cannot hold
+    y = t.from_numpy(a).to(device(), non_blocking=False)
+    if dtype is not None and y.dtype != dtype:
+        y = y.to(dtype)
+    return y
 
 
 def to_host_like(y, like):

@@ -168,7 +168,7 @@ static int plan_impl(const LookupTables& t, int use_lookup, const int64_t* token
                      int64_t* forward, int64_t* inverse, int32_t* counts, int64_t* group,
                      int32_t* err, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (G < 1 || G > SMOE_MAX_PLAN_DEVICES) return SMOE_ERR_UNSUPPORTED;
-  if (n < 0 || !forward || !inverse || !counts || !group) return SMOE_ERR_INVALID_ARG;
+  if (n < 0 || !counts || !group || (n > 0 && (!forward || !inverse))) return SMOE_ERR_INVALID_ARG;
   if (ws_bytes < smoe_plan_workspace_bytes(n, G) || (n > 0 && !ws)) return SMOE_ERR_INVALID_ARG;
   if (n == 0) {
     SMOE_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int32_t) * G, st));

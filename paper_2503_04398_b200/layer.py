@@ -225,17 +225,24 @@ class SpecMoELayer:
             return self.out[g, :n]
         return self.out[g - self.shard_begin, :n]
 
-    def forward(self, hidden_partials, token_ids, histories=None):
+    def forward(self, hidden_partials, token_ids, histories=None, out=None):
         """Full layer from user tensors (host or device).
 
         hidden_partials: [L, n, d] (one partial per resident shard) or [n, d]
         when there is a single shard; token_ids int [n]; histories int [n, h].
-        Returns the layer output [n, d] (bf16) in the original token order,
-        on the device for torch inputs, as a host tensor otherwise.
+        Returns the layer output [n, d] (bf16) in the original token order:
+        a device view for CUDA inputs, else a host tensor (`out` if given —
+        pass pinned host tensors for asynchronous copies).
         """
         t = _dev.torch()
         host = not (isinstance(hidden_partials, t.Tensor) and hidden_partials.is_cuda)
-        tok = _dev.to_device(token_ids, t.int64).reshape(-1)
+
+        def dev_i64(x):
+            if isinstance(x, t.Tensor):
+                return x.to(device=self.w_gate.device, dtype=t.int64, non_blocking=True)
+            return _dev.to_device(x, t.int64)
+
+        tok = dev_i64(token_ids).reshape(-1)
         n = int(tok.numel())
         hp = hidden_partials if isinstance(hidden_partials, t.Tensor) else t.as_tensor(
             np.asarray(hidden_partials))
@@ -243,11 +250,21 @@ class SpecMoELayer:
             hp = hp.unsqueeze(0)
         if hp.shape[0] != self.shard_count or hp.shape[1] != n or hp.shape[2] != self.d:
             raise SchedulerError(f"partials must be [{self.shard_count}, {n}, {self.d}]")
-        self.partial_views(n).copy_(hp.to(t.bfloat16), non_blocking=True)
-        hist = None if histories is None else _dev.to_device(histories, t.int64)
-        out = self.run_device(tok, hist)
-        self.check_errors()
-        return out.cpu() if host else out
+        dst = self.partial_views(n)
+        if hp.dtype == t.bfloat16:
+            dst.copy_(hp, non_blocking=True)
+        else:
+            dst.copy_(hp.to(device=dst.device, non_blocking=True).to(t.bfloat16))
+        hist = None if histories is None else dev_i64(histories)
+        res = self.run_device(tok, hist)
+        if not host:
+            self.check_errors()
+            return res
+        if out is None:
+            out = t.empty((n, self.d), dtype=t.bfloat16)
+        out.copy_(res, non_blocking=out.is_pinned())
+        self.check_errors()                 # stream sync: `out` is complete after this
+        return out
 
     # ------------------------------------------------------------ results
     def check_errors(self):

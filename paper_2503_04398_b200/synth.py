@@ -78,8 +78,10 @@ def make_bundle(G: int, N: int, vocab: int, rng: np.random.Generator, hist_len: 
 
 
 def routing_choices(bundle, tokens: np.ndarray, k: int, eps: float, rng) -> np.ndarray:
-    """Per occurrence, k original expert ids: the token's preferred set inside
-    its planted cluster's block w.p. 1-eps, else k of another block."""
+    """Per occurrence, k distinct original expert ids: the token's preferred
+    window inside its planted cluster's block w.p. 1-eps, else a window of
+    another block.  When k exceeds the block size (Mixtral EP8: 1 expert per
+    cluster) the window continues into the following clusters' blocks."""
     labels = np.asarray(bundle.expert_labels, dtype=np.int64)
     G = int(bundle.token_table.n_clusters)
     blocks = [np.nonzero(labels == c)[0] for c in range(G)]
@@ -92,13 +94,18 @@ def routing_choices(bundle, tokens: np.ndarray, k: int, eps: float, rng) -> np.n
     for i in range(n):
         c = int(cl[i])
         if noisy[i] and G > 1:
-            c2 = int(other[i]) + (int(other[i]) >= c)
-            b = blocks[c2]
-            s = int(start[i]) % len(b)
+            c = c + 1 + int(other[i]) % (G - 1)
+            s = int(start[i])
         else:
-            b = blocks[c]
-            s = int(tokens[i]) % len(b)             # fixed preferred window per token
-        out[i] = b[(s + np.arange(k)) % len(b)]
+            s = int(tokens[i])                       # fixed preferred window per token
+        picked = []
+        j = 0
+        while len(picked) < k:
+            b = blocks[(c + j) % G]
+            take = min(k - len(picked), len(b))
+            picked.extend(b[(s + np.arange(take)) % len(b)])
+            j += 1
+        out[i] = picked
     return out
 
 
@@ -109,8 +116,8 @@ def make_workload(name: str = "toy", n: int = 256, eps: float = 0.1, seed: int =
     if cfg_override:
         cfg.update(cfg_override)
     G, N, k, d, f, vocab = cfg["G"], cfg["N"], cfg["k"], cfg["d"], cfg["f"], cfg["vocab"]
-    if k > N // G:
-        raise ValueError("top_k must not exceed experts per cluster (profiles.py:332-333)")
+    if k > N:
+        raise ValueError("top_k must not exceed the expert count")
     rng = np.random.default_rng(seed)
     bundle = make_bundle(G, N, vocab, rng)
     tokens = rng.integers(0, vocab, size=n).astype(np.int64)
