@@ -1,0 +1,58 @@
+"""EP shards spread over processes: CUDA-IPC peer buffers + signal-pad
+barriers.  Both ranks share the one GPU of the test box (IPC between
+processes on one device behaves like NVLink peers functionally); results
+must be bit-identical to the single-process layer."""
+
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+import mp_worker
+from paper_2503_04398_b200 import SpecMoELayer, synth
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world,over", [(2, {"G": 2, "N": 8}), (2, {"G": 4, "N": 16})])
+def test_two_process_layer_matches_single_process(world, over):
+    n = 300
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=mp_worker.layer_worker, args=(r, world, port, over, n, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, outs, st, all_out = q.get(timeout=540)
+        res[r] = (outs, st, all_out)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    w = synth.make_workload("toy", n=n, eps=0.3, seed=11, cfg_override=over)
+    ref_layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=w.cfg["k"], max_tokens=n)
+    ref = ref_layer.forward(torch.from_numpy(w.partials).cuda(), w.tokens, w.hist)
+    ref = ref.float().cpu().numpy()
+    st = ref_layer.stats_t.cpu().numpy()[:2]
+    tot = np.zeros(2, dtype=np.int64)
+    for r in range(world):
+        outs, s, all_out = res[r]
+        for o in outs:
+            assert np.array_equal(o, ref)
+        for o in all_out:                            # every resident shard got the SAG copy
+            assert np.array_equal(o, ref)
+        tot += np.asarray(s)
+    assert tot.tolist() == st.tolist()
