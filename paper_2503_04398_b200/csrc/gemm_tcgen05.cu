@@ -123,19 +123,26 @@ struct TileCoord {
   int32_t p, m_blk, n_blk;
 };
 
-// Tiles are enumerated problem-major; inside a problem m-blocks vary fastest
-// so the CTAs of one wave share a weight tile (n-block) and sweep the
-// problem's A rows, which stay L2-resident.
+// Tiles are enumerated problem-major.  Inside a problem, m-blocks are taken
+// in groups of `group_m` (sized on the host so a group's A rows stay in L2)
+// and m varies fastest inside a group: the CTAs of one wave share a few weight
+// tiles (n-blocks) and sweep the group's A rows, so A is read from DRAM once
+// and B once per group.
 __device__ __forceinline__ TileCoord decode_tile(const SmemProblems& sp, int32_t np,
-                                                 int32_t n_tiles_n, int32_t t, int32_t& cursor) {
+                                                 int32_t n_tiles_n, int32_t group_m, int32_t t,
+                                                 int32_t& cursor) {
   while (cursor + 1 < np && sp.tile_prefix[cursor + 1] <= t) ++cursor;
   const int32_t local = t - sp.tile_prefix[cursor];
   const int32_t mt = (sp.m[cursor] + kGemmBM - 1) / kGemmBM;
+  const int32_t per_group = group_m * n_tiles_n;
+  const int32_t g = local / per_group;
+  const int32_t first_m = g * group_m;
+  const int32_t gm = min(group_m, mt - first_m);
+  const int32_t r = local - g * per_group;
   TileCoord c;
   c.p = cursor;
-  c.m_blk = local % mt;
-  c.n_blk = local / mt;
-  (void)n_tiles_n;
+  c.m_blk = first_m + r % gm;
+  c.n_blk = r / gm;
   return c;
 }
 
@@ -212,7 +219,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       uint32_t phase = 0;
       int32_t cursor = 0;
       for (int32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        const TileCoord tc = decode_tile(sp, np, args.n_tiles_n, t, cursor);
+        const TileCoord tc = decode_tile(sp, np, args.n_tiles_n, args.group_m, t, cursor);
         const int32_t a_row = (int32_t)(sp.a_off[tc.p] + (int64_t)tc.m_blk * kGemmBM);
         const int32_t b_row = sp.b_idx[tc.p] * args.n_b + tc.n_blk * kGemmBN;
         for (int32_t kb = 0; kb < args.num_k_blocks; ++kb) {
@@ -258,7 +265,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     uint32_t acc = 0, acc_phase = 0;
     int32_t cursor = 0;
     for (int32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      const TileCoord tc = decode_tile(sp, np, args.n_tiles_n, t, cursor);
+      const TileCoord tc = decode_tile(sp, np, args.n_tiles_n, args.group_m, t, cursor);
       const int32_t m = sp.m[tc.p];
       const int32_t row0 = tc.m_blk * kGemmBM + ew * 32;   // first row of this warp
       // per-lane destination row pointer (lane l <-> row row0 + l)
@@ -388,7 +395,13 @@ static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
                                        (int)kGemmSmem));
     attr_set = true;
   }
-  grouped_gemm_kernel<EPI><<<num_sms(), kThreads, kGemmSmem, st>>>(a, b, args);
+  GemmArgs g = args;
+  if (g.group_m <= 0) {
+    // keep a group's A rows (128 x K bf16 per m-block) within ~40 MB of L2
+    const int64_t a_blk = (int64_t)kGemmBM * g.num_k_blocks * kGemmBK * 2;
+    g.group_m = (int32_t)std::max<int64_t>(1, (40ll << 20) / a_blk);
+  }
+  grouped_gemm_kernel<EPI><<<num_sms(), kThreads, kGemmSmem, st>>>(a, b, g);
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }

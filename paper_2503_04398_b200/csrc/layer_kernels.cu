@@ -236,12 +236,226 @@ gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ 
   }
 }
 
+// Tensor-core gate: logits[64 rows, N] per CTA with mma.sync m16n8k16 (bf16 in,
+// fp32 accumulate).  The gate is HBM-bound on the hidden rows (d*2 bytes per
+// token); the CUDA-core version above is compute-bound for N = 64.  H rows and
+// W rows stream through a 4-stage cp.async ring in 128-B rows with a 16-B XOR
+// swizzle (conflict-free ldmatrix).
+constexpr int kMmaRows = 64;
+constexpr int kMmaKC = 64;                       // bf16 per row per stage (128 B)
+constexpr int kMmaStages = 4;
+constexpr int kMmaThreads = 128;
+constexpr int kMmaStageBytes = (kMmaRows + kGateMaxN) * kMmaKC * 2;   // 16 KiB
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+               :: "r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// byte offset of 16-B chunk `c` of row `r` in a 128-B-row tile
+__device__ __forceinline__ uint32_t swz(int r, int c) { return r * 128 + ((c ^ (r & 7)) << 4); }
+
+template <int NT>   // NT = N / 8 n-tiles
+__global__ void __launch_bounds__(kMmaThreads)
+gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ w_gate,
+                const float* __restrict__ b_gate, int32_t k, int32_t renorm,
+                const int32_t* __restrict__ slot_owner, ShardPtrs topk_ids, ShardPtrs topk_w,
+                int64_t* stats) {
+  constexpr int N = NT * 8;
+  extern __shared__ __align__(128) uint8_t gsm[];
+  __shared__ RowMap rm;
+  __shared__ const char* s_row[kMmaRows];
+  __shared__ int32_t s_gl[kMmaRows];
+  __shared__ int64_t s_j[kMmaRows];
+  __shared__ unsigned long long s_local, s_remote;
+  load_rowmap(rm, lr);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(gsm));
+  const int kchunks = (int)(d / kMmaKC);
+  for (int64_t rb = blockIdx.x; rb * kMmaRows < rm.total; rb += gridDim.x) {
+    if (tid < kMmaRows) {
+      const int64_t q = rb * kMmaRows + tid;
+      int32_t gl = -1; int64_t j = 0;
+      if (q < rm.total) decode_row(rm, lr.shard_count, q, gl, j);
+      s_gl[tid] = gl;
+      s_j[tid] = j;
+      s_row[tid] = gl >= 0 ? hs.p[gl] + j * d * 2 : nullptr;
+    }
+    if (tid == 0) { s_local = 0; s_remote = 0; }
+    __syncthreads();
+    auto load_stage = [&](int kc, int stage) {
+      const uint32_t st = sbase + stage * kMmaStageBytes;
+      for (int e = tid; e < (kMmaRows + N) * 8; e += kMmaThreads) {
+        const int r = e >> 3, c = e & 7;
+        if (r < kMmaRows) {
+          const char* src = s_row[r];
+          cp_async16(st + swz(r, c), src ? src + (kc * kMmaKC + c * 8) * 2 : w_gate, src != nullptr);
+        } else {
+          const int n = r - kMmaRows;
+          cp_async16(st + swz(r, c), w_gate + ((int64_t)n * d + kc * kMmaKC + c * 8) * 2, true);
+        }
+      }
+    };
+    float acc[NT][4];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+#pragma unroll
+    for (int s = 0; s < kMmaStages - 1; ++s) {
+      if (s < kchunks) load_stage(s, s);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int kc = 0; kc < kchunks; ++kc) {
+      asm volatile("cp.async.wait_group %0;" :: "n"(kMmaStages - 2) : "memory");
+      __syncthreads();
+      {  // prefetch kc + stages - 1 into the slot freed last iteration
+        const int nk = kc + kMmaStages - 1;
+        if (nk < kchunks) load_stage(nk, nk % kMmaStages);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+      const uint32_t st = sbase + (kc % kMmaStages) * kMmaStageBytes;
+#pragma unroll
+      for (int ks = 0; ks < kMmaKC / 16; ++ks) {
+        // A: rows warp*16 + (lane & 15), 16-B chunk 2*ks + (lane >> 4)
+        uint32_t a0, a1, a2, a3;
+        const int ar = warp * 16 + (lane & 15);
+        ldsm_x4(st + swz(ar, 2 * ks + (lane >> 4)), a0, a1, a2, a3);
+#pragma unroll
+        for (int t = 0; t < NT; t += 2) {
+          // B for n-tiles t, t+1: matrices (n t*8.., k lo), (k hi), (n (t+1)*8.., k lo), (k hi)
+          uint32_t b0, b1, b2, b3;
+          const int nr = kMmaRows + t * 8 + (lane & 7) + ((lane >> 4) << 3);
+          const int nt_ok = (t + 1 < NT) || (lane < 16);
+          ldsm_x4(st + swz(nt_ok ? nr : kMmaRows + t * 8 + (lane & 7), 2 * ks + ((lane >> 3) & 1)),
+                  b0, b1, b2, b3);
+          mma_bf16(acc[t], a0, a1, a2, a3, b0, b1);
+          if (t + 1 < NT) mma_bf16(acc[t + 1], a0, a1, a2, a3, b2, b3);
+        }
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    // logits -> smem [64][N + 1] (reuses the staging ring)
+    float* lgs = reinterpret_cast<float*>(gsm);
+    {
+      const int r0 = warp * 16 + (lane >> 2);
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const int c0 = t * 8 + 2 * (lane & 3);
+        const float b0 = b_gate ? __ldg(b_gate + c0) : 0.f, b1 = b_gate ? __ldg(b_gate + c0 + 1) : 0.f;
+        lgs[r0 * (N + 1) + c0] = acc[t][0] + b0;
+        lgs[r0 * (N + 1) + c0 + 1] = acc[t][1] + b1;
+        lgs[(r0 + 8) * (N + 1) + c0] = acc[t][2] + b0;
+        lgs[(r0 + 8) * (N + 1) + c0 + 1] = acc[t][3] + b1;
+      }
+    }
+    __syncthreads();
+    unsigned long long my_local = 0, my_remote = 0;
+    for (int r = warp; r < kMmaRows; r += kMmaThreads / 32) {
+      const int32_t gl = s_gl[r];
+      if (gl < 0) continue;
+      const float* lg = lgs + r * (N + 1);
+      float v0 = lane < N ? lg[lane] : -INFINITY;
+      float v1 = lane + 32 < N ? lg[lane + 32] : -INFINITY;
+      float mx = fmaxf(v0, v1);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      float ex = (lane < N ? __expf(v0 - mx) : 0.f) + (lane + 32 < N ? __expf(v1 - mx) : 0.f);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ex += __shfl_xor_sync(0xffffffffu, ex, o);
+      const float inv = 1.0f / ex;
+      int sel_e[kGateMaxK];
+      float sel_p[kGateMaxK];
+      float psum = 0.f;
+      for (int s = 0; s < k; ++s) {
+        float bv; int bi;
+        if (v1 > v0) { bv = v1; bi = lane + 32; } else { bv = v0; bi = lane; }
+        if (bv == -INFINITY) bi = 1 << 20;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+        }
+        sel_e[s] = bi;
+        sel_p[s] = __expf(bv - mx) * inv;
+        psum += sel_p[s];
+        if (bi == lane) v0 = -INFINITY;
+        if (bi == lane + 32) v1 = -INFINITY;
+      }
+      if (lane < k) {
+        // lane s writes slot s (all lanes hold the same selection)
+        float p = 0.f; int e = 0;
+#pragma unroll
+        for (int s = 0; s < kGateMaxK; ++s) if (s == lane) { p = sel_p[s]; e = sel_e[s]; }
+        const int64_t g = lr.shard_begin + gl;
+        reinterpret_cast<int32_t*>(topk_ids.p[gl])[s_j[r] * k + lane] = e;
+        reinterpret_cast<float*>(topk_w.p[gl])[s_j[r] * k + lane] = renorm ? p / psum : p;
+        if (slot_owner[e] == g) ++my_local; else ++my_remote;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      my_local += __shfl_xor_sync(0xffffffffu, my_local, o);
+      my_remote += __shfl_xor_sync(0xffffffffu, my_remote, o);
+    }
+    if (lane == 0 && (my_local | my_remote)) {
+      atomicAdd(&s_local, my_local);
+      atomicAdd(&s_remote, my_remote);
+    }
+    __syncthreads();
+    if (tid == 0 && stats) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_LOCAL_PAIRS), s_local);
+      atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_REMOTE_PAIRS), s_remote);
+    }
+    __syncthreads();
+  }
+}
+
+template <int NT>
+static int launch_gate_mma(const LocalRows& lr, const ShardPtrs& hs, int64_t d, const void* w,
+                           const float* b, int32_t k, int32_t renorm, const int32_t* owner,
+                           const ShardPtrs& ids, const ShardPtrs& wts, int64_t* stats,
+                           int64_t n_rows_bound, cudaStream_t st) {
+  const size_t smem = (size_t)kMmaStages * ((kMmaRows + NT * 8) * kMmaKC * 2);
+  static bool attr = false;
+  if (!attr) {
+    SMOE_CUDA_TRY(cudaFuncSetAttribute(gate_mma_kernel<NT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  gate_mma_kernel<NT><<<grid_cap(ceil_div(n_rows_bound, kMmaRows), 4), kMmaThreads, smem, st>>>(
+      lr, hs, d, static_cast<const char*>(w), b, k, renorm, owner, ids, wts, stats);
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
 int launch_gate(const LocalRows& lr, const ShardPtrs& hs, int64_t d, const void* w_gate,
                 const float* b_gate, int32_t N, int32_t k, int32_t renorm,
                 const int32_t* slot_owner, const ShardPtrs& topk_ids, const ShardPtrs& topk_w,
                 int64_t* stats, int64_t n_rows_bound, cudaStream_t st) {
   if (N < 1 || N > kGateMaxN || k < 1 || k > kGateMaxK || k > N || d % 2) return SMOE_ERR_UNSUPPORTED;
   if (n_rows_bound <= 0) return SMOE_OK;
+  if (d % kMmaKC == 0) {
+    switch (N) {   // tensor-core path for N in {8, 16, ..., 64}
+      case 8: return launch_gate_mma<1>(lr, hs, d, w_gate, b_gate, k, renorm, slot_owner, topk_ids, topk_w, stats, n_rows_bound, st);
+      case 16: return launch_gate_mma<2>(lr, hs, d, w_gate, b_gate, k, renorm, slot_owner, topk_ids, topk_w, stats, n_rows_bound, st);
+      case 32: return launch_gate_mma<4>(lr, hs, d, w_gate, b_gate, k, renorm, slot_owner, topk_ids, topk_w, stats, n_rows_bound, st);
+      case 64: return launch_gate_mma<8>(lr, hs, d, w_gate, b_gate, k, renorm, slot_owner, topk_ids, topk_w, stats, n_rows_bound, st);
+      default: break;
+    }
+  }
   gate_kernel<<<grid_cap(ceil_div(n_rows_bound, kGateRows), 4), 256, 0, st>>>(
       lr, hs, d, static_cast<const uint32_t*>(w_gate), b_gate, N, k, renorm, slot_owner,
       topk_ids, topk_w, stats);

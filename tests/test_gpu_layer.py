@@ -33,6 +33,8 @@ CASES = [
     ("toy", 500, 0.1, {"G": 4, "N": 64, "k": 8, "d": 256, "f": 384}),
     ("toy", 300, 0.1, {"G": 1, "N": 8, "k": 2}),
     ("toy", 512, 0.2, {"G": 8, "N": 8, "k": 1, "d": 4096, "f": 512}),
+    ("toy", 333, 0.2, {"G": 4, "N": 24, "k": 3}),          # CUDA-core gate path (N % 8 != 0 tiles)
+    ("toy", 2000, 0.4, {"G": 8, "N": 32, "k": 4, "d": 1024, "f": 256}),
 ]
 
 
