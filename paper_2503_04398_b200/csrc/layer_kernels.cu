@@ -245,7 +245,6 @@ constexpr int kMmaRows = 64;
 constexpr int kMmaKC = 64;                       // bf16 per row per stage (128 B)
 constexpr int kMmaStages = 4;
 constexpr int kMmaThreads = 128;
-constexpr int kMmaStageBytes = (kMmaRows + kGateMaxN) * kMmaKC * 2;   // 16 KiB
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
@@ -274,6 +273,7 @@ gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ 
                 const int32_t* __restrict__ slot_owner, ShardPtrs topk_ids, ShardPtrs topk_w,
                 int64_t* stats) {
   constexpr int N = NT * 8;
+  constexpr int kMmaStageBytes = (kMmaRows + N) * kMmaKC * 2;   // H rows + W rows, 128 B each
   extern __shared__ __align__(128) uint8_t gsm[];
   __shared__ RowMap rm;
   __shared__ const char* s_row[kMmaRows];
