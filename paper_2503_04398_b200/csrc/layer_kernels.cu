@@ -58,33 +58,45 @@ __device__ __forceinline__ void decode_row(const RowMap& rm, int32_t shard_count
 }
 
 // ------------------------------------------------------------------ K3 SRS
+// One warp per output row; G is a template parameter so the 2*G 16-B loads
+// of an iteration (two vectors per lane) are all in flight before the sum.
+template <int G>
 __global__ void __launch_bounds__(256)
 srs_kernel(LocalRows lr, ShardPtrs partials, int64_t d, ShardPtrs hs) {
   __shared__ RowMap rm;
   load_rowmap(rm, lr);
   const int lane = threadIdx.x & 31;
-  const int G = lr.n_shards;
   const int64_t vecs = d / 8;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const char* src_base[G];
+#pragma unroll
+  for (int r = 0; r < G; ++r) src_base[r] = partials.p[r];
   for (int64_t q = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); q < rm.total;
        q += nwarps) {
     int32_t gl; int64_t j;
     decode_row(rm, lr.shard_count, q, gl, j);
     const int64_t g = lr.shard_begin + gl;
-    const int64_t src = lr.forward[g * rm.group + j];
-    const int64_t row_off = src * d * 2;
+    const int64_t row_off = lr.forward[g * rm.group + j] * d * 2;
     char* out = hs.p[gl] + j * d * 2;
-    for (int64_t v = lane; v < vecs; v += 32) {
-      uint4 x[SMOE_MAX_SHARDS];
+    for (int64_t v = lane; v < vecs; v += 64) {
+      const bool two = v + 32 < vecs;
+      uint4 x[G], y[G];
 #pragma unroll
-      for (int r = 0; r < SMOE_MAX_SHARDS; ++r)
-        if (r < G) x[r] = ld_nc_v4(partials.p[r] + row_off + v * 16);
-      float a[8];
+      for (int r = 0; r < G; ++r) {
+        x[r] = ld_nc_v4(src_base[r] + row_off + v * 16);
+        if (two) y[r] = ld_nc_v4(src_base[r] + row_off + (v + 32) * 16);
+      }
+      float a[8], b[8];
       set_bf16x8(a, x[0]);
 #pragma unroll
-      for (int r = 1; r < SMOE_MAX_SHARDS; ++r)
-        if (r < G) acc_bf16x8(a, x[r]);
+      for (int r = 1; r < G; ++r) acc_bf16x8(a, x[r]);
       st_v4(out + v * 16, pack_bf16x8(a));
+      if (two) {
+        set_bf16x8(b, y[0]);
+#pragma unroll
+        for (int r = 1; r < G; ++r) acc_bf16x8(b, y[r]);
+        st_v4(out + (v + 32) * 16, pack_bf16x8(b));
+      }
     }
   }
 }
@@ -93,7 +105,17 @@ int launch_srs(const LocalRows& lr, const ShardPtrs& partials, int64_t d, const 
                int64_t n_rows_bound, cudaStream_t st) {
   if (d % 8) return SMOE_ERR_UNSUPPORTED;
   if (n_rows_bound <= 0) return SMOE_OK;
-  srs_kernel<<<grid_cap(ceil_div(n_rows_bound, 8), 16), 256, 0, st>>>(lr, partials, d, hs);
+  const int grid = grid_cap(ceil_div(n_rows_bound, 8), 16);
+  switch (lr.n_shards) {
+#define SMOE_SRS_CASE(G_) \
+    case G_: srs_kernel<G_><<<grid, 256, 0, st>>>(lr, partials, d, hs); break;
+    SMOE_SRS_CASE(1) SMOE_SRS_CASE(2) SMOE_SRS_CASE(3) SMOE_SRS_CASE(4) SMOE_SRS_CASE(5)
+    SMOE_SRS_CASE(6) SMOE_SRS_CASE(7) SMOE_SRS_CASE(8) SMOE_SRS_CASE(9) SMOE_SRS_CASE(10)
+    SMOE_SRS_CASE(11) SMOE_SRS_CASE(12) SMOE_SRS_CASE(13) SMOE_SRS_CASE(14) SMOE_SRS_CASE(15)
+    SMOE_SRS_CASE(16)
+#undef SMOE_SRS_CASE
+    default: return SMOE_ERR_UNSUPPORTED;
+  }
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }
@@ -241,10 +263,10 @@ gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ 
 // token); the CUDA-core version above is compute-bound for N = 64.  H rows and
 // W rows stream through a 4-stage cp.async ring in 128-B rows with a 16-B XOR
 // swizzle (conflict-free ldmatrix).
-constexpr int kMmaRows = 64;
+constexpr int kMmaRows = 32;
 constexpr int kMmaKC = 64;                       // bf16 per row per stage (128 B)
-constexpr int kMmaStages = 4;
-constexpr int kMmaThreads = 128;
+constexpr int kMmaStages = 6;
+constexpr int kMmaThreads = 64;
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
@@ -435,7 +457,7 @@ static int launch_gate_mma(const LocalRows& lr, const ShardPtrs& hs, int64_t d, 
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  gate_mma_kernel<NT><<<grid_cap(ceil_div(n_rows_bound, kMmaRows), 4), kMmaThreads, smem, st>>>(
+  gate_mma_kernel<NT><<<grid_cap(ceil_div(n_rows_bound, kMmaRows), 8), kMmaThreads, smem, st>>>(
       lr, hs, d, static_cast<const char*>(w), b, k, renorm, owner, ids, wts, stats);
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
@@ -573,7 +595,14 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
     if (pos >= expert_rows) { if (lane == 0) set_err(err, SMOE_ERRBIT_CAPACITY); continue; }
     const char* src = hs.p[gl] + j * d * 2;
     char* dst = xin.p[o] + pos * d * 2;
-    for (int64_t v = lane; v < vecs; v += 32) st_v4(dst + v * 16, ld_nc_v4(src + v * 16));
+    int64_t v = lane;
+    for (; v + 96 < vecs; v += 128) {
+      const uint4 a = ld_nc_v4(src + v * 16), b = ld_nc_v4(src + (v + 32) * 16),
+                  c = ld_nc_v4(src + (v + 64) * 16), e4 = ld_nc_v4(src + (v + 96) * 16);
+      st_v4(dst + v * 16, a); st_v4(dst + (v + 32) * 16, b);
+      st_v4(dst + (v + 64) * 16, c); st_v4(dst + (v + 96) * 16, e4);
+    }
+    for (; v < vecs; v += 32) st_v4(dst + v * 16, ld_nc_v4(src + v * 16));
     if (lane == 0)
       reinterpret_cast<int64_t*>(xmeta.p[o])[pos] = ((int64_t)g << 40) | (j * k + s);
   }
@@ -595,15 +624,18 @@ int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
 }
 
 // ------------------------------------------------------------------ K8 combine + SAG
+template <int G>
 __global__ void __launch_bounds__(256)
 combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtrs topk_w,
                    ShardPtrs outs) {
   __shared__ RowMap rm;
   load_rowmap(rm, lr);
   const int lane = threadIdx.x & 31;
-  const int G = lr.n_shards;
   const int64_t vecs = d / 8;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  char* dst_base[G];
+#pragma unroll
+  for (int r = 0; r < G; ++r) dst_base[r] = outs.p[r];
   for (int64_t q = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); q < rm.total;
        q += nwarps) {
     int32_t gl; int64_t j;
@@ -616,20 +648,23 @@ combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtr
     for (int s = 0; s < kGateMaxK; ++s) wk[s] = s < k ? w[s] : 0.f;
     const char* y = ypair.p[gl] + j * k * d * 2;
     for (int64_t v = lane; v < vecs; v += 32) {
+      uint4 yv[kGateMaxK];
+#pragma unroll
+      for (int s = 0; s < kGateMaxK; ++s)
+        if (s < k) yv[s] = ld_nc_v4(y + ((int64_t)s * d + v * 8) * 2);
       float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int s = 0; s < kGateMaxK; ++s) {
         if (s < k) {
           float t[8];
-          set_bf16x8(t, ld_nc_v4(y + ((int64_t)s * d + v * 8) * 2));
+          set_bf16x8(t, yv[s]);
 #pragma unroll
           for (int c = 0; c < 8; ++c) a[c] += wk[s] * t[c];
         }
       }
       const uint4 o = pack_bf16x8(a);
 #pragma unroll
-      for (int r = 0; r < SMOE_MAX_SHARDS; ++r)
-        if (r < G) st_v4(outs.p[r] + (i * d + v * 8) * 2, o);
+      for (int r = 0; r < G; ++r) st_v4(dst_base[r] + (i * d + v * 8) * 2, o);
     }
   }
 }
@@ -639,8 +674,17 @@ int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtr
                        cudaStream_t st) {
   if (k > kGateMaxK || d % 8) return SMOE_ERR_UNSUPPORTED;
   if (n_rows_bound <= 0) return SMOE_OK;
-  combine_sag_kernel<<<grid_cap(ceil_div(n_rows_bound, 8), 16), 256, 0, st>>>(lr, k, d, ypair,
-                                                                             topk_w, outs);
+  const int grid = grid_cap(ceil_div(n_rows_bound, 8), 16);
+  switch (lr.n_shards) {
+#define SMOE_CMB_CASE(G_) \
+    case G_: combine_sag_kernel<G_><<<grid, 256, 0, st>>>(lr, k, d, ypair, topk_w, outs); break;
+    SMOE_CMB_CASE(1) SMOE_CMB_CASE(2) SMOE_CMB_CASE(3) SMOE_CMB_CASE(4) SMOE_CMB_CASE(5)
+    SMOE_CMB_CASE(6) SMOE_CMB_CASE(7) SMOE_CMB_CASE(8) SMOE_CMB_CASE(9) SMOE_CMB_CASE(10)
+    SMOE_CMB_CASE(11) SMOE_CMB_CASE(12) SMOE_CMB_CASE(13) SMOE_CMB_CASE(14) SMOE_CMB_CASE(15)
+    SMOE_CMB_CASE(16)
+#undef SMOE_CMB_CASE
+    default: return SMOE_ERR_UNSUPPORTED;
+  }
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }
