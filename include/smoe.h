@@ -256,6 +256,26 @@ int smoe_layer_forward(smoe_layer* layer, const int64_t* tokens,
 /* Cross-process barrier over the bound SIGNAL pads (no-op if world_size 1). */
 int smoe_layer_barrier(smoe_layer* layer, void* stream);
 
+/* ---- single-rank building blocks (used by the DS-MoE baseline pipeline) -- */
+/* Gate over `rows` contiguous bf16 rows h[rows, hidden]: top-k expert ids
+ * (lowest index on ties) and softmax weights; stats[0..1] += local / remote
+ * pairs where local means expert_owner[e] == my_shard (stats nullable). */
+int smoe_gate_topk(const void* h, int64_t rows, int32_t hidden, const void* w_gate,
+                   const float* b_gate, int32_t n_experts, int32_t top_k,
+                   int32_t renormalize, const int32_t* expert_owner, int32_t my_shard,
+                   int32_t* topk_ids, float* topk_w, int64_t* stats, void* stream);
+/* Expert-major send position of every (row, slot) pair:
+ *   pair_pos[j*k+s] = sum_{e'<e} counts[e'] + #{earlier pairs with expert e},
+ * counts[N] = pairs per expert (stable, deterministic). */
+int smoe_pair_offsets(const int32_t* topk_ids, int64_t rows, int32_t top_k,
+                      int32_t n_experts, int32_t* pair_pos, int32_t* counts, void* stream);
+/* dst[pair_pos[j*k+s], :] = src[j, :] (all2allv send-buffer packing). */
+int smoe_pack_rows(const void* src, int64_t rows, int32_t top_k, int32_t hidden,
+                   const int32_t* pair_pos, void* dst, void* stream);
+/* out[j, :] = bf16( sum_s topk_w[j*k+s] * y[pair_pos[j*k+s], :] ) (fp32 sum). */
+int smoe_combine_rows(const void* y, const int32_t* pair_pos, const float* topk_w,
+                      int64_t rows, int32_t top_k, int32_t hidden, void* out, void* stream);
+
 /* ======================================================================= *
  *  Grouped GEMM (K6) — exposed for tests and microbenchmarks                *
  * ======================================================================= */

@@ -43,6 +43,11 @@ SIGNATURES = [
     ("smoe_layer_stage", C.c_int, [P, c_i32, P, P, c_i64, P]),
     ("smoe_layer_forward", C.c_int, [P, P, P, c_i64, P]),
     ("smoe_layer_barrier", C.c_int, [P, P]),
+    ("smoe_gate_topk", C.c_int,
+     [P, c_i64, c_i32, P, P, c_i32, c_i32, c_i32, P, c_i32, P, P, P, P]),
+    ("smoe_pair_offsets", C.c_int, [P, c_i64, c_i32, c_i32, P, P, P]),
+    ("smoe_pack_rows", C.c_int, [P, c_i64, c_i32, c_i32, P, P, P]),
+    ("smoe_combine_rows", C.c_int, [P, P, P, c_i64, c_i32, c_i32, P, P]),
     ("smoe_grouped_gemm", C.c_int,
      [P, c_i64, c_i64, P, c_i64, c_i64, P, c_i32, c_i32, P, c_i64, c_i64, P]),
     ("smoe_device_alloc", C.c_int, [c_sz, P]),

@@ -1,0 +1,219 @@
+"""DS-MoE pipeline baseline: AR -> A2A -> A2A -> AG (comm.py:99-108).
+
+The comparison point of the north star.  Densely-replicated attention output
+is all-reduced on every rank, tokens are sharded by position
+(token_dev = i % G, comm.py:202), experts sit in contiguous blocks
+(expert_dev = e // (N/G), comm.py:201), the dispatch / combine all-to-alls
+are all2allv with host-synchronised split sizes, and an all-gather restores
+the batch on every rank.  The compute uses the same sm_100a kernels as the
+s-MoE layer (tensor-core gate, tcgen05 grouped GEMM); the collectives are
+NCCL through torch.distributed (one rank per GPU), or — with G virtual ranks
+in one process — the equivalent device copies.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _dev, _native as N
+
+
+class DSMoELayer:
+    def __init__(self, gate_w, w1, w3, w2, *, n_ranks: int, top_k: int, max_tokens: int,
+                 renormalize: bool = True, process_group=None, distributed: bool = False):
+        t = _dev.torch()
+        self.lib = N.lib()
+        self.G = int(n_ranks)
+        self.k = int(top_k)
+        self.max_tokens = int(max_tokens)
+        self.renormalize = bool(renormalize)
+        self.distributed = distributed
+        self.pg = process_group
+        gw = _dev.to_device(gate_w, t.bfloat16)
+        self.N, self.d = int(gw.shape[0]), int(gw.shape[1])
+        self.f = int(w1.shape[1])
+        if self.N % self.G:
+            raise ValueError("DS-MoE contiguous placement needs G | N")
+        self.npc = self.N // self.G
+        dev = gw.device
+        if distributed:
+            import torch.distributed as dist
+            self.rank = dist.get_rank(process_group)
+            if dist.get_world_size(process_group) != self.G:
+                raise ValueError("distributed DS-MoE runs one rank per process")
+            self.local_ranks = [self.rank]
+        else:
+            self.rank = 0
+            self.local_ranks = list(range(self.G))
+        self.w_gate = gw
+        self.owner = t.arange(self.N, device=dev, dtype=t.int32) // self.npc
+        self.w13, self.w2 = {}, {}
+        for r in self.local_ranks:
+            sl = slice(r * self.npc, (r + 1) * self.npc)
+            w1r = _dev.to_device(w1[sl] if not isinstance(w1, t.Tensor) else w1[sl], t.bfloat16)
+            w3r = _dev.to_device(w3[sl] if not isinstance(w3, t.Tensor) else w3[sl], t.bfloat16)
+            packed = t.empty((self.npc, 2 * self.f, self.d), dtype=t.bfloat16, device=dev)
+            N.check(self.lib.smoe_pack_w13(N.ptr(w1r.contiguous()), N.ptr(w3r.contiguous()),
+                                           self.npc, self.f, self.d, N.ptr(packed),
+                                           N.stream_ptr()), "pack_w13")
+            self.w13[r] = packed
+            self.w2[r] = _dev.to_device(w2[sl] if not isinstance(w2, t.Tensor) else w2[sl],
+                                        t.bfloat16).contiguous()
+        n, k, d = self.max_tokens, self.k, self.d
+        cap = n * k
+        self.buf = {r: {"hs": t.empty((n, d), dtype=t.bfloat16, device=dev),
+                        "ids": t.empty((n, k), dtype=t.int32, device=dev),
+                        "w": t.empty((n, k), dtype=t.float32, device=dev),
+                        "pos": t.empty((n, k), dtype=t.int32, device=dev),
+                        "cnt": t.zeros(self.N, dtype=t.int32, device=dev),
+                        "send": t.empty((cap, d), dtype=t.bfloat16, device=dev),
+                        "recv": t.empty((cap, d), dtype=t.bfloat16, device=dev),
+                        "hmid": t.empty((cap, self.f), dtype=t.bfloat16, device=dev),
+                        "yrecv": t.empty((cap, d), dtype=t.bfloat16, device=dev),
+                        "yback": t.empty((cap, d), dtype=t.bfloat16, device=dev),
+                        "out": t.empty((n, d), dtype=t.bfloat16, device=dev)}
+                    for r in self.local_ranks}
+        self.stats_t = t.zeros(N.STAT_COUNT, dtype=t.int64, device=dev)
+        self.problems = {r: t.zeros((256, 4), dtype=t.int64, device=dev) for r in self.local_ranks}
+        self.last = {}
+
+    # ------------------------------------------------------------ collectives
+    def _all_reduce(self, partials):
+        t = _dev.torch()
+        if self.distributed:
+            import torch.distributed as dist
+            h = partials[0].clone()
+            dist.all_reduce(h, group=self.pg)
+            return {self.rank: h}
+        s = partials[0].float()
+        for p in partials[1:]:
+            s += p.float()
+        h = s.to(t.bfloat16)
+        return {r: h.clone() for r in self.local_ranks}        # every rank holds the sum
+
+    def _gather_counts(self):
+        t = _dev.torch()
+        if self.distributed:
+            import torch.distributed as dist
+            out = t.empty((self.G, self.N), dtype=t.int32, device=self.w_gate.device)
+            dist.all_gather_into_tensor(out, self.buf[self.rank]["cnt"], group=self.pg)
+            return out.cpu().numpy().astype(np.int64)
+        return t.stack([self.buf[r]["cnt"] for r in range(self.G)]).cpu().numpy().astype(np.int64)
+
+    def _all_to_all(self, name_in, name_out, send_splits, recv_splits):
+        """send_splits[r][o] rows go from rank r to rank o; received rows are
+        source-major in name_out."""
+        if self.distributed:
+            import torch.distributed as dist
+            r = self.rank
+            dist.all_to_all_single(self.buf[r][name_out][: int(sum(recv_splits[r]))],
+                                   self.buf[r][name_in][: int(sum(send_splits[r]))],
+                                   output_split_sizes=[int(x) for x in recv_splits[r]],
+                                   input_split_sizes=[int(x) for x in send_splits[r]],
+                                   group=self.pg)
+            return
+        soff = {r: np.concatenate([[0], np.cumsum(send_splits[r])]) for r in range(self.G)}
+        for o in range(self.G):
+            dst = self.buf[o][name_out]
+            off = 0
+            for r in range(self.G):
+                m = int(send_splits[r][o])
+                if m:
+                    dst[off:off + m].copy_(self.buf[r][name_in][soff[r][o]:soff[r][o] + m])
+                off += m
+
+    def _all_gather_out(self, group):
+        t = _dev.torch()
+        if self.distributed:
+            import torch.distributed as dist
+            full = t.empty((self.G * group, self.d), dtype=t.bfloat16, device=self.w_gate.device)
+            dist.all_gather_into_tensor(full, self.buf[self.rank]["out"][:group], group=self.pg)
+            return full
+        return t.cat([self.buf[r]["out"][:group] for r in range(self.G)])
+
+    # ------------------------------------------------------------ forward
+    def forward(self, partials, n: int):
+        """partials: list (one per local rank) of [n, d] bf16 CUDA tensors.
+        Returns the layer output [n, d] in the original token order."""
+        t = _dev.torch()
+        L, sp = self.lib, N.stream_ptr()
+        G, k, d, npc = self.G, self.k, self.d, self.npc
+        dev = self.w_gate.device
+        # 1. all-reduce of the attention-TP partials
+        H = self._all_reduce(partials)
+        # 2. position sharding plan (comm.py:202: token i -> rank i % G)
+        devices = t.arange(n, device=dev, dtype=t.int64) % G
+        fwd = t.empty(G * max(n, 1), dtype=t.int64, device=dev)
+        inv = t.empty(n, dtype=t.int64, device=dev)
+        counts = t.empty(G, dtype=t.int32, device=dev)
+        group_t = t.empty(1, dtype=t.int64, device=dev)
+        ws_b = int(L.smoe_plan_workspace_bytes(n, G))
+        ws = t.empty(ws_b, dtype=t.uint8, device=dev)
+        N.check(L.smoe_rebatch_plan(N.ptr(devices), n, G, N.ptr(fwd), N.ptr(inv), N.ptr(counts),
+                                    N.ptr(group_t), 0, N.ptr(ws), ws_b, sp), "plan")
+        cnt_h = [(n - r + G - 1) // G for r in range(G)]            # i % G sharding
+        group = max(cnt_h) if n else 0
+        self.stats_t.zero_()
+        for r in self.local_ranks:
+            b = self.buf[r]
+            rows = cnt_h[r]
+            idx = fwd[r * group: r * group + rows]
+            # 3. my token rows
+            N.check(L.smoe_gather_rows(N.ptr(H[r]), n, 2, d, N.ptr(idx), rows, 0, 0, N.ptr(b["hs"]),
+                                       0, sp), "gather")
+            # 4. gate + 5. expert-major send positions + 6. pack
+            N.check(L.smoe_gate_topk(N.ptr(b["hs"]), rows, d, N.ptr(self.w_gate), 0, self.N, k,
+                                     int(self.renormalize), N.ptr(self.owner), r, N.ptr(b["ids"]),
+                                     N.ptr(b["w"]), N.ptr(self.stats_t), sp), "gate")
+            N.check(L.smoe_pair_offsets(N.ptr(b["ids"]), rows, k, self.N, N.ptr(b["pos"]),
+                                        N.ptr(b["cnt"]), sp), "pair_offsets")
+            N.check(L.smoe_pack_rows(N.ptr(b["hs"]), rows, k, d, N.ptr(b["pos"]), N.ptr(b["send"]),
+                                     sp), "pack")
+        # 7. counts exchange (host sync: all2allv needs split sizes)
+        C = self._gather_counts()                                # [G src, N]
+        send = {r: [int(C[r, o * npc:(o + 1) * npc].sum()) for o in range(G)] for r in range(G)}
+        recv = {o: [send[r][o] for r in range(G)] for o in range(G)}
+        # 8. dispatch all-to-all
+        self._all_to_all("send", "recv", send, recv)
+        # 9. experts: one grouped GEMM per rank, problems = (source rank, local expert)
+        for o in self.local_ranks:
+            b = self.buf[o]
+            probs, off = [], 0
+            for r in range(G):
+                for e in range(o * npc, (o + 1) * npc):
+                    m = int(C[r, e])
+                    probs.append([off, m, e - o * npc, off])
+                    off += m
+            rows_in = off
+            self.problems[o][: len(probs)].copy_(t.as_tensor(probs, dtype=t.int64))
+            if rows_in:
+                N.check(L.smoe_grouped_gemm(N.ptr(b["recv"]), b["recv"].shape[0], d,
+                                            N.ptr(self.w13[o]), npc * 2 * self.f, 2 * self.f,
+                                            N.ptr(self.problems[o]), len(probs), 1, N.ptr(b["hmid"]),
+                                            b["hmid"].shape[0], self.f, sp), "gemm_up")
+                N.check(L.smoe_grouped_gemm(N.ptr(b["hmid"]), b["hmid"].shape[0], self.f,
+                                            N.ptr(self.w2[o]), npc * d, d, N.ptr(self.problems[o]),
+                                            len(probs), 0, N.ptr(b["yrecv"]), b["yrecv"].shape[0],
+                                            d, sp), "gemm_down")
+        # 10. combine all-to-all (reverse splits)
+        self._all_to_all("yrecv", "yback", recv, send)
+        # 11. weighted combine of the k expert outputs
+        for r in self.local_ranks:
+            b = self.buf[r]
+            N.check(L.smoe_combine_rows(N.ptr(b["yback"]), N.ptr(b["pos"]), N.ptr(b["w"]),
+                                        cnt_h[r], k, d, N.ptr(b["out"]), sp), "combine")
+        # 12. all-gather and restore the original order
+        full = self._all_gather_out(group)
+        out = t.empty((n, d), dtype=t.bfloat16, device=dev)
+        N.check(L.smoe_gather_rows(N.ptr(full), full.shape[0], 2, d, N.ptr(inv), n, 0, 0,
+                                   N.ptr(out), 0, sp), "resume")
+        self.last = {"counts": C, "group": group, "send_splits": send}
+        return out
+
+    def stats(self) -> dict:
+        s = self.stats_t.cpu().numpy()
+        loc, rem = int(s[0]), int(s[1])
+        row = 2 * self.d
+        return {"local_tokens": loc, "remote_tokens": rem,
+                "measured_alpha": loc / max(loc + rem, 1),
+                "bytes": {"all_reduce": None, "a2a_dispatch": rem * row, "a2a_combine": rem * row}}

@@ -323,3 +323,45 @@ extern "C" int smoe_layer_forward(smoe_layer* L, const int64_t* tokens, const in
   }
   return SMOE_OK;
 }
+
+// ---------------------------------------------------------------- single-rank C-ABI
+extern "C" int smoe_gate_topk(const void* h, int64_t rows, int32_t hidden, const void* w_gate,
+                              const float* b_gate, int32_t n_experts, int32_t top_k,
+                              int32_t renormalize, const int32_t* expert_owner, int32_t my_shard,
+                              int32_t* topk_ids, float* topk_w, int64_t* stats, void* stream) {
+  if (rows < 0 || !w_gate || !expert_owner || !topk_ids || !topk_w) return SMOE_ERR_INVALID_ARG;
+  if (rows == 0) return SMOE_OK;
+  if (!h) return SMOE_ERR_INVALID_ARG;
+  LocalRows lr{};
+  lr.counts = nullptr;
+  lr.single_rows = rows;
+  lr.shard_begin = my_shard;     // locality: expert_owner[e] == my_shard
+  lr.shard_count = 1;
+  lr.n_shards = my_shard + 1;
+  ShardPtrs hp{}, ip{}, wp{};
+  hp.p[0] = static_cast<char*>(const_cast<void*>(h));
+  ip.p[0] = reinterpret_cast<char*>(topk_ids);
+  wp.p[0] = reinterpret_cast<char*>(topk_w);
+  return launch_gate(lr, hp, hidden, w_gate, b_gate, n_experts, top_k, renormalize, expert_owner,
+                     ip, wp, stats, rows, as_stream(stream));
+}
+
+extern "C" int smoe_pair_offsets(const int32_t* topk_ids, int64_t rows, int32_t top_k,
+                                 int32_t n_experts, int32_t* pair_pos, int32_t* counts,
+                                 void* stream) {
+  if (rows < 0 || !counts || (rows > 0 && (!topk_ids || !pair_pos))) return SMOE_ERR_INVALID_ARG;
+  return launch_pair_offsets(topk_ids, rows, top_k, n_experts, pair_pos, counts, as_stream(stream));
+}
+
+extern "C" int smoe_pack_rows(const void* src, int64_t rows, int32_t top_k, int32_t hidden,
+                              const int32_t* pair_pos, void* dst, void* stream) {
+  if (rows < 0 || (rows > 0 && (!src || !pair_pos || !dst))) return SMOE_ERR_INVALID_ARG;
+  return launch_pack_rows(src, rows, top_k, hidden, pair_pos, dst, as_stream(stream));
+}
+
+extern "C" int smoe_combine_rows(const void* y, const int32_t* pair_pos, const float* topk_w,
+                                 int64_t rows, int32_t top_k, int32_t hidden, void* out,
+                                 void* stream) {
+  if (rows < 0 || (rows > 0 && (!y || !pair_pos || !topk_w || !out))) return SMOE_ERR_INVALID_ARG;
+  return launch_combine_rows(y, pair_pos, topk_w, rows, top_k, hidden, out, as_stream(stream));
+}

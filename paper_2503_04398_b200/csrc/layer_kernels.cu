@@ -37,7 +37,11 @@ struct RowMap {
 };
 
 __device__ __forceinline__ void load_rowmap(RowMap& rm, const LocalRows& lr) {
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && lr.counts == nullptr) {
+    rm.cnt[0] = (int32_t)lr.single_rows;
+    rm.total = (int32_t)lr.single_rows;
+    rm.group = 0;
+  } else if (threadIdx.x == 0) {
     int32_t t = 0;
     for (int i = 0; i < lr.shard_count; ++i) {
       rm.cnt[i] = lr.counts[lr.shard_begin + i];
@@ -263,10 +267,11 @@ gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ 
 // token); the CUDA-core version above is compute-bound for N = 64.  H rows and
 // W rows stream through a 4-stage cp.async ring in 128-B rows with a 16-B XOR
 // swizzle (conflict-free ldmatrix).
-constexpr int kMmaRows = 32;
 constexpr int kMmaKC = 64;                       // bf16 per row per stage (128 B)
-constexpr int kMmaStages = 6;
-constexpr int kMmaThreads = 64;
+constexpr int kMmaStages = 4;
+// rows per CTA: 16 per warp; more rows amortise the W tile (N x 64) over the
+// CTA when N is large, fewer keep more CTAs (bytes in flight) when N is small
+__host__ __device__ constexpr int mma_rows(int nt) { return nt <= 2 ? 64 : 128; }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
@@ -289,12 +294,14 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1
 __device__ __forceinline__ uint32_t swz(int r, int c) { return r * 128 + ((c ^ (r & 7)) << 4); }
 
 template <int NT>   // NT = N / 8 n-tiles
-__global__ void __launch_bounds__(kMmaThreads)
+__global__ void __launch_bounds__(mma_rows(NT) * 2)
 gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ w_gate,
                 const float* __restrict__ b_gate, int32_t k, int32_t renorm,
                 const int32_t* __restrict__ slot_owner, ShardPtrs topk_ids, ShardPtrs topk_w,
                 int64_t* stats) {
   constexpr int N = NT * 8;
+  constexpr int kMmaRows = mma_rows(NT);
+  constexpr int kMmaThreads = kMmaRows * 2;                     // 16 rows per warp
   constexpr int kMmaStageBytes = (kMmaRows + N) * kMmaKC * 2;   // H rows + W rows, 128 B each
   extern __shared__ __align__(128) uint8_t gsm[];
   __shared__ RowMap rm;
@@ -450,14 +457,15 @@ static int launch_gate_mma(const LocalRows& lr, const ShardPtrs& hs, int64_t d, 
                            const float* b, int32_t k, int32_t renorm, const int32_t* owner,
                            const ShardPtrs& ids, const ShardPtrs& wts, int64_t* stats,
                            int64_t n_rows_bound, cudaStream_t st) {
-  const size_t smem = (size_t)kMmaStages * ((kMmaRows + NT * 8) * kMmaKC * 2);
+  constexpr int rows = mma_rows(NT);
+  const size_t smem = (size_t)kMmaStages * ((rows + NT * 8) * kMmaKC * 2);
   static bool attr = false;
   if (!attr) {
     SMOE_CUDA_TRY(cudaFuncSetAttribute(gate_mma_kernel<NT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  gate_mma_kernel<NT><<<grid_cap(ceil_div(n_rows_bound, kMmaRows), 8), kMmaThreads, smem, st>>>(
+  gate_mma_kernel<NT><<<grid_cap(ceil_div(n_rows_bound, rows), 4), rows * 2, smem, st>>>(
       lr, hs, d, static_cast<const char*>(w), b, k, renorm, owner, ids, wts, stats);
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
@@ -685,6 +693,113 @@ int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtr
 #undef SMOE_CMB_CASE
     default: return SMOE_ERR_UNSUPPORTED;
   }
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
+// ------------------------------------------------------------------ single-rank helpers
+// Pair offsets in expert-major send order (DS-MoE all2allv packing):
+//   pos(j, s) = sum_{e' < e} counts[e'] + #{earlier pairs with the same expert e}
+__global__ void __launch_bounds__(kRouteThreads)
+pair_offsets_kernel(const int32_t* __restrict__ ids, int64_t P, int32_t N,
+                    int32_t* __restrict__ pos, int32_t* __restrict__ counts) {
+  __shared__ int32_t s_run[kGateMaxN];
+  __shared__ int32_t s_w[32 * kGateMaxN];
+  __shared__ int32_t s_base[kGateMaxN];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < N; e += kRouteThreads) s_run[e] = 0;
+  for (int e = tid; e < 32 * N; e += kRouteThreads) s_w[e] = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < P; base += kRouteThreads) {
+    const int64_t p = base + tid;
+    const int32_t e = p < P ? ids[p] : -1;
+    const uint32_t peers = __match_any_sync(0xffffffffu, e);
+    const int32_t rw = __popc(peers & lanemask_lt());
+    if (e >= 0 && lane == __ffs(peers) - 1) s_w[warp * N + e] = __popc(peers);
+    __syncthreads();
+    if (e >= 0) {
+      int32_t r = s_run[e] + rw;
+      for (int w = 0; w < warp; ++w) r += s_w[w * N + e];
+      pos[p] = r;
+    }
+    __syncthreads();
+    for (int ee = tid; ee < N; ee += kRouteThreads) {
+      int32_t s = 0;
+      for (int w = 0; w < 32; ++w) { s += s_w[w * N + ee]; s_w[w * N + ee] = 0; }
+      s_run[ee] += s;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    int32_t acc = 0;
+    for (int e = 0; e < N; ++e) { s_base[e] = acc; acc += s_run[e]; }
+  }
+  __syncthreads();
+  for (int e = tid; e < N; e += kRouteThreads) counts[e] = s_run[e];
+  for (int64_t p = tid; p < P; p += kRouteThreads) pos[p] += s_base[ids[p]];
+}
+
+int launch_pair_offsets(const int32_t* topk_ids, int64_t rows, int32_t k, int32_t N,
+                        int32_t* pair_pos, int32_t* counts, cudaStream_t st) {
+  if (N > kGateMaxN) return SMOE_ERR_UNSUPPORTED;
+  pair_offsets_kernel<<<1, kRouteThreads, 0, st>>>(topk_ids, rows * k, N, pair_pos, counts);
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
+__global__ void __launch_bounds__(256)
+pack_rows_kernel(const char* __restrict__ src, int64_t P, int32_t k, int64_t d,
+                 const int32_t* __restrict__ pos, char* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t vecs = d / 8;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t p = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); p < P;
+       p += nwarps) {
+    const char* s = src + (p / k) * d * 2;
+    char* o = dst + (int64_t)pos[p] * d * 2;
+    for (int64_t v = lane; v < vecs; v += 32) st_v4(o + v * 16, ld_nc_v4(s + v * 16));
+  }
+}
+
+int launch_pack_rows(const void* src, int64_t rows, int32_t k, int64_t d, const int32_t* pair_pos,
+                     void* dst, cudaStream_t st) {
+  if (d % 8) return SMOE_ERR_UNSUPPORTED;
+  if (rows <= 0) return SMOE_OK;
+  pack_rows_kernel<<<grid_cap(ceil_div(rows * k, 8), 16), 256, 0, st>>>(
+      static_cast<const char*>(src), rows * k, k, d, pair_pos, static_cast<char*>(dst));
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
+__global__ void __launch_bounds__(256)
+combine_rows_kernel(const char* __restrict__ y, const int32_t* __restrict__ pos,
+                    const float* __restrict__ topk_w, int64_t rows, int32_t k, int64_t d,
+                    char* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t vecs = d / 8;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); j < rows;
+       j += nwarps) {
+    for (int64_t v = lane; v < vecs; v += 32) {
+      float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int s = 0; s < k; ++s) {
+        float t[8];
+        set_bf16x8(t, ld_nc_v4(y + ((int64_t)pos[j * k + s] * d + v * 8) * 2));
+        const float w = topk_w[j * k + s];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) a[c] += w * t[c];
+      }
+      st_v4(out + (j * d + v * 8) * 2, pack_bf16x8(a));
+    }
+  }
+}
+
+int launch_combine_rows(const void* y, const int32_t* pair_pos, const float* topk_w, int64_t rows,
+                        int32_t k, int64_t d, void* out, cudaStream_t st) {
+  if (d % 8) return SMOE_ERR_UNSUPPORTED;
+  if (rows <= 0) return SMOE_OK;
+  combine_rows_kernel<<<grid_cap(ceil_div(rows, 8), 16), 256, 0, st>>>(
+      static_cast<const char*>(y), pair_pos, topk_w, rows, k, d, static_cast<char*>(out));
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }

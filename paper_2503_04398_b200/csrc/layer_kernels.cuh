@@ -15,6 +15,7 @@ struct LocalRows {
   const int64_t* group;      // [1] max group
   const int64_t* forward;    // [G * max_tokens]
   int32_t shard_begin, shard_count, n_shards;
+  int64_t single_rows;       // counts == nullptr: one block of `single_rows` rows (shard 0)
 };
 
 int launch_srs(const LocalRows& lr, const ShardPtrs& partials, int64_t d, const ShardPtrs& hs,
@@ -39,6 +40,14 @@ int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
 int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtrs& ypair,
                        const ShardPtrs& topk_w, const ShardPtrs& outs, int64_t n_rows_bound,
                        cudaStream_t st);
+
+// Single-rank building blocks (DS-MoE baseline, smoe_gate_topk & co.)
+int launch_pair_offsets(const int32_t* topk_ids, int64_t rows, int32_t k, int32_t N,
+                        int32_t* pair_pos, int32_t* counts, cudaStream_t st);
+int launch_pack_rows(const void* src, int64_t rows, int32_t k, int64_t d, const int32_t* pair_pos,
+                     void* dst, cudaStream_t st);
+int launch_combine_rows(const void* y, const int32_t* pair_pos, const float* topk_w, int64_t rows,
+                        int32_t k, int64_t d, void* out, cudaStream_t st);
 
 int launch_barrier(const ShardPtrs& signals, int32_t world, int32_t rank, uint32_t* my_signal,
                    uint32_t* epoch, cudaStream_t st);

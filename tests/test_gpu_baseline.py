@@ -1,0 +1,36 @@
+"""DS-MoE baseline pipeline (AR -> A2A -> A2A -> AG) vs the fp32 oracle, and
+its event counts vs the reference's ds_moe layout (comm.py:200-202)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import layer_ref, scheduler_ref as R
+from paper_2503_04398_b200 import synth
+from paper_2503_04398_b200.baseline import DSMoELayer
+
+
+@pytest.mark.parametrize("n,over", [(300, {"G": 2, "N": 8}), (1000, {"G": 8, "N": 16}),
+                                    (777, {"G": 8, "N": 64, "k": 6, "d": 512, "f": 256})])
+def test_dsmoe_matches_oracle(n, over):
+    w = synth.make_workload("toy", n=n, eps=0.3, seed=n, cfg_override=over)
+    G, k = w.cfg["G"], w.cfg["k"]
+    b = w.bundle
+    ref = layer_ref.layer_forward(partials=w.partials, tokens=w.tokens, hist=w.hist,
+                                  t_labels=b.token_table.labels, t_conf=b.token_table.confidence,
+                                  a_best=b.ngram_table.best, a_conf=b.ngram_table.confidence,
+                                  n_clusters=G, expert_labels=w.expert_labels, gate_w=w.gate_w,
+                                  w1=w.w1, w3=w.w3, w2=w.w2, k=k)
+    layer = DSMoELayer(w.gate_w, w.w1, w.w3, w.w2, n_ranks=G, top_k=k, max_tokens=n)
+    parts = [torch.from_numpy(w.partials[g]).cuda().to(torch.bfloat16) for g in range(G)]
+    out = layer.forward(parts, n).float().cpu().numpy()
+    err = np.linalg.norm(out - ref["out"]) / np.linalg.norm(ref["out"])
+    assert err <= 1e-2, err
+    st = layer.stats()
+    loc, rem = R.simulate_counts(w.tokens, ref["experts"], "ds_moe", G, w.cfg["N"])
+    assert (st["local_tokens"], st["remote_tokens"]) == (loc, rem)
+    # the per-expert routed counts equal the oracle's expert histogram
+    C = layer.last["counts"]
+    assert np.array_equal(C.sum(0), np.bincount(ref["experts"].ravel(), minlength=w.cfg["N"]))
