@@ -40,7 +40,7 @@ sys.path.insert(0, str(ROOT))
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="smoe", choices=["smoe", "reference"])
     p.add_argument("--config", default="mixtral")
@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU baseline work")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-dsmoe", action="store_true", help="skip the DS-MoE baseline timing")
     return p.parse_args()
 
 
@@ -81,7 +82,7 @@ class Clocks:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
                 stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -335,6 +336,41 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(out_h.numel() * 2),
                "steps": ksteps, "api": "SpecMoELayer.forward(host pinned partials, ids, hist)"}
 
+    # ---------------- DS-MoE pipeline baseline (AR -> A2A -> A2A -> AG), same kernels
+    dsm = None
+    if not args.no_dsmoe and world in (1, G):
+        from paper_2503_04398_b200.baseline import DSMoELayer
+        base = DSMoELayer(w.gate_w, w.w1, w.w3, w.w2, n_ranks=G, top_k=k, max_tokens=n,
+                          distributed=world > 1)
+        parts = [layer.partial_views(n)[i] for i in range(L)]
+        for _ in range(max(2, args.warmup)):
+            base.forward(parts, n)
+        barrier()
+        torch.cuda.synchronize()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        bsteps = max(3, args.steps // 2)
+        b0.record(stream)
+        for _ in range(bsteps):
+            base.forward(parts, n)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        b_ms = b0.elapsed_time(b1)
+        if world > 1:
+            t = torch.tensor([b_ms], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            b_ms = float(t.item())
+        bst = base.stats()
+        dsm = {"value": n * bsteps / (b_ms / 1e3), "unit": "tokens/s",
+               "ms_per_step": b_ms / bsteps, "local_activation_rate": bst["measured_alpha"],
+               "a2a_bytes_per_step": bst["bytes"]["a2a_dispatch"] * 2,
+               "impl": "NCCL all_reduce / all_to_all_single / all_gather_into_tensor"
+                       if world > 1 else f"{G} ranks emulated on one GPU (collectives = "
+                                         "device copies)",
+               "speedup_smoe_over_dsmoe": (n * args.steps / (ms_total / 1e3)) /
+                                          (n * bsteps / (b_ms / 1e3))}
+        del base, parts
+        torch.cuda.empty_cache()
+
     # ---------------- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -369,7 +405,7 @@ def main():
                            "peak_src": pk["src"] + " sustained",
                            "down_gemm_tflops": down_flops / (down_ms / 1e3) / 1e12,
                            "layer_tflops": (up_flops + down_flops) / (ms_step / 1e3) / 1e12},
-              "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
+              "e2e": e2e, "cpu_baseline": cpu, "dsmoe_baseline": dsm, "clocks": clocks,
               "gpu_launches": launches_per_step * args.steps})
     if world > 1:
         torch.distributed.destroy_process_group()
