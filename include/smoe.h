@@ -190,6 +190,10 @@ enum {
   SMOE_BUF_WORKSPACE,     /* bytes: smoe_layer_workspace_bytes()                     */
   SMOE_BUF_PROBLEMS,      /* bytes: grouped-GEMM problem table, 64 KiB               */
   SMOE_BUF_EPOCH,         /* uint32 [1]: barrier epoch (device)                      */
+  SMOE_BUF_HIST_OUT,      /* peer, one per process (optional): int64 [max_tokens, h]  */
+                          /* next layer's n-gram window = this window shifted by one  */
+                          /* plus the cluster of each token's top-1 expert            */
+                          /* (predictor.py:165-166)                                   */
   SMOE_BUF__COUNT
 };
 

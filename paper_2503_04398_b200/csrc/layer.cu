@@ -305,8 +305,17 @@ extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tok
       return smoe_layer_barrier(L, stream);
     }
     case SMOE_STAGE_COMBINE_SAG: {
+      HistUpdate hu{};
+      hu.hist_in = hist;
+      hu.hist_len = L->hist_len;
+      hu.slot_owner = L->slot_owner_d;
+      hu.topk_ids = local_ptrs(L, SMOE_BUF_TOPK_IDS);
+      hu.n_hist_outs = 0;
+      if (L->buf[SMOE_BUF_HIST_OUT][0] && hu.hist_len > 0 && hu.hist_len <= 32)
+        hu.hist_outs = distinct_ptrs(L, SMOE_BUF_HIST_OUT, &hu.n_hist_outs);
       rc = launch_combine_sag(lr, c.top_k, c.hidden, resident_ptrs(L, SMOE_BUF_YPAIR),
-                              local_ptrs(L, SMOE_BUF_TOPK_W), peer_ptrs(L, SMOE_BUF_OUT), n, st);
+                              local_ptrs(L, SMOE_BUF_TOPK_W), peer_ptrs(L, SMOE_BUF_OUT), hu, n,
+                              st);
       if (rc) return rc;
       return smoe_layer_barrier(L, stream);
     }

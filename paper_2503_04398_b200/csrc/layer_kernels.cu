@@ -635,7 +635,7 @@ int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
 template <int G>
 __global__ void __launch_bounds__(256)
 combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtrs topk_w,
-                   ShardPtrs outs) {
+                   ShardPtrs outs, HistUpdate hu) {
   __shared__ RowMap rm;
   load_rowmap(rm, lr);
   const int lane = threadIdx.x & 31;
@@ -650,6 +650,20 @@ combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtr
     decode_row(rm, lr.shard_count, q, gl, j);
     const int64_t g = lr.shard_begin + gl;
     const int64_t i = lr.forward[g * rm.group + j];    // original token position
+    if (hu.n_hist_outs > 0 && lane < hu.hist_len) {
+      // next layer's window: drop the oldest digit, append the cluster of the
+      // top-1 expert (the device of this routing event, predictor.py:165-166)
+      const int64_t L = hu.hist_len;
+      int64_t v;
+      if (lane == L - 1) {
+        const int32_t top1 = reinterpret_cast<const int32_t*>(hu.topk_ids.p[gl])[j * k];
+        v = hu.slot_owner[top1];
+      } else {
+        v = hu.hist_in ? hu.hist_in[i * L + lane + 1] : g;   // no history yet: this shard
+      }
+      for (int b = 0; b < hu.n_hist_outs; ++b)
+        reinterpret_cast<int64_t*>(hu.hist_outs.p[b])[i * L + lane] = v;
+    }
     const float* w = reinterpret_cast<const float*>(topk_w.p[gl]) + j * k;
     float wk[kGateMaxK];
 #pragma unroll
@@ -678,14 +692,14 @@ combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtr
 }
 
 int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtrs& ypair,
-                       const ShardPtrs& topk_w, const ShardPtrs& outs, int64_t n_rows_bound,
-                       cudaStream_t st) {
+                       const ShardPtrs& topk_w, const ShardPtrs& outs, const HistUpdate& hu,
+                       int64_t n_rows_bound, cudaStream_t st) {
   if (k > kGateMaxK || d % 8) return SMOE_ERR_UNSUPPORTED;
   if (n_rows_bound <= 0) return SMOE_OK;
   const int grid = grid_cap(ceil_div(n_rows_bound, 8), 16);
   switch (lr.n_shards) {
 #define SMOE_CMB_CASE(G_) \
-    case G_: combine_sag_kernel<G_><<<grid, 256, 0, st>>>(lr, k, d, ypair, topk_w, outs); break;
+    case G_: combine_sag_kernel<G_><<<grid, 256, 0, st>>>(lr, k, d, ypair, topk_w, outs, hu); break;
     SMOE_CMB_CASE(1) SMOE_CMB_CASE(2) SMOE_CMB_CASE(3) SMOE_CMB_CASE(4) SMOE_CMB_CASE(5)
     SMOE_CMB_CASE(6) SMOE_CMB_CASE(7) SMOE_CMB_CASE(8) SMOE_CMB_CASE(9) SMOE_CMB_CASE(10)
     SMOE_CMB_CASE(11) SMOE_CMB_CASE(12) SMOE_CMB_CASE(13) SMOE_CMB_CASE(14) SMOE_CMB_CASE(15)

@@ -37,9 +37,18 @@ int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
                     int64_t expert_rows, int64_t* problems, int32_t* err, int64_t n_rows_bound,
                     cudaStream_t st);
 
+struct HistUpdate {
+  const int64_t* hist_in;     // [n, hist_len] or nullptr (first layers)
+  ShardPtrs hist_outs;        // one [n, hist_len] int64 buffer per process (SAG of the history)
+  int32_t n_hist_outs;        // 0: not requested
+  int32_t hist_len;
+  const int32_t* slot_owner;  // [N] cluster of each expert slot
+  ShardPtrs topk_ids;         // per resident shard [n, k]
+};
+
 int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtrs& ypair,
-                       const ShardPtrs& topk_w, const ShardPtrs& outs, int64_t n_rows_bound,
-                       cudaStream_t st);
+                       const ShardPtrs& topk_w, const ShardPtrs& outs, const HistUpdate& hu,
+                       int64_t n_rows_bound, cudaStream_t st);
 
 // Single-rank building blocks (DS-MoE baseline, smoe_gate_topk & co.)
 int launch_pair_offsets(const int32_t* topk_ids, int64_t rows, int32_t k, int32_t N,

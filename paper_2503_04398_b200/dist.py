@@ -71,7 +71,8 @@ class ShardGroup:
         handles = self._allgather(self._ipc_handle(ptr))
         return [ptr if r == self.rank else self._ipc_open(hb) for r, hb in enumerate(handles)]
 
-    def peer_tables(self, G: int, n_experts: int, per_shard: dict) -> tuple[dict, dict]:
+    def peer_tables(self, G: int, n_experts: int, per_shard: dict,
+                    per_process: dict | None = None) -> tuple[dict, dict]:
         """Allocate this process's share of every peer buffer and build the
         per-shard pointer tables (shard g lives on process g // L at offset
         (g % L) * size).  Returns (tables, local base pointers)."""
@@ -82,7 +83,8 @@ class ShardGroup:
             bases = self._exchange(base)
             peer[name] = [bases[g // L] + (g % L) * size for g in range(G)]
             local[name] = base
-        for name, size in (("counts", G * n_experts * 4), ("signal", 64 * 4)):
+        procs = {"counts": G * n_experts * 4, "signal": 64 * 4, **(per_process or {})}
+        for name, size in procs.items():
             base = self._alloc(size)
             bases = self._exchange(base)
             peer[name] = [bases[g // L] for g in range(G)]
@@ -95,7 +97,8 @@ class ShardGroup:
         n, d, k, R = layer.max_tokens, layer.d, layer.k, layer.expert_rows
         per_shard = {"partial": n * d * 2, "xin": R * d * 2, "xmeta": R * 8,
                      "ypair": n * k * d * 2, "out": n * d * 2}
-        peer, local = self.peer_tables(G, layer.N, per_shard)
+        h = max(int(layer.tables.ngram_n), 1)
+        peer, local = self.peer_tables(G, layer.N, per_shard, {"hist": n * h * 8})
 
         def tensor(ptr, shape, typestr):
             return torch.as_tensor(_CudaArray(ptr, shape, typestr), device=device)
@@ -104,6 +107,7 @@ class ShardGroup:
         peer["partial_local"] = tensor(local["partial"], (L, n, d), "<i2").view(torch.bfloat16)
         peer["out_local"] = tensor(local["out"], (L, n, d), "<i2").view(torch.bfloat16)
         peer["counts_local"] = tensor(local["counts"], (G, layer.N), "<i4")
+        peer["hist_local"] = tensor(local["hist"], (n, h), "<i8")
         tensor(local["signal"], (64,), "<i4").zero_()
         peer["partial_local"].zero_()
         torch.cuda.synchronize()

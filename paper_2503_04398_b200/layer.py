@@ -108,18 +108,21 @@ class SpecMoELayer:
             self.ypair = t.empty((G, n * k, d), dtype=bf, device=dev)
             self.out = t.empty((G, n, d), dtype=bf, device=dev)
             self.counts_mat = t.zeros((G, self.N), dtype=t.int32, device=dev)
+            self.hist_next = t.zeros((n, max(self.tables.ngram_n, 1)), dtype=t.int64, device=dev)
             peer = {"partial": [self.partial[g] for g in range(G)],
                     "xin": [self.xin[g] for g in range(G)],
                     "xmeta": [self.xmeta[g] for g in range(G)],
                     "ypair": [self.ypair[g] for g in range(G)],
                     "out": [self.out[g] for g in range(G)],
                     "counts": [self.counts_mat] * G,
+                    "hist": [self.hist_next] * G,
                     "signal": [None] * G}
         else:
             peer = self.group.alloc_layer_buffers(self, dev)
             self.partial = peer["partial_local"]
             self.out = peer["out_local"]
             self.counts_mat = peer["counts_local"]
+            self.hist_next = peer["hist_local"]
         self._peer = peer
         self.hs = t.empty((L, n, d), dtype=bf, device=dev)
         self.topk_ids = t.empty((L, n, k), dtype=t.int32, device=dev)
@@ -161,6 +164,7 @@ class SpecMoELayer:
             bind(N.BUF_YPAIR, g, p["ypair"][g])
             bind(N.BUF_OUT, g, p["out"][g])
             bind(N.BUF_COUNTS, g, p["counts"][g])
+            bind(N.BUF_HIST_OUT, g, p["hist"][g])
             if p["signal"][g] is not None:
                 bind(N.BUF_SIGNAL, g, p["signal"][g])
         for i in range(self.shard_count):
@@ -224,6 +228,13 @@ class SpecMoELayer:
         if self.group is None:
             return self.out[g, :n]
         return self.out[g - self.shard_begin, :n]
+
+    def next_history(self, n: int):
+        """[n, h] device view of the n-gram window for the NEXT MoE layer,
+        written by the last forward: this window shifted by one layer plus the
+        cluster of each token's top-1 expert (predictor.py:165-166).  Without
+        an input history the older digits are the token's shard this layer."""
+        return self.hist_next[:n]
 
     def forward(self, hidden_partials, token_ids, histories=None, out=None):
         """Full layer from user tensors (host or device).

@@ -87,3 +87,63 @@ def test_layer_repeatable_and_graph_capturable():
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(layer.out_view(256), a)
+
+
+def _oracle(w, hist, **kw):
+    b = w.bundle
+    return layer_ref.layer_forward(
+        partials=w.partials, tokens=w.tokens, hist=hist, t_labels=b.token_table.labels,
+        t_conf=b.token_table.confidence, a_best=b.ngram_table.best,
+        a_conf=b.ngram_table.confidence, n_clusters=w.cfg["G"], expert_labels=w.expert_labels,
+        gate_w=w.gate_w, w1=w.w1, w3=w.w3, w2=w.w2, k=w.cfg["k"], **kw)
+
+
+def test_layer_bias_no_renorm_no_history():
+    w = synth.make_workload("toy", n=400, eps=0.2, seed=9, cfg_override={"G": 4, "N": 16})
+    bias = np.random.default_rng(0).normal(scale=0.05, size=16).astype(np.float32)
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=400,
+                         gate_b=bias, renormalize=False)
+    out = layer.forward(torch.from_numpy(w.partials), w.tokens, None).float().numpy()
+    ref = _oracle(w, None, renorm=False, bias=bias)
+    assert np.array_equal(layer.plan_indices(400).forward, ref["forward"])
+    r = layer.routing(400)
+    assert np.array_equal(r["experts"], ref["experts"])
+    assert np.allclose(r["weights"], ref["weights"], rtol=1e-4, atol=1e-6)
+    assert np.linalg.norm(out - ref["out"]) / np.linalg.norm(ref["out"]) <= TOL
+
+
+def test_layer_empty_batch():
+    w = synth.make_workload("toy", n=8, eps=0.2, seed=2)
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=64)
+    out = layer.forward(torch.zeros((2, 0, 256), dtype=torch.bfloat16), np.zeros(0, np.int64),
+                        np.zeros((0, 2), np.int64))
+    assert tuple(out.shape) == (0, 256)
+    assert layer.stats()["local_tokens"] == 0
+
+
+def test_layer_history_chain():
+    """§8f rank 1: the n-gram window for the next layer is produced on the GPU
+    (shift + cluster of the top-1 expert, predictor.py:165-166) and drives the
+    next layer's lookup."""
+    over = {"G": 4, "N": 16}
+    w1 = synth.make_workload("toy", n=500, eps=0.3, seed=21, cfg_override=over)
+    layer = SpecMoELayer(w1.bundle, w1.gate_w, w1.w1, w1.w3, w1.w2, top_k=2, max_tokens=500)
+    layer.forward(torch.from_numpy(w1.partials), w1.tokens, w1.hist)
+    ref1 = _oracle(w1, w1.hist)
+    labels = np.asarray(w1.expert_labels)
+    want = np.concatenate([w1.hist[:, 1:], labels[ref1["experts"][:, :1]]], axis=1)
+    nh = layer.next_history(500).cpu().numpy()
+    assert np.array_equal(nh, want)
+    # layer 2 consumes it (same tables, new hidden states)
+    w2 = synth.make_workload("toy", n=500, eps=0.3, seed=22, cfg_override=over)
+    w2.bundle, w2.tokens = w1.bundle, w1.tokens
+    out2 = layer.forward(torch.from_numpy(w2.partials), w2.tokens,
+                         layer.next_history(500).clone())
+    ref2 = layer_ref.layer_forward(
+        partials=w2.partials, tokens=w2.tokens, hist=want, t_labels=w1.bundle.token_table.labels,
+        t_conf=w1.bundle.token_table.confidence, a_best=w1.bundle.ngram_table.best,
+        a_conf=w1.bundle.ngram_table.confidence, n_clusters=4, expert_labels=labels,
+        gate_w=w1.gate_w, w1=w1.w1, w3=w1.w3, w2=w1.w2, k=2)
+    assert np.array_equal(layer.plan_indices(500).forward, ref2["forward"])
+    o = out2.float().numpy()
+    assert np.linalg.norm(o - ref2["out"]) / np.linalg.norm(ref2["out"]) <= TOL
