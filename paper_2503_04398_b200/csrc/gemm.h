@@ -37,6 +37,10 @@ struct GemmArgs {
 int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols,
                    int32_t box_rows);
 
+// Rows of B staged per CTA per k-block (256, or 128 with the SM-pair MMA):
+// the box height of B's tensor map.
+int gemm_b_box_rows();
+
 int launch_grouped_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap_b,
                         const GemmArgs& args, int32_t epilogue, cudaStream_t stream);
 

@@ -23,22 +23,30 @@
 #include "common.cuh"
 #include "gemm.h"
 #include <algorithm>
+#include <cstdlib>
 
 namespace smoe {
 
-constexpr int kStages = 4;
 constexpr int kThreads = 256;
-constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2;    // 16 KiB
-constexpr uint32_t kBBytes = kGemmBN * kGemmBK * 2;    // 32 KiB
-constexpr uint32_t kStageBytes = kABytes + kBBytes;
+constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2;    // 16 KiB: 128 A rows x 64 K per CTA
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kStagingBytes = 4 * 32 * 64;        // 4 epilogue warps x 32 rows x 64 B
-constexpr size_t kGemmSmem = 1024 /*align slack*/ + kStages * kStageBytes + kStagingBytes +
-                             1024 /*barriers*/ + kGemmMaxProblems * 32 + 4 * (kGemmMaxProblems + 1);
 
-// instruction descriptor: D f32, A/B bf16, K-major both, N=256, M=128
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) |
-                            (uint32_t(kGemmBN >> 3) << 17) | (uint32_t(kGemmBM >> 4) << 24);
+// Per cta_group: CG = 1 (one SM, tile 128 x 256) or CG = 2 (an SM pair, tile
+// 256 x 256: each CTA stages 128 A rows and half of the 256 B rows, the
+// leader issues tcgen05.mma.cta_group::2 over both CTAs' shared memory).
+template <int CG> struct GemmShape {
+  static constexpr uint32_t kBBytes = (kGemmBN / CG) * kGemmBK * 2;   // B rows staged per CTA
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = CG == 1 ? 4 : 6;
+  static constexpr int kTileM = kGemmBM * CG;
+  static constexpr size_t kSmem = 1024 + kStages * kStageBytes + kStagingBytes + 1024 +
+                                  kGemmMaxProblems * 32 + 4 * (kGemmMaxProblems + 1);
+  // instruction descriptor: D f32, A/B bf16, K-major both, N = 256, M = 128 * CG
+  static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) |
+                                     (uint32_t(kGemmBN >> 3) << 17) |
+                                     (uint32_t((kGemmBM * CG) >> 4) << 24);
+};
 
 // ---------------------------------------------------------------- PTX glue
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -88,6 +96,45 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
       :: "r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+__device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* map,
+                                                uint32_t bar_cluster, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];"
+      :: "r"(dst), "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void tc_mma_cg2(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      :: "r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit_cg2_mc(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" :: "r"(bar), "h"(mask) : "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(bar_cluster)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 // K-major, 128B-swizzled operand tile: 8-row core groups 1024 B apart.
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
@@ -128,12 +175,13 @@ struct TileCoord {
 // and m varies fastest inside a group: the CTAs of one wave share a few weight
 // tiles (n-blocks) and sweep the group's A rows, so A is read from DRAM once
 // and B once per group.
+template <int TILE_M>
 __device__ __forceinline__ TileCoord decode_tile(const SmemProblems& sp, int32_t np,
                                                  int32_t n_tiles_n, int32_t group_m, int32_t t,
                                                  int32_t& cursor) {
   while (cursor + 1 < np && sp.tile_prefix[cursor + 1] <= t) ++cursor;
   const int32_t local = t - sp.tile_prefix[cursor];
-  const int32_t mt = (sp.m[cursor] + kGemmBM - 1) / kGemmBM;
+  const int32_t mt = (sp.m[cursor] + TILE_M - 1) / TILE_M;
   const int32_t per_group = group_m * n_tiles_n;
   const int32_t g = local / per_group;
   const int32_t first_m = g * group_m;
@@ -146,16 +194,20 @@ __device__ __forceinline__ TileCoord decode_tile(const SmemProblems& sp, int32_t
   return c;
 }
 
-template <int EPI>
+template <int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                     const __grid_constant__ CUtensorMap tmap_b, const GemmArgs args) {
+  using S = GemmShape<CG>;
+  constexpr int kStages = S::kStages;
+  constexpr uint32_t kBBytes = S::kBBytes;
+  constexpr int kTileM = S::kTileM;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + kStages * kABytes;
-  uint8_t* staging = smem + kStages * kStageBytes;
+  uint8_t* staging = smem + kStages * S::kStageBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(staging + kStagingBytes);
   // bars: full[kStages], empty[kStages], tfull[2], tempty[2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
@@ -163,6 +215,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t np = args.num_problems;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;     // CTA rank inside the SM pair
+  const int32_t unit = blockIdx.x / CG, n_units = gridDim.x / CG;
 
   // ---- problem table -> shared, tile prefix
   for (int p = threadIdx.x; p < np; p += kThreads) {
@@ -178,7 +232,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     for (int p = 0; p < np; ++p) {
       sp.tile_prefix[p] = acc;
       const int32_t m = sp.m[p] > 0 ? sp.m[p] : 0;
-      acc += ((m + kGemmBM - 1) / kGemmBM) * args.n_tiles_n;
+      acc += ((m + kTileM - 1) / kTileM) * args.n_tiles_n;
     }
     sp.tile_prefix[np] = acc;
   }
@@ -189,7 +243,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_addr(&bars[2 * kStages + a]), 1);
-      mbar_init(smem_addr(&bars[2 * kStages + 2 + a]), 128);
+      mbar_init(smem_addr(&bars[2 * kStages + 2 + a]), 4 * CG);   // one arrival per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -198,12 +252,18 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     asm volatile("prefetch.tensormap [%0];" :: "l"(&tmap_b) : "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 :: "r"(smem_addr(tmem_holder)), "r"(kTmemCols) : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                   :: "r"(smem_addr(tmem_holder)), "r"(kTmemCols) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                   :: "r"(smem_addr(tmem_holder)), "r"(kTmemCols) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   const int32_t total_tiles = sp.tile_prefix[np];
@@ -214,31 +274,42 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
 
   if (warp == 0) {
     if (lane == 0) {
-      // ===== TMA producer =====
+      // ===== TMA producer (both CTAs of a pair; bytes land on the leader's barrier) =====
       int32_t stage = 0;
       uint32_t phase = 0;
       int32_t cursor = 0;
-      for (int32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        const TileCoord tc = decode_tile(sp, np, args.n_tiles_n, args.group_m, t, cursor);
-        const int32_t a_row = (int32_t)(sp.a_off[tc.p] + (int64_t)tc.m_blk * kGemmBM);
-        const int32_t b_row = sp.b_idx[tc.p] * args.n_b + tc.n_blk * kGemmBN;
+      for (int32_t t = unit; t < total_tiles; t += n_units) {
+        const TileCoord tc = decode_tile<kTileM>(sp, np, args.n_tiles_n, args.group_m, t, cursor);
+        const int32_t a_row =
+            (int32_t)(sp.a_off[tc.p] + (int64_t)tc.m_blk * kTileM + rank * kGemmBM);
+        const int32_t b_row =
+            sp.b_idx[tc.p] * args.n_b + tc.n_blk * kGemmBN + rank * (kGemmBN / CG);
         for (int32_t kb = 0; kb < args.num_k_blocks; ++kb) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
-          mbar_expect_tx(fb, kStageBytes);
-          tma_load_2d(smem_addr(smem_a + stage * kABytes), &tmap_a, fb, kb * kGemmBK, a_row);
-          tma_load_2d(smem_addr(smem_b + stage * kBBytes), &tmap_b, fb, kb * kGemmBK, b_row);
+          const uint32_t sa = smem_addr(smem_a + stage * kABytes);
+          const uint32_t sb = smem_addr(smem_b + stage * kBBytes);
+          if (CG == 1) {
+            mbar_expect_tx(fb, S::kStageBytes);
+            tma_load_2d(sa, &tmap_a, fb, kb * kGemmBK, a_row);
+            tma_load_2d(sb, &tmap_b, fb, kb * kGemmBK, b_row);
+          } else {
+            if (rank == 0) mbar_expect_tx(fb, 2 * S::kStageBytes);
+            const uint32_t fb0 = map_to_rank(fb, 0);
+            tma_load_2d_cg2(sa, &tmap_a, fb0, kb * kGemmBK, a_row);
+            tma_load_2d_cg2(sb, &tmap_b, fb0, kb * kGemmBK, b_row);
+          }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer =====
+    if (lane == 0 && rank == 0) {
+      // ===== MMA issuer (leader CTA only) =====
       int32_t stage = 0;
       uint32_t phase = 0;
       uint32_t acc = 0, acc_phase = 0;
-      for (int32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int32_t t = unit; t < total_tiles; t += n_units) {
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kGemmBN;
@@ -248,26 +319,30 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
           const uint64_t ad = sdesc(smem_addr(smem_a + stage * kABytes));
           const uint64_t bd = sdesc(smem_addr(smem_b + stage * kBBytes));
 #pragma unroll
-          for (int k = 0; k < kGemmBK / 16; ++k)   // +32 B per K=16 step inside the swizzle atom
-            tc_mma(d_tmem, ad + 2 * k, bd + 2 * k, kIdesc, (kb | k) != 0);
-          tc_commit(empty0 + 8 * stage);
+          for (int k = 0; k < kGemmBK / 16; ++k) {  // +32 B per K=16 step inside the swizzle atom
+            if (CG == 1) tc_mma(d_tmem, ad + 2 * k, bd + 2 * k, S::kIdesc, (kb | k) != 0);
+            else tc_mma_cg2(d_tmem, ad + 2 * k, bd + 2 * k, S::kIdesc, (kb | k) != 0);
+          }
+          if (CG == 1) tc_commit(empty0 + 8 * stage);
+          else tc_commit_cg2_mc(empty0 + 8 * stage, 0x3);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        tc_commit(tfull0 + 8 * acc);
+        if (CG == 1) tc_commit(tfull0 + 8 * acc);
+        else tc_commit_cg2_mc(tfull0 + 8 * acc, 0x3);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
     }
   } else if (warp >= 4) {
-    // ===== epilogue =====
+    // ===== epilogue (both CTAs: each owns 128 rows of the tile) =====
     const int ew = warp - 4;                          // TMEM lane quarter
     uint8_t* stg = staging + ew * (32 * 64);
     uint32_t acc = 0, acc_phase = 0;
     int32_t cursor = 0;
-    for (int32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      const TileCoord tc = decode_tile(sp, np, args.n_tiles_n, args.group_m, t, cursor);
+    for (int32_t t = unit; t < total_tiles; t += n_units) {
+      const TileCoord tc = decode_tile<kTileM>(sp, np, args.n_tiles_n, args.group_m, t, cursor);
       const int32_t m = sp.m[tc.p];
-      const int32_t row0 = tc.m_blk * kGemmBM + ew * 32;   // first row of this warp
+      const int32_t row0 = tc.m_blk * kTileM + rank * kGemmBM + ew * 32;   // first row of warp
       // per-lane destination row pointer (lane l <-> row row0 + l)
       char* my_row = nullptr;
       {
@@ -296,7 +371,6 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
           SMOE_TMEM_LD32(tbase + ch * 32, g);
           SMOE_TMEM_LD32(tbase + 128 + ch * 32, u);
           tmem_wait_ld();
-          if (ch == kChunks - 1) { tc_fence_before(); mbar_arrive(tempty0 + 8 * acc); }
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const float g0 = __uint_as_float(g[2 * j]), g1 = __uint_as_float(g[2 * j + 1]);
@@ -309,10 +383,18 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
           uint32_t v[32];
           SMOE_TMEM_LD32(tbase + ch * 32, v);
           tmem_wait_ld();
-          if (ch == kChunks - 1) { tc_fence_before(); mbar_arrive(tempty0 + 8 * acc); }
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             packed[j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+        }
+        if (ch == kChunks - 1) {
+          // this warp has read its accumulator lanes: release them to the MMA issuer
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (CG == 1) mbar_arrive(tempty0 + 8 * acc);
+            else mbar_arrive_cluster(map_to_rank(tempty0 + 8 * acc, 0));
+          }
         }
         // stage row `lane` (64 B = 4 x 16 B chunks, XOR-swizzled against bank conflicts)
 #pragma unroll
@@ -342,11 +424,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
-                 :: "r"(tmem_base), "r"(kTmemCols) : "memory");
+    if (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
+                   :: "r"(tmem_base), "r"(kTmemCols) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;"
+                   :: "r"(tmem_base), "r"(kTmemCols) : "memory");
   }
 }
 
@@ -385,35 +471,68 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t col
   return r == CUDA_SUCCESS ? SMOE_OK : SMOE_ERR_CUDA;
 }
 
-template <int EPI>
+template <int EPI, int CG>
 static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args,
                        cudaStream_t st) {
+  using S = GemmShape<CG>;
   static bool attr_set = false;
   if (!attr_set) {
-    SMOE_CUDA_TRY(cudaFuncSetAttribute(grouped_gemm_kernel<EPI>,
+    SMOE_CUDA_TRY(cudaFuncSetAttribute(grouped_gemm_kernel<EPI, CG>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)kGemmSmem));
+                                       (int)S::kSmem));
     attr_set = true;
   }
   GemmArgs g = args;
   if (g.group_m <= 0) {
-    // keep a group's A rows (128 x K bf16 per m-block) within ~40 MB of L2
-    const int64_t a_blk = (int64_t)kGemmBM * g.num_k_blocks * kGemmBK * 2;
+    // keep a group's A rows (tile_m x K bf16 per m-block) within ~40 MB of L2
+    const int64_t a_blk = (int64_t)S::kTileM * g.num_k_blocks * kGemmBK * 2;
     g.group_m = (int32_t)std::max<int64_t>(1, (40ll << 20) / a_blk);
   }
-  grouped_gemm_kernel<EPI><<<num_sms(), kThreads, kGemmSmem, st>>>(a, b, g);
+  const int grid = (num_sms() / CG) * CG;
+  if (CG == 1) {
+    grouped_gemm_kernel<EPI, 1><<<grid, kThreads, S::kSmem, st>>>(a, b, g);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = S::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SMOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<EPI, 2>, a, b, g));
+  }
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }
+
+static int gemm_cta_group() {
+  static int cg = 0;
+  if (!cg) {
+    const char* e = getenv("SMOE_GEMM_CTA_GROUP");
+    cg = (e && e[0] == '1') ? 1 : 2;
+  }
+  return cg;
+}
+
+int gemm_b_box_rows() { return kGemmBN / gemm_cta_group(); }
 
 int launch_grouped_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args,
                         int32_t epilogue, cudaStream_t st) {
   if (args.num_problems <= 0) return SMOE_OK;
   if (args.num_problems > kGemmMaxProblems) return SMOE_ERR_UNSUPPORTED;
+  const bool pair = gemm_cta_group() == 2;
   switch (epilogue) {
-    case kEpiStore: return launch_impl<kEpiStore>(a, b, args, st);
-    case kEpiSwiGLU: return launch_impl<kEpiSwiGLU>(a, b, args, st);
-    case kEpiScatter: return launch_impl<kEpiScatter>(a, b, args, st);
+    case kEpiStore: return pair ? launch_impl<kEpiStore, 2>(a, b, args, st)
+                                : launch_impl<kEpiStore, 1>(a, b, args, st);
+    case kEpiSwiGLU: return pair ? launch_impl<kEpiSwiGLU, 2>(a, b, args, st)
+                                 : launch_impl<kEpiSwiGLU, 1>(a, b, args, st);
+    case kEpiScatter: return pair ? launch_impl<kEpiScatter, 2>(a, b, args, st)
+                                  : launch_impl<kEpiScatter, 1>(a, b, args, st);
     default: return SMOE_ERR_INVALID_ARG;
   }
 }
@@ -464,7 +583,7 @@ extern "C" int smoe_grouped_gemm(const void* A, int64_t a_rows, int64_t K, const
   CUtensorMap ta, tb;
   int rc = make_tmap_bf16(&ta, A, a_rows, K, kGemmBM);
   if (rc) return rc;
-  rc = make_tmap_bf16(&tb, B, b_rows, K, kGemmBN);
+  rc = make_tmap_bf16(&tb, B, b_rows, K, gemm_b_box_rows());
   if (rc) return rc;
   GemmArgs args{};
   args.problems = problems;

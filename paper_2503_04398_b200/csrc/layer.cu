@@ -195,9 +195,10 @@ static int ensure_maps(smoe_layer* L) {
   if ((rc = make_tmap_bf16(&L->map_x, L->buf[SMOE_BUF_XIN][c.shard_begin], rows, c.hidden,
                            kGemmBM)))
     return rc;
-  if ((rc = make_tmap_bf16(&L->map_w13, L->w13, nl * 2 * c.ffn, c.hidden, kGemmBN))) return rc;
+  if ((rc = make_tmap_bf16(&L->map_w13, L->w13, nl * 2 * c.ffn, c.hidden, gemm_b_box_rows())))
+    return rc;
   if ((rc = make_tmap_bf16(&L->map_h, L->buf[SMOE_BUF_HMID][0], rows, c.ffn, kGemmBM))) return rc;
-  if ((rc = make_tmap_bf16(&L->map_w2, L->w2, nl * c.hidden, c.ffn, kGemmBN))) return rc;
+  if ((rc = make_tmap_bf16(&L->map_w2, L->w2, nl * c.hidden, c.ffn, gemm_b_box_rows()))) return rc;
   L->maps_ready = true;
   return SMOE_OK;
 }
