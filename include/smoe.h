@@ -51,6 +51,10 @@ extern "C" {
 #define SMOE_MAX_PLAN_DEVICES 1024  /* n_devices supported by rebatch plan   */
 
 const char* smoe_version(void);
+/* Process-wide tuning switches. */
+#define SMOE_OPT_GEMM_CTA_GROUP 0   /* 1: 128x256 tile per SM, 2: 256x256 per SM pair */
+int smoe_set_option(int32_t key, int32_t value);
+int smoe_get_option(int32_t key);
 const char* smoe_status_string(int status);
 /* 1 when the current device is sm_100 (B200) and the kernels can run. */
 int smoe_device_ok(void);

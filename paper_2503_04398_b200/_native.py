@@ -22,6 +22,8 @@ SIGNATURES = [
     ("smoe_version", C.c_char_p, []),
     ("smoe_status_string", C.c_char_p, [C.c_int]),
     ("smoe_device_ok", C.c_int, []),
+    ("smoe_set_option", C.c_int, [c_i32, c_i32]),
+    ("smoe_get_option", C.c_int, [c_i32]),
     ("smoe_lookup_devices", C.c_int,
      [P, c_i64, P, c_i32, P, P, c_i64, P, P, c_i64, c_i32, P, P, P]),
     ("smoe_plan_workspace_bytes", c_sz, [c_i64, c_i32]),
@@ -66,6 +68,7 @@ ERRBIT_HISTORY_RANGE = 8
 ERRBIT_INDEX_RANGE = 16
 ERRBIT_CAPACITY = 32
 MAX_SHARDS = 16
+OPT_GEMM_CTA_GROUP = 0
 
 (BUF_PARTIAL, BUF_XIN, BUF_XMETA, BUF_YPAIR, BUF_OUT, BUF_COUNTS, BUF_SIGNAL, BUF_HS,
  BUF_TOPK_IDS, BUF_TOPK_W, BUF_PAIR_RANK, BUF_HMID, BUF_FORWARD, BUF_INVERSE, BUF_DEV,

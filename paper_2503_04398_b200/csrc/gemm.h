@@ -40,6 +40,8 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t col
 // Rows of B staged per CTA per k-block (256, or 128 with the SM-pair MMA):
 // the box height of B's tensor map.
 int gemm_b_box_rows();
+int gemm_cta_group();            // 1: one SM per tile, 2: SM pair (tcgen05 cta_group::2)
+void set_gemm_cta_group(int cg);
 
 int launch_grouped_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap_b,
                         const GemmArgs& args, int32_t epilogue, cudaStream_t stream);

@@ -510,14 +510,17 @@ static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
   return SMOE_OK;
 }
 
-static int gemm_cta_group() {
-  static int cg = 0;
-  if (!cg) {
+static int g_cta_group = 0;   // 0: not chosen yet (env SMOE_GEMM_CTA_GROUP, default 1)
+
+int gemm_cta_group() {
+  if (!g_cta_group) {
     const char* e = getenv("SMOE_GEMM_CTA_GROUP");
-    cg = (e && e[0] == '1') ? 1 : 2;
+    g_cta_group = (e && e[0] == '2') ? 2 : 1;
   }
-  return cg;
+  return g_cta_group;
 }
+
+void set_gemm_cta_group(int cg) { g_cta_group = (cg == 2) ? 2 : 1; }
 
 int gemm_b_box_rows() { return kGemmBN / gemm_cta_group(); }
 

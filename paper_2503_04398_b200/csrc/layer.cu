@@ -37,6 +37,7 @@ struct smoe_layer {
   const void* w2 = nullptr;
   // GEMM descriptors
   bool maps_ready = false;
+  int maps_cta_group = 0;
   CUtensorMap map_x, map_w13, map_h, map_w2;
 };
 
@@ -185,7 +186,7 @@ static int check_bound(const smoe_layer* L) {
 }
 
 static int ensure_maps(smoe_layer* L) {
-  if (L->maps_ready) return SMOE_OK;
+  if (L->maps_ready && L->maps_cta_group == gemm_cta_group()) return SMOE_OK;
   int rc = check_bound(L);
   if (rc) return rc;
   if (!L->w13 || !L->w2 || !L->w_gate || !L->t_labels) return SMOE_ERR_INVALID_ARG;
@@ -200,6 +201,7 @@ static int ensure_maps(smoe_layer* L) {
   if ((rc = make_tmap_bf16(&L->map_h, L->buf[SMOE_BUF_HMID][0], rows, c.ffn, kGemmBM))) return rc;
   if ((rc = make_tmap_bf16(&L->map_w2, L->w2, nl * c.hidden, c.ffn, gemm_b_box_rows()))) return rc;
   L->maps_ready = true;
+  L->maps_cta_group = gemm_cta_group();
   return SMOE_OK;
 }
 
@@ -374,4 +376,19 @@ extern "C" int smoe_combine_rows(const void* y, const int32_t* pair_pos, const f
                                  void* stream) {
   if (rows < 0 || (rows > 0 && (!y || !pair_pos || !topk_w || !out))) return SMOE_ERR_INVALID_ARG;
   return launch_combine_rows(y, pair_pos, topk_w, rows, top_k, hidden, out, as_stream(stream));
+}
+
+extern "C" int smoe_set_option(int32_t key, int32_t value) {
+  switch (key) {
+    case SMOE_OPT_GEMM_CTA_GROUP:
+      if (value != 1 && value != 2) return SMOE_ERR_INVALID_ARG;
+      set_gemm_cta_group(value);
+      return SMOE_OK;
+    default:
+      return SMOE_ERR_INVALID_ARG;
+  }
+}
+
+extern "C" int smoe_get_option(int32_t key) {
+  return key == SMOE_OPT_GEMM_CTA_GROUP ? gemm_cta_group() : -1;
 }
