@@ -68,7 +68,7 @@ ERRBIT_HISTORY_RANGE = 8
 ERRBIT_INDEX_RANGE = 16
 ERRBIT_CAPACITY = 32
 MAX_SHARDS = 16
-OPT_GEMM_CTA_GROUP = 0
+OPT_GEMM_CTA_GROUP_UP, OPT_GEMM_CTA_GROUP_DOWN = 0, 1
 
 (BUF_PARTIAL, BUF_XIN, BUF_XMETA, BUF_YPAIR, BUF_OUT, BUF_COUNTS, BUF_SIGNAL, BUF_HS,
  BUF_TOPK_IDS, BUF_TOPK_W, BUF_PAIR_RANK, BUF_HMID, BUF_FORWARD, BUF_INVERSE, BUF_DEV,

@@ -37,13 +37,14 @@ struct GemmArgs {
 int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols,
                    int32_t box_rows);
 
-// Rows of B staged per CTA per k-block (256, or 128 with the SM-pair MMA):
-// the box height of B's tensor map.
-int gemm_b_box_rows();
-int gemm_cta_group();            // 1: one SM per tile, 2: SM pair (tcgen05 cta_group::2)
-void set_gemm_cta_group(int cg);
+// cta_group of the up (which = 0) / down (which = 1) GEMM: 1 = one SM per
+// 128x256 tile, 2 = SM pair per 256x256 tile (tcgen05 cta_group::2).
+int gemm_cta_group(int which);
+void set_gemm_cta_group(int which, int cg);
+// Rows of B staged per CTA per k-block: the box height of B's tensor map.
+int gemm_b_box_rows(int cg);
 
 int launch_grouped_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap_b,
-                        const GemmArgs& args, int32_t epilogue, cudaStream_t stream);
+                        const GemmArgs& args, int32_t epilogue, int cg, cudaStream_t stream);
 
 }  // namespace smoe

@@ -510,25 +510,21 @@ static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
   return SMOE_OK;
 }
 
-static int g_cta_group = 0;   // 0: not chosen yet (env SMOE_GEMM_CTA_GROUP, default 1)
+// cta_group per GEMM kind (SMOE_OPT_GEMM_CTA_GROUP_UP / _DOWN).  Measured on
+// B200 (tools/gemm_ab.py, interleaved): the SM pair is ~10% faster for the
+// down projection (K = f, scatter epilogue) and neutral for the SwiGLU up
+// projection, so the defaults are up = 1, down = 2.
+static int g_cta_group[2] = {1, 2};
 
-int gemm_cta_group() {
-  if (!g_cta_group) {
-    const char* e = getenv("SMOE_GEMM_CTA_GROUP");
-    g_cta_group = (e && e[0] == '2') ? 2 : 1;
-  }
-  return g_cta_group;
-}
-
-void set_gemm_cta_group(int cg) { g_cta_group = (cg == 2) ? 2 : 1; }
-
-int gemm_b_box_rows() { return kGemmBN / gemm_cta_group(); }
+int gemm_cta_group(int which) { return g_cta_group[which ? 1 : 0]; }
+void set_gemm_cta_group(int which, int cg) { g_cta_group[which ? 1 : 0] = (cg == 2) ? 2 : 1; }
+int gemm_b_box_rows(int cg) { return kGemmBN / cg; }
 
 int launch_grouped_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args,
-                        int32_t epilogue, cudaStream_t st) {
+                        int32_t epilogue, int cg, cudaStream_t st) {
   if (args.num_problems <= 0) return SMOE_OK;
   if (args.num_problems > kGemmMaxProblems) return SMOE_ERR_UNSUPPORTED;
-  const bool pair = gemm_cta_group() == 2;
+  const bool pair = cg == 2;
   switch (epilogue) {
     case kEpiStore: return pair ? launch_impl<kEpiStore, 2>(a, b, args, st)
                                 : launch_impl<kEpiStore, 1>(a, b, args, st);
@@ -586,7 +582,8 @@ extern "C" int smoe_grouped_gemm(const void* A, int64_t a_rows, int64_t K, const
   CUtensorMap ta, tb;
   int rc = make_tmap_bf16(&ta, A, a_rows, K, kGemmBM);
   if (rc) return rc;
-  rc = make_tmap_bf16(&tb, B, b_rows, K, gemm_b_box_rows());
+  const int cg = gemm_cta_group(epilogue == kEpiSwiGLU ? 0 : 1);
+  rc = make_tmap_bf16(&tb, B, b_rows, K, gemm_b_box_rows(cg));
   if (rc) return rc;
   GemmArgs args{};
   args.problems = problems;
@@ -596,5 +593,5 @@ extern "C" int smoe_grouped_gemm(const void* A, int64_t a_rows, int64_t K, const
   args.n_b = (int32_t)n_b;
   args.c = static_cast<char*>(C);
   args.ldc = ldc;
-  return launch_grouped_gemm(ta, tb, args, epilogue, as_stream(stream));
+  return launch_grouped_gemm(ta, tb, args, epilogue, cg, as_stream(stream));
 }

@@ -37,7 +37,7 @@ struct smoe_layer {
   const void* w2 = nullptr;
   // GEMM descriptors
   bool maps_ready = false;
-  int maps_cta_group = 0;
+  int maps_cg_up = 0, maps_cg_down = 0;
   CUtensorMap map_x, map_w13, map_h, map_w2;
 };
 
@@ -186,7 +186,9 @@ static int check_bound(const smoe_layer* L) {
 }
 
 static int ensure_maps(smoe_layer* L) {
-  if (L->maps_ready && L->maps_cta_group == gemm_cta_group()) return SMOE_OK;
+  if (L->maps_ready && L->maps_cg_up == gemm_cta_group(0) &&
+      L->maps_cg_down == gemm_cta_group(1))
+    return SMOE_OK;
   int rc = check_bound(L);
   if (rc) return rc;
   if (!L->w13 || !L->w2 || !L->w_gate || !L->t_labels) return SMOE_ERR_INVALID_ARG;
@@ -196,12 +198,16 @@ static int ensure_maps(smoe_layer* L) {
   if ((rc = make_tmap_bf16(&L->map_x, L->buf[SMOE_BUF_XIN][c.shard_begin], rows, c.hidden,
                            kGemmBM)))
     return rc;
-  if ((rc = make_tmap_bf16(&L->map_w13, L->w13, nl * 2 * c.ffn, c.hidden, gemm_b_box_rows())))
+  if ((rc = make_tmap_bf16(&L->map_w13, L->w13, nl * 2 * c.ffn, c.hidden,
+                           gemm_b_box_rows(gemm_cta_group(0)))))
     return rc;
   if ((rc = make_tmap_bf16(&L->map_h, L->buf[SMOE_BUF_HMID][0], rows, c.ffn, kGemmBM))) return rc;
-  if ((rc = make_tmap_bf16(&L->map_w2, L->w2, nl * c.hidden, c.ffn, gemm_b_box_rows()))) return rc;
+  if ((rc = make_tmap_bf16(&L->map_w2, L->w2, nl * c.hidden, c.ffn,
+                           gemm_b_box_rows(gemm_cta_group(1)))))
+    return rc;
   L->maps_ready = true;
-  L->maps_cta_group = gemm_cta_group();
+  L->maps_cg_up = gemm_cta_group(0);
+  L->maps_cg_down = gemm_cta_group(1);
   return SMOE_OK;
 }
 
@@ -291,7 +297,7 @@ extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tok
       a.n_b = 2 * c.ffn;
       a.c = static_cast<char*>(L->buf[SMOE_BUF_HMID][0]);
       a.ldc = c.ffn;
-      return launch_grouped_gemm(L->map_x, L->map_w13, a, kEpiSwiGLU, st);
+      return launch_grouped_gemm(L->map_x, L->map_w13, a, kEpiSwiGLU, L->maps_cg_up, st);
     }
     case SMOE_STAGE_EXPERT_DOWN: {
       GemmArgs a{};
@@ -303,7 +309,7 @@ extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tok
       a.meta = static_cast<const int64_t*>(L->buf[SMOE_BUF_XMETA][c.shard_begin]);
       for (int g = 0; g < c.n_shards; ++g) a.dst_base[g] = static_cast<char*>(L->buf[SMOE_BUF_YPAIR][g]);
       a.ldd = c.hidden;
-      rc = launch_grouped_gemm(L->map_h, L->map_w2, a, kEpiScatter, st);
+      rc = launch_grouped_gemm(L->map_h, L->map_w2, a, kEpiScatter, L->maps_cg_down, st);
       if (rc) return rc;
       return smoe_layer_barrier(L, stream);
     }
@@ -380,9 +386,10 @@ extern "C" int smoe_combine_rows(const void* y, const int32_t* pair_pos, const f
 
 extern "C" int smoe_set_option(int32_t key, int32_t value) {
   switch (key) {
-    case SMOE_OPT_GEMM_CTA_GROUP:
+    case SMOE_OPT_GEMM_CTA_GROUP_UP:
+    case SMOE_OPT_GEMM_CTA_GROUP_DOWN:
       if (value != 1 && value != 2) return SMOE_ERR_INVALID_ARG;
-      set_gemm_cta_group(value);
+      set_gemm_cta_group(key == SMOE_OPT_GEMM_CTA_GROUP_DOWN, value);
       return SMOE_OK;
     default:
       return SMOE_ERR_INVALID_ARG;
@@ -390,5 +397,7 @@ extern "C" int smoe_set_option(int32_t key, int32_t value) {
 }
 
 extern "C" int smoe_get_option(int32_t key) {
-  return key == SMOE_OPT_GEMM_CTA_GROUP ? gemm_cta_group() : -1;
+  if (key == SMOE_OPT_GEMM_CTA_GROUP_UP) return gemm_cta_group(0);
+  if (key == SMOE_OPT_GEMM_CTA_GROUP_DOWN) return gemm_cta_group(1);
+  return -1;
 }

@@ -9,6 +9,18 @@ pytestmark = pytest.mark.gpu
 from paper_2503_04398_b200 import _native as N
 
 
+@pytest.fixture(params=[1, 2], ids=["cta_group1", "cta_group2"], autouse=True)
+def cta_group(request):
+    """Run every GEMM test with the one-SM and the SM-pair MMA variants."""
+    lib = N.lib()
+    old = [lib.smoe_get_option(k) for k in (N.OPT_GEMM_CTA_GROUP_UP, N.OPT_GEMM_CTA_GROUP_DOWN)]
+    for k in (N.OPT_GEMM_CTA_GROUP_UP, N.OPT_GEMM_CTA_GROUP_DOWN):
+        N.check(lib.smoe_set_option(k, request.param), "set_option")
+    yield request.param
+    for k, v in zip((N.OPT_GEMM_CTA_GROUP_UP, N.OPT_GEMM_CTA_GROUP_DOWN), old):
+        lib.smoe_set_option(k, v)
+
+
 def run_gemm(A, B, problems, n_b, epilogue, c_cols):
     lib = N.lib()
     C = torch.zeros((A.shape[0], c_cols), dtype=torch.bfloat16, device="cuda")

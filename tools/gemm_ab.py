@@ -27,7 +27,8 @@ def main(name="mixtral", tokens=16384, reps=6, steps=5):
     ref = None
     for rep in range(reps):
         for cg in (1, 2) if rep % 2 == 0 else (2, 1):
-            N.check(lib.smoe_set_option(N.OPT_GEMM_CTA_GROUP, cg), "set_option")
+            for key in (N.OPT_GEMM_CTA_GROUP_UP, N.OPT_GEMM_CTA_GROUP_DOWN):
+                N.check(lib.smoe_set_option(key, cg), "set_option")
             layer.run_device(tok, hist)       # warm (maps rebuilt on switch)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             up = dn = 0.0
