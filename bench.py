@@ -234,6 +234,11 @@ def main():
         return run_reference(args, world, rank)
 
     import torch
+    # SMOE_BENCH_SAME_GPU=1 (tests only): every rank on cuda:0 with gloo for the
+    # host plumbing, so the multi-process path can be exercised on one GPU.
+    same_gpu = os.environ.get("SMOE_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     from paper_2503_04398_b200 import SpecMoELayer, synth
     from paper_2503_04398_b200 import _native as N
@@ -241,7 +246,11 @@ def main():
     group = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if same_gpu:
+            dist.init_process_group("gloo")
+            args.no_dsmoe = True            # NCCL cannot put two ranks on one GPU
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         from paper_2503_04398_b200.dist import ShardGroup
         group = ShardGroup.from_torch_distributed()
 
@@ -263,6 +272,13 @@ def main():
     def barrier():
         if world > 1:
             torch.distributed.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cpu" if same_gpu else "cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
 
     # ---------------- device-resident timed region (value + roofline)
     for _ in range(args.warmup):
@@ -291,19 +307,25 @@ def main():
     ms_total = start.elapsed_time(end)
     up_ms = np.mean([ev[s][0].elapsed_time(ev[s][1]) for s in range(args.steps)])
     down_ms = np.mean([ev[s][1].elapsed_time(ev[s][2]) for s in range(args.steps)])
-    if world > 1:
-        t = torch.tensor([ms_total], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_total = float(t.item())
+    ms_total = max_over_ranks(ms_total)
     layer.check_errors()
     st = layer.stats(n)
+    if world > 1:                        # pair counts of this process's shards -> whole job
+        lr = [float(st["local_tokens"]), float(st["remote_tokens"])]
+        tot = torch.tensor(lr, device="cpu" if same_gpu else "cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tot)
+        st["local_tokens"], st["remote_tokens"] = int(tot[0].item()), int(tot[1].item())
+        st["measured_alpha"] = st["local_tokens"] / max(st["local_tokens"] + st["remote_tokens"], 1)
     ms_step = ms_total / args.steps
     value = n * args.steps / (ms_total / 1e3)
-    rows = st["local_tokens"] + st["remote_tokens"]           # (token, expert) pairs
-    local_rows = rows if world == 1 else None
+    # rows the expert GEMMs of THIS process multiplied = pairs routed to its expert slots
+    cm = layer.counts_mat.cpu().numpy()
+    e0 = int(layer.slot_first[layer.shard_begin])
+    e1 = int(layer.slot_first[layer.shard_begin + layer.shard_count])
+    gemm_rows = float(cm[:, e0:e1].sum())
     pk = peaks()
-    up_flops = 2.0 * rows * d * (2 * f) / world
-    down_flops = 2.0 * rows * f * d / world
+    up_flops = 2.0 * gemm_rows * d * (2 * f)
+    down_flops = 2.0 * gemm_rows * f * d
     achieved = up_flops / (up_ms / 1e3) / 1e12
     clocks = clk.summary()
 
@@ -327,10 +349,7 @@ def main():
         e_end.record(stream)
         torch.cuda.synchronize()
         e_ms = max(e_start.elapsed_time(e_end), 1e3 * (time.perf_counter() - t0))
-        if world > 1:
-            t = torch.tensor([e_ms], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e_ms = float(t.item())
+        e_ms = max_over_ranks(e_ms)
         h2d = host_p.numel() * 2 + host_tok.numel() * 8 + host_hist.numel() * 8
         e2e = {"value": n * ksteps / (e_ms / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(out_h.numel() * 2),
@@ -355,10 +374,7 @@ def main():
         b1.record(stream)
         torch.cuda.synchronize()
         b_ms = b0.elapsed_time(b1)
-        if world > 1:
-            t = torch.tensor([b_ms], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            b_ms = float(t.item())
+        b_ms = max_over_ranks(b_ms)
         bst = base.stats()
         dsm = {"value": n * bsteps / (b_ms / 1e3), "unit": "tokens/s",
                "ms_per_step": b_ms / bsteps, "local_activation_rate": bst["measured_alpha"],
