@@ -193,15 +193,12 @@ enum {
   SMOE_BUF_STATS,         /* int64 [16]: see SMOE_STAT_*                             */
   SMOE_BUF_ERR,           /* int32 [1]                                               */
   SMOE_BUF_WORKSPACE,     /* bytes: smoe_layer_workspace_bytes()                     */
-  SMOE_BUF_PROBLEMS,      /* int64 [256, 8]: grouped-GEMM problem table              */
+  SMOE_BUF_PROBLEMS,      /* bytes: grouped-GEMM problem table, 64 KiB               */
   SMOE_BUF_EPOCH,         /* uint32 [1]: barrier epoch (device)                      */
   SMOE_BUF_HIST_OUT,      /* peer, one per process (optional): int64 [max_tokens, h]  */
                           /* next layer's n-gram window = this window shifted by one  */
                           /* plus the cluster of each token's top-1 expert            */
                           /* (predictor.py:165-166)                                   */
-  SMOE_BUF_XSRC,          /* local, once: int32 [shard_count * expert_rows]: source   */
-                          /* row (in the resident shards' HS arena) of every expert   */
-                          /* input row the up-GEMM gathers instead of a dispatch copy */
   SMOE_BUF__COUNT
 };
 

@@ -73,7 +73,7 @@ OPT_GEMM_CTA_GROUP_UP, OPT_GEMM_CTA_GROUP_DOWN = 0, 1
 (BUF_PARTIAL, BUF_XIN, BUF_XMETA, BUF_YPAIR, BUF_OUT, BUF_COUNTS, BUF_SIGNAL, BUF_HS,
  BUF_TOPK_IDS, BUF_TOPK_W, BUF_PAIR_RANK, BUF_HMID, BUF_FORWARD, BUF_INVERSE, BUF_DEV,
  BUF_PLAN_COUNTS, BUF_GROUP, BUF_STATS, BUF_ERR, BUF_WORKSPACE, BUF_PROBLEMS,
- BUF_EPOCH, BUF_HIST_OUT, BUF_XSRC) = range(24)
+ BUF_EPOCH, BUF_HIST_OUT) = range(23)
 STAT_LOCAL_PAIRS, STAT_REMOTE_PAIRS, STAT_SRS_ROWS, STAT_GROUP = range(4)
 STAT_COUNT = 16
 (STAGE_PLAN, STAGE_SRS, STAGE_GATE, STAGE_ROUTE, STAGE_DISPATCH, STAGE_EXPERT_UP,

@@ -20,8 +20,7 @@ constexpr int kGemmMaxProblems = 256;
 constexpr int64_t kMetaSlotMask = (int64_t(1) << 40) - 1;
 
 struct GemmArgs {
-  const int64_t* problems;   // [P, stride] {a_off, m, b_index, c_off[, gathered rows]}
-  int32_t problem_stride;    // 4, or 8 with the gathered-rows column
+  const int64_t* problems;   // [P, 4] {a_off, m, b_index, c_off}
   int32_t num_problems;
   int32_t num_k_blocks;      // K / 64
   int32_t n_tiles_n;         // n_b / 256
@@ -32,10 +31,6 @@ struct GemmArgs {
   const int64_t* meta;       // scatter: per A row
   char* dst_base[SMOE_MAX_SHARDS];
   int64_t ldd;               // elements
-  // gather mode (up-GEMM of the layer, cta_group 1 only): rows [0, gathered)
-  // of a problem come from tmap_g at row xsrc[a_off + r] (-1: zeros), the
-  // rest from tmap_a at row a_off + r; both maps have box height 1 (gather4).
-  const int32_t* xsrc;
 };
 
 // Encodes a 2D bf16 K-major tensor map (rows x cols, box 64 x box_rows, 128B swizzle).
@@ -50,7 +45,6 @@ void set_gemm_cta_group(int which, int cg);
 int gemm_b_box_rows(int cg);
 
 int launch_grouped_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap_b,
-                        const GemmArgs& args, int32_t epilogue, int cg, cudaStream_t stream,
-                        const CUtensorMap* tmap_g = nullptr);
+                        const GemmArgs& args, int32_t epilogue, int cg, cudaStream_t stream);
 
 }  // namespace smoe

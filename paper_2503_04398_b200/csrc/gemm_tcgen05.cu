@@ -41,7 +41,7 @@ template <int CG> struct GemmShape {
   static constexpr int kStages = CG == 1 ? 4 : 6;
   static constexpr int kTileM = kGemmBM * CG;
   static constexpr size_t kSmem = 1024 + kStages * kStageBytes + kStagingBytes + 1024 +
-                                  kGemmMaxProblems * 36 + 4 * (kGemmMaxProblems + 1);
+                                  kGemmMaxProblems * 32 + 4 * (kGemmMaxProblems + 1);
   // instruction descriptor: D f32, A/B bf16, K-major both, N = 256, M = 128 * CG
   static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) |
                                      (uint32_t(kGemmBN >> 3) << 17) |
@@ -95,17 +95,6 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
       :: "r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-// TMA tile::gather4: four arbitrary rows (box height 1) into 4 x 128 B of
-// shared memory; the 128B swizzle follows the destination address, so 32
-// gathers into consecutive 512 B slots form the canonical 128-row tile.
-__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, uint32_t bar,
-                                            int32_t col, int32_t r0, int32_t r1, int32_t r2,
-                                            int32_t r3) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];"
-      :: "r"(dst), "l"(map), "r"(bar), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3) : "memory");
 }
 __device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* map,
                                                 uint32_t bar_cluster, int32_t c0, int32_t c1) {
@@ -174,7 +163,6 @@ struct SmemProblems {
   int64_t c_off[kGemmMaxProblems];
   int32_t m[kGemmMaxProblems];
   int32_t b_idx[kGemmMaxProblems];
-  int32_t gathered[kGemmMaxProblems];
   int32_t tile_prefix[kGemmMaxProblems + 1];
 };
 
@@ -209,8 +197,7 @@ __device__ __forceinline__ TileCoord decode_tile(const SmemProblems& sp, int32_t
 template <int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
-                    const __grid_constant__ CUtensorMap tmap_b,
-                    const __grid_constant__ CUtensorMap tmap_g, const GemmArgs args) {
+                    const __grid_constant__ CUtensorMap tmap_b, const GemmArgs args) {
   using S = GemmShape<CG>;
   constexpr int kStages = S::kStages;
   constexpr uint32_t kBBytes = S::kBBytes;
@@ -233,12 +220,11 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
 
   // ---- problem table -> shared, tile prefix
   for (int p = threadIdx.x; p < np; p += kThreads) {
-    const int64_t* q = args.problems + (int64_t)args.problem_stride * p;
+    const int64_t* q = args.problems + 4 * p;
     sp.a_off[p] = q[0];
     sp.m[p] = (int32_t)q[1];
     sp.b_idx[p] = (int32_t)q[2];
     sp.c_off[p] = q[3];
-    sp.gathered[p] = args.problem_stride >= 5 ? (int32_t)q[4] : 0;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -287,40 +273,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
   const uint32_t tempty0 = smem_addr(&bars[2 * kStages + 2]);
 
   if (warp == 0) {
-    const bool gather = (CG == 1) && args.xsrc != nullptr;
-    if (gather) {
-      // ===== gather producer (whole warp): lane l stages rows 4l..4l+3 of the
-      // A tile with one gather4; lane 0 arms the barrier and loads B =====
-      if (lane == 0) asm volatile("prefetch.tensormap [%0];" :: "l"(&tmap_g) : "memory");
-      int32_t stage = 0;
-      uint32_t phase = 0;
-      int32_t cursor = 0;
-      for (int32_t t = unit; t < total_tiles; t += n_units) {
-        const TileCoord tc = decode_tile<kTileM>(sp, np, args.n_tiles_n, args.group_m, t, cursor);
-        const int64_t a_off = sp.a_off[tc.p];
-        const int32_t r0 = tc.m_blk * kTileM + lane * 4;
-        const bool from_src = r0 < sp.gathered[tc.p];      // 4-row groups never straddle
-        int32_t c[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          c[i] = from_src ? __ldg(args.xsrc + a_off + r0 + i) : (int32_t)(a_off + r0 + i);
-        const CUtensorMap* map = from_src ? &tmap_g : &tmap_a;
-        const int32_t b_row = sp.b_idx[tc.p] * args.n_b + tc.n_blk * kGemmBN;
-        for (int32_t kb = 0; kb < args.num_k_blocks; ++kb) {
-          const uint32_t fb = full0 + 8 * stage;
-          if (lane == 0) {
-            mbar_wait(empty0 + 8 * stage, phase ^ 1);
-            mbar_expect_tx(fb, S::kStageBytes);
-          }
-          __syncwarp();
-          tma_gather4(smem_addr(smem_a + stage * kABytes) + lane * 512, map, fb, kb * kGemmBK,
-                      c[0], c[1], c[2], c[3]);
-          if (lane == 0)
-            tma_load_2d(smem_addr(smem_b + stage * kBBytes), &tmap_b, fb, kb * kGemmBK, b_row);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
-        }
-      }
-    } else if (lane == 0) {
+    if (lane == 0) {
       // ===== TMA producer (both CTAs of a pair; bytes land on the leader's barrier) =====
       int32_t stage = 0;
       uint32_t phase = 0;
@@ -397,11 +350,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         if (r < m) {
           if (EPI == kEpiScatter) {
             const int64_t meta = __ldg(args.meta + sp.a_off[tc.p] + r);
-            if (meta >= 0) {                                  // pad rows carry -1
-              const int32_t shard = (int32_t)(meta >> 40);
-              my_row = args.dst_base[shard] + ((meta & kMetaSlotMask) * args.ldd +
-                                                (int64_t)tc.n_blk * kGemmBN) * 2;
-            }
+            const int32_t shard = (int32_t)(meta >> 40);
+            my_row = args.dst_base[shard] + ((meta & kMetaSlotMask) * args.ldd +
+                                              (int64_t)tc.n_blk * kGemmBN) * 2;
           } else {
             const int64_t ncols = (EPI == kEpiSwiGLU) ? kGemmBN / 2 : kGemmBN;
             my_row = args.c + ((sp.c_off[tc.p] + r) * args.ldc + (int64_t)tc.n_blk * ncols) * 2;
@@ -521,8 +472,8 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t col
 }
 
 template <int EPI, int CG>
-static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& gm,
-                       const GemmArgs& args, cudaStream_t st) {
+static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args,
+                       cudaStream_t st) {
   using S = GemmShape<CG>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -539,7 +490,7 @@ static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const CUtenso
   }
   const int grid = (num_sms() / CG) * CG;
   if (CG == 1) {
-    grouped_gemm_kernel<EPI, 1><<<grid, kThreads, S::kSmem, st>>>(a, b, gm, g);
+    grouped_gemm_kernel<EPI, 1><<<grid, kThreads, S::kSmem, st>>>(a, b, g);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -553,7 +504,7 @@ static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const CUtenso
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    SMOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<EPI, 2>, a, b, gm, g));
+    SMOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<EPI, 2>, a, b, g));
   }
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
@@ -570,19 +521,17 @@ void set_gemm_cta_group(int which, int cg) { g_cta_group[which ? 1 : 0] = (cg ==
 int gemm_b_box_rows(int cg) { return kGemmBN / cg; }
 
 int launch_grouped_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args,
-                        int32_t epilogue, int cg, cudaStream_t st, const CUtensorMap* g) {
+                        int32_t epilogue, int cg, cudaStream_t st) {
   if (args.num_problems <= 0) return SMOE_OK;
   if (args.num_problems > kGemmMaxProblems) return SMOE_ERR_UNSUPPORTED;
-  if (args.xsrc && (cg != 1 || !g)) return SMOE_ERR_UNSUPPORTED;   // gather: one-SM tiles
-  const CUtensorMap& gm = g ? *g : a;
   const bool pair = cg == 2;
   switch (epilogue) {
-    case kEpiStore: return pair ? launch_impl<kEpiStore, 2>(a, b, gm, args, st)
-                                : launch_impl<kEpiStore, 1>(a, b, gm, args, st);
-    case kEpiSwiGLU: return pair ? launch_impl<kEpiSwiGLU, 2>(a, b, gm, args, st)
-                                 : launch_impl<kEpiSwiGLU, 1>(a, b, gm, args, st);
-    case kEpiScatter: return pair ? launch_impl<kEpiScatter, 2>(a, b, gm, args, st)
-                                  : launch_impl<kEpiScatter, 1>(a, b, gm, args, st);
+    case kEpiStore: return pair ? launch_impl<kEpiStore, 2>(a, b, args, st)
+                                : launch_impl<kEpiStore, 1>(a, b, args, st);
+    case kEpiSwiGLU: return pair ? launch_impl<kEpiSwiGLU, 2>(a, b, args, st)
+                                 : launch_impl<kEpiSwiGLU, 1>(a, b, args, st);
+    case kEpiScatter: return pair ? launch_impl<kEpiScatter, 2>(a, b, args, st)
+                                  : launch_impl<kEpiScatter, 1>(a, b, args, st);
     default: return SMOE_ERR_INVALID_ARG;
   }
 }
@@ -638,7 +587,6 @@ extern "C" int smoe_grouped_gemm(const void* A, int64_t a_rows, int64_t K, const
   if (rc) return rc;
   GemmArgs args{};
   args.problems = problems;
-  args.problem_stride = 4;
   args.num_problems = num_problems;
   args.num_k_blocks = (int32_t)(K / kGemmBK);
   args.n_tiles_n = (int32_t)(n_b / kGemmBN);

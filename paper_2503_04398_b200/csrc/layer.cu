@@ -38,7 +38,7 @@ struct smoe_layer {
   // GEMM descriptors
   bool maps_ready = false;
   int maps_cg_up = 0, maps_cg_down = 0;
-  CUtensorMap map_x, map_g, map_w13, map_h, map_w2;
+  CUtensorMap map_x, map_w13, map_h, map_w2;
 };
 
 static bool valid_cfg(const smoe_layer_config* c) {
@@ -164,21 +164,16 @@ static int check_bound(const smoe_layer* L) {
       if (!L->buf[s][i]) return SMOE_ERR_INVALID_ARG;
   for (int s : {SMOE_BUF_HMID, SMOE_BUF_FORWARD, SMOE_BUF_INVERSE, SMOE_BUF_DEV,
                 SMOE_BUF_PLAN_COUNTS, SMOE_BUF_GROUP, SMOE_BUF_STATS, SMOE_BUF_ERR,
-                SMOE_BUF_WORKSPACE, SMOE_BUF_PROBLEMS, SMOE_BUF_XSRC})
+                SMOE_BUF_WORKSPACE, SMOE_BUF_PROBLEMS})
     if (!L->buf[s][0]) return SMOE_ERR_INVALID_ARG;
   if (c.world_size > 1) {
     for (int g = 0; g < c.n_shards; ++g)
       if (!L->buf[SMOE_BUF_SIGNAL][g]) return SMOE_ERR_INVALID_ARG;
     if (!L->buf[SMOE_BUF_EPOCH][0]) return SMOE_ERR_INVALID_ARG;
   }
-  // the resident shards' expert inputs / metadata / SRS rows must each form
-  // one arena (one TMA descriptor covers all local problems)
+  // the resident shards' expert inputs / metadata must form one arena
+  // (one TMA descriptor covers all local problems)
   const int64_t xs = c.expert_rows * (int64_t)c.hidden * 2, ms = c.expert_rows * 8;
-  const int64_t hss = c.max_tokens * (int64_t)c.hidden * 2;
-  for (int i = 1; i < c.shard_count; ++i)
-    if (static_cast<char*>(L->buf[SMOE_BUF_HS][i]) !=
-        static_cast<char*>(L->buf[SMOE_BUF_HS][0]) + i * hss)
-      return SMOE_ERR_INVALID_ARG;
   for (int i = 1; i < c.shard_count; ++i) {
     const int g0 = c.shard_begin;
     if (static_cast<char*>(L->buf[SMOE_BUF_XIN][g0 + i]) !=
@@ -191,28 +186,27 @@ static int check_bound(const smoe_layer* L) {
 }
 
 static int ensure_maps(smoe_layer* L) {
-  if (L->maps_ready && L->maps_cg_down == gemm_cta_group(1)) return SMOE_OK;
+  if (L->maps_ready && L->maps_cg_up == gemm_cta_group(0) &&
+      L->maps_cg_down == gemm_cta_group(1))
+    return SMOE_OK;
   int rc = check_bound(L);
   if (rc) return rc;
   if (!L->w13 || !L->w2 || !L->w_gate || !L->t_labels) return SMOE_ERR_INVALID_ARG;
   const auto& c = L->cfg;
   const int64_t rows = c.expert_rows * c.shard_count;
   const int64_t nl = std::max<int32_t>(L->local_slots, 1);
-  // the up-GEMM gathers its A rows (gather4, box height 1): from the SRS rows
-  // of the resident shards, or from xin for rows other GPUs pushed
-  if ((rc = make_tmap_bf16(&L->map_x, L->buf[SMOE_BUF_XIN][c.shard_begin], rows, c.hidden, 1)))
+  if ((rc = make_tmap_bf16(&L->map_x, L->buf[SMOE_BUF_XIN][c.shard_begin], rows, c.hidden,
+                           kGemmBM)))
     return rc;
-  if ((rc = make_tmap_bf16(&L->map_g, L->buf[SMOE_BUF_HS][0], c.max_tokens * c.shard_count,
-                           c.hidden, 1)))
-    return rc;
-  if ((rc = make_tmap_bf16(&L->map_w13, L->w13, nl * 2 * c.ffn, c.hidden, gemm_b_box_rows(1))))
+  if ((rc = make_tmap_bf16(&L->map_w13, L->w13, nl * 2 * c.ffn, c.hidden,
+                           gemm_b_box_rows(gemm_cta_group(0)))))
     return rc;
   if ((rc = make_tmap_bf16(&L->map_h, L->buf[SMOE_BUF_HMID][0], rows, c.ffn, kGemmBM))) return rc;
   if ((rc = make_tmap_bf16(&L->map_w2, L->w2, nl * c.hidden, c.ffn,
                            gemm_b_box_rows(gemm_cta_group(1)))))
     return rc;
   L->maps_ready = true;
-  L->maps_cg_up = 1;                 // gathering up-GEMM runs on one-SM tiles
+  L->maps_cg_up = gemm_cta_group(0);
   L->maps_cg_down = gemm_cta_group(1);
   return SMOE_OK;
 }
@@ -289,7 +283,6 @@ extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tok
                            L->slot_owner_d, L->slot_first_d, local_ptrs(L, SMOE_BUF_HS),
                            local_ptrs(L, SMOE_BUF_TOPK_IDS), local_ptrs(L, SMOE_BUF_PAIR_RANK),
                            peer_ptrs(L, SMOE_BUF_XIN), peer_ptrs(L, SMOE_BUF_XMETA),
-                           static_cast<int32_t*>(L->buf[SMOE_BUF_XSRC][0]), c.max_tokens,
                            c.expert_rows, static_cast<int64_t*>(L->buf[SMOE_BUF_PROBLEMS][0]),
                            err, n, st);
       if (rc) return rc;
@@ -298,20 +291,17 @@ extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tok
     case SMOE_STAGE_EXPERT_UP: {
       GemmArgs a{};
       a.problems = static_cast<const int64_t*>(L->buf[SMOE_BUF_PROBLEMS][0]);
-      a.problem_stride = 8;
-      a.xsrc = static_cast<const int32_t*>(L->buf[SMOE_BUF_XSRC][0]);
       a.num_problems = L->local_slots;
       a.num_k_blocks = c.hidden / kGemmBK;
       a.n_tiles_n = 2 * c.ffn / kGemmBN;
       a.n_b = 2 * c.ffn;
       a.c = static_cast<char*>(L->buf[SMOE_BUF_HMID][0]);
       a.ldc = c.ffn;
-      return launch_grouped_gemm(L->map_x, L->map_w13, a, kEpiSwiGLU, 1, st, &L->map_g);
+      return launch_grouped_gemm(L->map_x, L->map_w13, a, kEpiSwiGLU, L->maps_cg_up, st);
     }
     case SMOE_STAGE_EXPERT_DOWN: {
       GemmArgs a{};
       a.problems = static_cast<const int64_t*>(L->buf[SMOE_BUF_PROBLEMS][0]);
-      a.problem_stride = 8;
       a.num_problems = L->local_slots;
       a.num_k_blocks = c.ffn / kGemmBK;
       a.n_tiles_n = c.hidden / kGemmBN;

@@ -548,81 +548,47 @@ int launch_route(const LocalRows& lr, int32_t N, int32_t k, const ShardPtrs& top
 }
 
 // ------------------------------------------------------------------ K5b dispatch
-// Expert segment of slot e on its owner o (rows of the owner's expert-input
-// arena):   [ pairs from shards on o's GPU | pad to 4 | pairs from other GPUs | pad to 4 ]
-// Pairs whose source shard sits on the owner's GPU are NOT copied: the
-// dispatch records the source row (xsrc) and the up-GEMM gathers it with TMA
-// gather4 straight from the SRS output.  Only pairs from other GPUs travel
-// (peer stores into the owner's xin).  Pad rows carry xsrc = -1 (TMA zero
-// fill) and xmeta = -1 (skipped by the combine epilogue).  The problem table
-// row is {a_off, m (padded), b_index, c_off, gathered rows, 0, 0, 0}.
 __global__ void __launch_bounds__(256)
 dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __restrict__ C,
                 const int32_t* __restrict__ slot_owner, const int32_t* __restrict__ slot_first,
                 ShardPtrs hs, ShardPtrs topk_ids, ShardPtrs pair_rank, ShardPtrs xin,
-                ShardPtrs xmeta, int32_t* __restrict__ xsrc, int64_t hs_rows,
-                int64_t expert_rows, int64_t* problems, int32_t* err) {
+                ShardPtrs xmeta, int64_t expert_rows, int64_t* problems, int32_t* err) {
   __shared__ RowMap rm;
-  __shared__ int32_t s_M[kGateMaxN];      // padded segment length
-  __shared__ int32_t s_lpad[kGateMaxN];   // padded same-GPU part
+  __shared__ int32_t s_M[kGateMaxN];
   __shared__ int32_t s_seg[kGateMaxN];
   __shared__ int32_t s_off[SMOE_MAX_SHARDS * kGateMaxN];
   const int G = lr.n_shards;
-  const int Lp = lr.shard_count;          // shards per process (uniform)
   const int tid = threadIdx.x, lane = tid & 31;
   for (int e = tid; e < N; e += blockDim.x) {
-    const int po = slot_owner[e] / Lp;
-    int32_t loc = 0, rem = 0;
-    for (int g = 0; g < G; ++g) {
-      if (g / Lp == po) loc += C[g * N + e]; else rem += C[g * N + e];
-    }
-    const int32_t lpad = (loc + 3) & ~3;
-    s_lpad[e] = lpad;
-    s_M[e] = (lpad + rem + 3) & ~3;
+    int32_t m = 0;
+    for (int s = 0; s < G; ++s) m += C[s * N + e];
+    s_M[e] = m;
   }
   load_rowmap(rm, lr);    // contains __syncthreads
   for (int e = tid; e < N; e += blockDim.x) {
-    const int po = slot_owner[e] / Lp;
     int32_t seg = 0;
     for (int e2 = slot_first[slot_owner[e]]; e2 < e; ++e2) seg += s_M[e2];
     s_seg[e] = seg;
-    int32_t run_l = seg, run_r = seg + s_lpad[e];
-    for (int g = 0; g < G; ++g) {
-      if (g / Lp == po) { s_off[g * N + e] = run_l; run_l += C[g * N + e]; }
-      else { s_off[g * N + e] = run_r; run_r += C[g * N + e]; }
-    }
+    int32_t run = seg;
+    for (int s = 0; s < G; ++s) { s_off[s * N + e] = run; run += C[s * N + e]; }
   }
   __syncthreads();
-  const int32_t e0 = slot_first[lr.shard_begin];
-  const int32_t e1 = slot_first[lr.shard_begin + lr.shard_count];
   if (blockIdx.x == 0) {
-    // problem table + pad rows of the resident experts
+    // grouped-GEMM problem table: one problem per expert slot of the resident shards
+    const int32_t e0 = slot_first[lr.shard_begin];
+    const int32_t e1 = slot_first[lr.shard_begin + lr.shard_count];
     for (int e = e0 + tid; e < e1; e += blockDim.x) {
       const int32_t o = slot_owner[e];
-      const int po = o / Lp;
       int64_t m = s_M[e];
       if (s_seg[e] + m > expert_rows) { set_err(err, SMOE_ERRBIT_CAPACITY); m = 0; }
       const int64_t a_off = (int64_t)(o - lr.shard_begin) * expert_rows + s_seg[e];
-      int64_t* pr = problems + 8 * (e - e0);
-      pr[0] = a_off; pr[1] = m; pr[2] = e - e0; pr[3] = a_off; pr[4] = m ? s_lpad[e] : 0;
-      pr[5] = pr[6] = pr[7] = 0;
-      if (!m) continue;
-      int32_t loc = 0, rem = 0;
-      for (int g = 0; g < G; ++g) {
-        if (g / Lp == po) loc += C[g * N + e]; else rem += C[g * N + e];
-      }
-      int64_t* xm = reinterpret_cast<int64_t*>(xmeta.p[o]);
-      for (int r = loc; r < s_lpad[e]; ++r) {
-        xsrc[a_off + r] = -1;
-        xm[s_seg[e] + r] = -1;
-      }
-      for (int r = s_lpad[e] + rem; r < m; ++r) xm[s_seg[e] + r] = -1;
+      int64_t* pr = problems + 4 * (e - e0);
+      pr[0] = a_off; pr[1] = m; pr[2] = e - e0; pr[3] = a_off;
     }
   }
   const int64_t vecs = d / 8;
   const int64_t total_pairs = (int64_t)rm.total * k;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int my_proc = lr.shard_begin / Lp;
   for (int64_t pq = blockIdx.x * (int64_t)(blockDim.x >> 5) + (tid >> 5); pq < total_pairs;
        pq += nwarps) {
     const int64_t q = pq / k;
@@ -635,14 +601,6 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
     const int64_t pos =
         (int64_t)s_off[g * N + e] + reinterpret_cast<const int32_t*>(pair_rank.p[gl])[j * k + s];
     if (pos >= expert_rows) { if (lane == 0) set_err(err, SMOE_ERRBIT_CAPACITY); continue; }
-    if (o / Lp == my_proc) {
-      // same GPU: the up-GEMM gathers hs row (gl, j) itself
-      if (lane == 0) {
-        xsrc[(int64_t)(o - lr.shard_begin) * expert_rows + pos] = (int32_t)(gl * hs_rows + j);
-        reinterpret_cast<int64_t*>(xmeta.p[o])[pos] = ((int64_t)g << 40) | (j * k + s);
-      }
-      continue;
-    }
     const char* src = hs.p[gl] + j * d * 2;
     char* dst = xin.p[o] + pos * d * 2;
     int64_t v = lane;
@@ -662,13 +620,13 @@ int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
                     const int32_t* counts_mat, const int32_t* slot_owner,
                     const int32_t* slot_first, const ShardPtrs& hs, const ShardPtrs& topk_ids,
                     const ShardPtrs& pair_rank, const ShardPtrs& xin, const ShardPtrs& xmeta,
-                    int32_t* xsrc, int64_t hs_rows, int64_t expert_rows, int64_t* problems,
-                    int32_t* err, int64_t n_rows_bound, cudaStream_t st) {
+                    int64_t expert_rows, int64_t* problems, int32_t* err, int64_t n_rows_bound,
+                    cudaStream_t st) {
   if (N > kGateMaxN || d % 8) return SMOE_ERR_UNSUPPORTED;
   const int64_t blocks = std::max<int64_t>(1, ceil_div(n_rows_bound * k, 8));
-  dispatch_kernel<<<grid_cap(blocks, 16), 256, 0, st>>>(
-      lr, N, k, d, counts_mat, slot_owner, slot_first, hs, topk_ids, pair_rank, xin, xmeta, xsrc,
-      hs_rows, expert_rows, problems, err);
+  dispatch_kernel<<<grid_cap(blocks, 16), 256, 0, st>>>(lr, N, k, d, counts_mat, slot_owner,
+                                                        slot_first, hs, topk_ids, pair_rank, xin,
+                                                        xmeta, expert_rows, problems, err);
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }

@@ -34,8 +34,8 @@ int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
                     const int32_t* counts_mat, const int32_t* slot_owner,
                     const int32_t* slot_first, const ShardPtrs& hs, const ShardPtrs& topk_ids,
                     const ShardPtrs& pair_rank, const ShardPtrs& xin, const ShardPtrs& xmeta,
-                    int32_t* xsrc, int64_t hs_rows, int64_t expert_rows, int64_t* problems,
-                    int32_t* err, int64_t n_rows_bound, cudaStream_t st);
+                    int64_t expert_rows, int64_t* problems, int32_t* err, int64_t n_rows_bound,
+                    cudaStream_t st);
 
 struct HistUpdate {
   const int64_t* hist_in;     // [n, hist_len] or nullptr (first layers)

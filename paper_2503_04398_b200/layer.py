@@ -136,8 +136,7 @@ class SpecMoELayer:
         self.group_t = t.zeros(1, dtype=t.int64, device=dev)
         self.stats_t = t.zeros(N.STAT_COUNT, dtype=t.int64, device=dev)
         self.err = t.zeros(1, dtype=t.int32, device=dev)
-        self.problems = t.zeros((256, 8), dtype=t.int64, device=dev)
-        self.xsrc = t.empty(L * R, dtype=t.int32, device=dev)
+        self.problems = t.zeros((256, 4), dtype=t.int64, device=dev)
         self.epoch = t.zeros(1, dtype=t.int32, device=dev)
 
     def _create_handle(self):
@@ -178,7 +177,6 @@ class SpecMoELayer:
                         (N.BUF_PLAN_COUNTS, self.plan_counts), (N.BUF_GROUP, self.group_t),
                         (N.BUF_STATS, self.stats_t), (N.BUF_ERR, self.err),
                         (N.BUF_WORKSPACE, self.workspace), (N.BUF_PROBLEMS, self.problems),
-                        (N.BUF_XSRC, self.xsrc),
                         (N.BUF_EPOCH, self.epoch)):
             bind(slot, 0, x)
         tb = self.tables
