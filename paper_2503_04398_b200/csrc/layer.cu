@@ -81,8 +81,11 @@ extern "C" void smoe_layer_destroy(smoe_layer* L) {
 extern "C" int smoe_layer_bind(smoe_layer* L, int32_t slot, int32_t index, void* ptr) {
   if (!L || slot < 0 || slot >= SMOE_BUF__COUNT || index < 0 || index >= SMOE_MAX_SHARDS)
     return SMOE_ERR_INVALID_ARG;
+  if (L->buf[slot][index] != ptr &&
+      (slot == SMOE_BUF_XIN || slot == SMOE_BUF_XMETA || slot == SMOE_BUF_HMID ||
+       slot == SMOE_BUF_HS))
+    L->maps_ready = false;           // only these feed TMA descriptors / arena checks
   L->buf[slot][index] = ptr;
-  L->maps_ready = false;
   return SMOE_OK;
 }
 

@@ -199,10 +199,16 @@ class SpecMoELayer:
     # ------------------------------------------------------------ forward
     def partial_views(self, n: int):
         """[L, n, d] views of the resident shards' partial-input buffers
-        (write the attention-TP partials here to avoid a copy)."""
-        if self.group is None:
-            return self.partial[:, :n]
-        return self.partial[:, :n]
+        currently bound to the layer (write the attention-TP partials here to
+        avoid a copy)."""
+        return getattr(self, "_bound_partial", self.partial)[:, :n]
+
+    def _bind_partial(self, P):
+        if getattr(self, "_bound_partial", self.partial) is P:
+            return
+        for g in range(self.G):
+            N.check(self.lib.smoe_layer_bind(self._h, N.BUF_PARTIAL, g, N.ptr(P[g])), "bind")
+        self._bound_partial = P
 
     def run_device(self, tokens_t, hist_t=None, stream=None, stages=None):
         """Run the layer on device-resident inputs already in the partial
@@ -277,6 +283,89 @@ class SpecMoELayer:
         self.check_errors()                 # stream sync: `out` is complete after this
         return out
 
+    # ------------------------------------------------------------ pipelined serving
+    def forward_async(self, hidden_partials, token_ids, histories=None, out=None):
+        """Pipelined `forward` for a stream of batches from HOST memory.
+
+        Returns a handle whose `.result()` yields the host output.  Inputs
+        should be pinned CPU tensors (their H2D copy runs on a copy stream);
+        `out` a pinned [n, d] bf16 tensor.  Partials are double-buffered:
+        the H2D of batch i+1 overlaps the layer of batch i (the buffer is
+        released as soon as batch i's SRS has read it), and the D2H of batch
+        i overlaps the first stages of batch i+1.  Single-process layers only
+        (peer processes read the partial buffers in place).  Data-dependent
+        errors surface in `.result()` of a later batch at the latest.
+        """
+        t = _dev.torch()
+        if self.group is not None:
+            res = self.forward(hidden_partials, token_ids, histories, out)
+            return _Done(res)
+        st = self._pipeline()
+        i = st["count"]
+        st["count"] += 1
+        slot = i % 2
+        n = int(token_ids.shape[0])
+        if n > self.max_tokens:
+            raise SchedulerError(f"{n} tokens exceed max_tokens={self.max_tokens}")
+        hp = hidden_partials if hidden_partials.dim() == 3 else hidden_partials.unsqueeze(0)
+        if tuple(hp.shape) != (self.shard_count, n, self.d) or hp.dtype != t.bfloat16:
+            raise SchedulerError(f"partials must be bf16 [{self.shard_count}, {n}, {self.d}]")
+        P, tok, hist = st["P"][slot], st["tok"][slot], st["hist"][slot]
+        # ---- H2D on the copy stream, once the slot's previous batch has passed its SRS
+        with t.cuda.stream(st["h2d"]):
+            st["h2d"].wait_event(st["free_p"][slot])     # batch i-2 finished its SRS
+            P[:, :n].copy_(hp, non_blocking=True)
+            st["h2d"].wait_event(st["free_ids"][slot])   # batch i-2 finished the layer
+            tok[:n].copy_(token_ids, non_blocking=True)
+            if histories is not None:
+                hist[:n].copy_(histories, non_blocking=True)
+            st["in"][slot].record(st["h2d"])
+        # ---- the layer on the compute stream
+        cs = st["compute"]
+        self._bind_partial(P)
+        with t.cuda.stream(cs):
+            cs.wait_event(st["in"][slot])
+            hp_t = hist[:n] if histories is not None else None
+            self.run_device(tok[:n], hp_t, stream=cs, stages=[N.STAGE_PLAN, N.STAGE_SRS])
+            st["free_p"][slot].record(cs)
+            self.run_device(tok[:n], hp_t, stream=cs, stages=range(N.STAGE_GATE,
+                                                                   N.STAGE_COMBINE_SAG))
+            cs.wait_event(st["d2h_done"])          # previous output fully read out
+            self.run_device(tok[:n], hp_t, stream=cs, stages=[N.STAGE_COMBINE_SAG])
+            st["free_ids"][slot].record(cs)
+            st["done"].record(cs)
+        # ---- D2H on its own stream
+        if out is None:
+            out = t.empty((n, self.d), dtype=t.bfloat16, pin_memory=True)
+        ev = t.cuda.Event()
+        with t.cuda.stream(st["d2h"]):
+            st["d2h"].wait_event(st["done"])
+            out.copy_(self.out_view(n), non_blocking=True)
+            st["d2h_done"].record(st["d2h"])
+            ev.record(st["d2h"])
+        return _Pending(self, out, ev)
+
+    def _pipeline(self):
+        st = getattr(self, "_pipe", None)
+        if st is None:
+            t = _dev.torch()
+            dev = self.w_gate.device
+            h = max(self.tables.ngram_n, 1)
+            st = {"P": [self.partial, t.zeros_like(self.partial)],
+                  "tok": [t.zeros(self.max_tokens, dtype=t.int64, device=dev) for _ in range(2)],
+                  "hist": [t.zeros((self.max_tokens, h), dtype=t.int64, device=dev)
+                           for _ in range(2)],
+                  "h2d": t.cuda.Stream(), "d2h": t.cuda.Stream(),
+                  "compute": t.cuda.current_stream(),
+                  "free_p": [t.cuda.Event(), t.cuda.Event()],
+                  "free_ids": [t.cuda.Event(), t.cuda.Event()],
+                  "in": [t.cuda.Event(), t.cuda.Event()],
+                  "done": t.cuda.Event(), "d2h_done": t.cuda.Event(), "count": 0}
+            for e in st["free_p"] + st["free_ids"] + [st["d2h_done"]]:
+                e.record(st["compute"])
+            self._pipe = st
+        return st
+
     # ------------------------------------------------------------ results
     def check_errors(self):
         bits = int(self.err.item())
@@ -339,3 +428,29 @@ class SpecMoELayer:
                       "srs_padded_model": G * group * (G - 1) * row,
                       "reference_model_a2a": a2a},
         }
+
+
+class _Pending:
+    """Handle of a `forward_async` batch."""
+
+    def __init__(self, layer, out, event):
+        self._layer, self._out, self._event = layer, out, event
+
+    def done(self) -> bool:
+        return self._event.query()
+
+    def result(self):
+        self._event.synchronize()
+        self._layer.check_errors()
+        return self._out
+
+
+class _Done:
+    def __init__(self, out):
+        self._out = out
+
+    def done(self) -> bool:
+        return True
+
+    def result(self):
+        return self._out

@@ -147,3 +147,31 @@ def test_layer_history_chain():
     assert np.array_equal(layer.plan_indices(500).forward, ref2["forward"])
     o = out2.float().numpy()
     assert np.linalg.norm(o - ref2["out"]) / np.linalg.norm(ref2["out"]) <= TOL
+
+
+def test_forward_async_pipeline_matches_sync():
+    """Pipelined serving API: double-buffered partials, H2D / compute / D2H on
+    three streams; every batch must equal the synchronous forward."""
+    over = {"G": 4, "N": 16}
+    ws = [synth.make_workload("toy", n=n, eps=0.2, seed=30 + i, cfg_override=over)
+          for i, n in enumerate((300, 257, 300, 12, 299))]
+    base = ws[0]
+    layer = SpecMoELayer(base.bundle, base.gate_w, base.w1, base.w3, base.w2, top_k=2,
+                         max_tokens=300)
+    want = []
+    for w in ws:
+        want.append(layer.forward(torch.from_numpy(w.partials).to(torch.bfloat16), w.tokens,
+                                  w.hist).float().numpy())
+    pins = [(torch.from_numpy(w.partials).to(torch.bfloat16).pin_memory(),
+             torch.from_numpy(w.tokens).pin_memory(), torch.from_numpy(w.hist).pin_memory())
+            for w in ws]
+    outs = [torch.empty((300, 256), dtype=torch.bfloat16).pin_memory() for _ in range(len(ws))]
+    handles = [layer.forward_async(p, t, h, out=outs[i][: len(t)]) for i, (p, t, h) in
+               enumerate(pins)]
+    for i, hd in enumerate(handles):
+        got = hd.result().float().numpy()
+        assert np.array_equal(got, want[i]), i
+    # the synchronous path still works after pipelining (partial buffer rebound)
+    again = layer.forward(torch.from_numpy(ws[1].partials).to(torch.bfloat16), ws[1].tokens,
+                          ws[1].hist).float().numpy()
+    assert np.array_equal(again, want[1])
