@@ -484,17 +484,11 @@ static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
   }
   GemmArgs g = args;
   if (g.group_m <= 0) {
-    // Rasterisation: when a group of m-blocks whose A rows fit ~40 MB of L2
-    // covers a whole wave, A stays resident and B streams once per group.
-    // When A tiles are big (large K: the down projection) that group is too
-    // small, and a wave spanning few m-blocks x many n-blocks re-reads B;
-    // then make the wave square (about sqrt(units) m-blocks), which
-    // minimises the distinct A + B tiles a wave touches.
+    // keep a group's A rows (tile_m x K bf16 per m-block) within ~40 MB of L2
     const int64_t a_blk = (int64_t)S::kTileM * g.num_k_blocks * kGemmBK * 2;
-    const int64_t fit = std::max<int64_t>(1, (40ll << 20) / a_blk);
-    int64_t square = 1;
-    while ((square + 1) * (square + 1) <= num_sms() / CG) ++square;
-    g.group_m = (int32_t)std::max(fit, square);
+    g.group_m = (int32_t)std::max<int64_t>(1, (40ll << 20) / a_blk);
+    const char* e = getenv(EPI == kEpiSwiGLU ? "SMOE_GROUP_M_UP" : "SMOE_GROUP_M_DOWN");
+    if (e && atoi(e) > 0) g.group_m = atoi(e);     // tuning experiments only
   }
   const int grid = (num_sms() / CG) * CG;
   if (CG == 1) {
