@@ -25,7 +25,8 @@ struct GemmArgs {
   int32_t num_k_blocks;      // K / 64
   int32_t n_tiles_n;         // n_b / 256
   int32_t n_b;               // rows of B per problem (output columns before SwiGLU)
-  int32_t group_m;           // m-blocks per rasterisation group (0: derive from K)
+  int32_t group_m;           // > 0: m-blocks per rasterisation group; < 0: -(n-blocks per
+                             // n-group); 0: derive from K
   char* c;                   // store / swiglu output
   int64_t ldc;               // elements
   const int64_t* meta;       // scatter: per A row

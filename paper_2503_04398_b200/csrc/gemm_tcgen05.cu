@@ -182,13 +182,26 @@ __device__ __forceinline__ TileCoord decode_tile(const SmemProblems& sp, int32_t
   while (cursor + 1 < np && sp.tile_prefix[cursor + 1] <= t) ++cursor;
   const int32_t local = t - sp.tile_prefix[cursor];
   const int32_t mt = (sp.m[cursor] + TILE_M - 1) / TILE_M;
+  TileCoord c;
+  c.p = cursor;
+  if (group_m < 0) {
+    // n-grouped order (group_m = -group_n): a group of n-blocks (a slice of the
+    // weights that stays L2-resident) is swept for every m-block, n fastest
+    const int32_t group_n = -group_m;
+    const int32_t per_group = group_n * mt;
+    const int32_t g = local / per_group;
+    const int32_t first_n = g * group_n;
+    const int32_t gn = min(group_n, n_tiles_n - first_n);
+    const int32_t r = local - g * per_group;
+    c.n_blk = first_n + r % gn;
+    c.m_blk = r / gn;
+    return c;
+  }
   const int32_t per_group = group_m * n_tiles_n;
   const int32_t g = local / per_group;
   const int32_t first_m = g * group_m;
   const int32_t gm = min(group_m, mt - first_m);
   const int32_t r = local - g * per_group;
-  TileCoord c;
-  c.p = cursor;
   c.m_blk = first_m + r % gm;
   c.n_blk = r / gm;
   return c;
@@ -483,7 +496,7 @@ static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
     attr_set = true;
   }
   GemmArgs g = args;
-  if (g.group_m <= 0) {
+  if (g.group_m == 0) {
     // A-resident order: a group of m-blocks whose A rows fit ~40 MB of L2 is
     // swept for every n-block (B streams once per group).  When A tiles are
     // so large that fewer than 8 fit (the down projection, K = f), use the
@@ -494,7 +507,7 @@ static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
     const int64_t fit = (40ll << 20) / a_blk;
     g.group_m = fit >= 8 ? (int32_t)fit : 1;
     const char* e = getenv(EPI == kEpiSwiGLU ? "SMOE_GROUP_M_UP" : "SMOE_GROUP_M_DOWN");
-    if (e && atoi(e) > 0) g.group_m = atoi(e);     // tuning experiments only
+    if (e && atoi(e) != 0) g.group_m = atoi(e);     // tuning experiments (< 0: n-groups)
   }
   const int grid = (num_sms() / CG) * CG;
   if (CG == 1) {
