@@ -49,9 +49,14 @@ static bool valid_cfg(const smoe_layer_config* c) {
          c->world_rank >= 0 && c->world_rank < c->world_size;
 }
 
+static size_t plan_ws_aligned(const smoe_layer_config* cfg) {
+  return (smoe_plan_workspace_bytes(cfg->max_tokens, cfg->n_shards) + 255) & ~size_t(255);
+}
+
 extern "C" size_t smoe_layer_workspace_bytes(const smoe_layer_config* cfg) {
   if (!cfg) return 0;
-  return smoe_plan_workspace_bytes(cfg->max_tokens, cfg->n_shards);
+  return plan_ws_aligned(cfg) +
+         route_workspace_bytes(cfg->max_tokens, cfg->top_k, cfg->n_experts, cfg->shard_count);
 }
 
 extern "C" int smoe_layer_create(const smoe_layer_config* cfg, smoe_layer** out) {
@@ -261,8 +266,7 @@ extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tok
                               static_cast<int64_t*>(L->buf[SMOE_BUF_INVERSE][0]),
                               static_cast<int32_t*>(L->buf[SMOE_BUF_PLAN_COUNTS][0]),
                               static_cast<int64_t*>(L->buf[SMOE_BUF_GROUP][0]), err,
-                              L->buf[SMOE_BUF_WORKSPACE][0], smoe_layer_workspace_bytes(&c),
-                              stream);
+                              L->buf[SMOE_BUF_WORKSPACE][0], plan_ws_aligned(&c), stream);
     }
     case SMOE_STAGE_SRS:
       return launch_srs(lr, peer_ptrs(L, SMOE_BUF_PARTIAL), c.hidden, local_ptrs(L, SMOE_BUF_HS),
@@ -275,8 +279,10 @@ extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tok
     case SMOE_STAGE_ROUTE: {
       int32_t nb = 0;
       ShardPtrs cb = distinct_ptrs(L, SMOE_BUF_COUNTS, &nb);
+      int32_t* chunk_counts = reinterpret_cast<int32_t*>(
+          static_cast<char*>(L->buf[SMOE_BUF_WORKSPACE][0]) + plan_ws_aligned(&c));
       rc = launch_route(lr, c.n_experts, c.top_k, local_ptrs(L, SMOE_BUF_TOPK_IDS),
-                        local_ptrs(L, SMOE_BUF_PAIR_RANK), cb, nb, st);
+                        local_ptrs(L, SMOE_BUF_PAIR_RANK), cb, nb, chunk_counts, n, st);
       if (rc) return rc;
       return smoe_layer_barrier(L, stream);
     }

@@ -269,9 +269,12 @@ gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ 
 // swizzle (conflict-free ldmatrix).
 constexpr int kMmaKC = 64;                       // bf16 per row per stage (128 B)
 constexpr int kMmaStages = 4;
-// rows per CTA: 16 per warp; more rows amortise the W tile (N x 64) over the
-// CTA when N is large, fewer keep more CTAs (bytes in flight) when N is small
-__host__ __device__ constexpr int mma_rows(int nt) { return nt <= 2 ? 64 : 128; }
+// 64 rows per CTA (4 row groups of 16) x S k-splits: warp (r, s) multiplies
+// row group r with k sub-chunk s of every stage, and the S partial logits are
+// summed through shared memory.  The split keeps 8-16 warps per CTA busy on
+// the short, latency-bound k loop (the gate reads only d*2 bytes per token).
+constexpr int kMmaRowsCTA = 64;
+__host__ __device__ constexpr int mma_splits(int nt) { return nt <= 2 ? 4 : 2; }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
@@ -294,15 +297,17 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1
 __device__ __forceinline__ uint32_t swz(int r, int c) { return r * 128 + ((c ^ (r & 7)) << 4); }
 
 template <int NT>   // NT = N / 8 n-tiles
-__global__ void __launch_bounds__(mma_rows(NT) * 2)
+__global__ void __launch_bounds__(128 * mma_splits(NT))
 gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ w_gate,
                 const float* __restrict__ b_gate, int32_t k, int32_t renorm,
                 const int32_t* __restrict__ slot_owner, ShardPtrs topk_ids, ShardPtrs topk_w,
                 int64_t* stats) {
   constexpr int N = NT * 8;
-  constexpr int kMmaRows = mma_rows(NT);
-  constexpr int kMmaThreads = kMmaRows * 2;                     // 16 rows per warp
-  constexpr int kMmaStageBytes = (kMmaRows + N) * kMmaKC * 2;   // H rows + W rows, 128 B each
+  constexpr int S = mma_splits(NT);
+  constexpr int kMmaRows = kMmaRowsCTA;
+  constexpr int kMmaThreads = 128 * S;
+  constexpr int kSubBytes = (kMmaRows + N) * kMmaKC * 2;        // H rows + W rows, 128 B each
+  constexpr int kMmaStageBytes = S * kSubBytes;
   extern __shared__ __align__(128) uint8_t gsm[];
   __shared__ RowMap rm;
   __shared__ const char* s_row[kMmaRows];
@@ -312,7 +317,8 @@ gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ 
   load_rowmap(rm, lr);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(gsm));
-  const int kchunks = (int)(d / kMmaKC);
+  const int kchunks = (int)(d / (kMmaKC * S));                  // stages of S sub-chunks
+  const int rgroup = warp & 3, split = warp >> 2;
   for (int64_t rb = blockIdx.x; rb * kMmaRows < rm.total; rb += gridDim.x) {
     if (tid < kMmaRows) {
       const int64_t q = rb * kMmaRows + tid;
@@ -325,15 +331,18 @@ gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ 
     if (tid == 0) { s_local = 0; s_remote = 0; }
     __syncthreads();
     auto load_stage = [&](int kc, int stage) {
-      const uint32_t st = sbase + stage * kMmaStageBytes;
-      for (int e = tid; e < (kMmaRows + N) * 8; e += kMmaThreads) {
-        const int r = e >> 3, c = e & 7;
+      for (int e = tid; e < S * (kMmaRows + N) * 8; e += kMmaThreads) {
+        const int sub = e / ((kMmaRows + N) * 8);
+        const int rem = e - sub * (kMmaRows + N) * 8;
+        const int r = rem >> 3, c = rem & 7;
+        const uint32_t st = sbase + stage * kMmaStageBytes + sub * kSubBytes;
+        const int64_t col = (int64_t)(kc * S + sub) * kMmaKC + c * 8;
         if (r < kMmaRows) {
           const char* src = s_row[r];
-          cp_async16(st + swz(r, c), src ? src + (kc * kMmaKC + c * 8) * 2 : w_gate, src != nullptr);
+          cp_async16(st + swz(r, c), src ? src + col * 2 : w_gate, src != nullptr);
         } else {
           const int n = r - kMmaRows;
-          cp_async16(st + swz(r, c), w_gate + ((int64_t)n * d + kc * kMmaKC + c * 8) * 2, true);
+          cp_async16(st + swz(r, c), w_gate + ((int64_t)n * d + col) * 2, true);
         }
       }
     };
@@ -353,12 +362,12 @@ gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ 
         if (nk < kchunks) load_stage(nk, nk % kMmaStages);
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
-      const uint32_t st = sbase + (kc % kMmaStages) * kMmaStageBytes;
+      const uint32_t st = sbase + (kc % kMmaStages) * kMmaStageBytes + split * kSubBytes;
 #pragma unroll
       for (int ks = 0; ks < kMmaKC / 16; ++ks) {
-        // A: rows warp*16 + (lane & 15), 16-B chunk 2*ks + (lane >> 4)
+        // A: rows rgroup*16 + (lane & 15), 16-B chunk 2*ks + (lane >> 4)
         uint32_t a0, a1, a2, a3;
-        const int ar = warp * 16 + (lane & 15);
+        const int ar = rgroup * 16 + (lane & 15);
         ldsm_x4(st + swz(ar, 2 * ks + (lane >> 4)), a0, a1, a2, a3);
 #pragma unroll
         for (int t = 0; t < NT; t += 2) {
@@ -375,19 +384,30 @@ gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ 
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
-    // logits -> smem [64][N + 1] (reuses the staging ring)
-    float* lgs = reinterpret_cast<float*>(gsm);
+    // partial logits of every k split -> smem [S][64][N + 1] (reuses the ring),
+    // then lgs[r][e] = bias + sum over splits in split order
+    float* red = reinterpret_cast<float*>(gsm);
     {
-      const int r0 = warp * 16 + (lane >> 2);
+      float* part = red + split * kMmaRows * (N + 1);
+      const int r0 = rgroup * 16 + (lane >> 2);
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
         const int c0 = t * 8 + 2 * (lane & 3);
-        const float b0 = b_gate ? __ldg(b_gate + c0) : 0.f, b1 = b_gate ? __ldg(b_gate + c0 + 1) : 0.f;
-        lgs[r0 * (N + 1) + c0] = acc[t][0] + b0;
-        lgs[r0 * (N + 1) + c0 + 1] = acc[t][1] + b1;
-        lgs[(r0 + 8) * (N + 1) + c0] = acc[t][2] + b0;
-        lgs[(r0 + 8) * (N + 1) + c0 + 1] = acc[t][3] + b1;
+        part[r0 * (N + 1) + c0] = acc[t][0];
+        part[r0 * (N + 1) + c0 + 1] = acc[t][1];
+        part[(r0 + 8) * (N + 1) + c0] = acc[t][2];
+        part[(r0 + 8) * (N + 1) + c0 + 1] = acc[t][3];
       }
+    }
+    __syncthreads();
+    float* lgs = red;
+    for (int i = tid; i < kMmaRows * N; i += kMmaThreads) {
+      const int r = i / N, e = i - r * N;
+      float v = red[r * (N + 1) + e];
+#pragma unroll
+      for (int sp = 1; sp < S; ++sp) v += red[sp * kMmaRows * (N + 1) + r * (N + 1) + e];
+      v += b_gate ? __ldg(b_gate + e) : 0.f;
+      lgs[r * (N + 1) + e] = v;      // split 0's slot: each element read then written by one thread
     }
     __syncthreads();
     unsigned long long my_local = 0, my_remote = 0;
@@ -457,15 +477,16 @@ static int launch_gate_mma(const LocalRows& lr, const ShardPtrs& hs, int64_t d, 
                            const float* b, int32_t k, int32_t renorm, const int32_t* owner,
                            const ShardPtrs& ids, const ShardPtrs& wts, int64_t* stats,
                            int64_t n_rows_bound, cudaStream_t st) {
-  constexpr int rows = mma_rows(NT);
-  const size_t smem = (size_t)kMmaStages * ((rows + NT * 8) * kMmaKC * 2);
+  constexpr int rows = kMmaRowsCTA, S = mma_splits(NT);
+  const size_t smem = (size_t)kMmaStages * S * ((rows + NT * 8) * kMmaKC * 2);
+  if (d % (kMmaKC * S)) return SMOE_ERR_UNSUPPORTED;
   static bool attr = false;
   if (!attr) {
     SMOE_CUDA_TRY(cudaFuncSetAttribute(gate_mma_kernel<NT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  gate_mma_kernel<NT><<<grid_cap(ceil_div(n_rows_bound, rows), 4), rows * 2, smem, st>>>(
+  gate_mma_kernel<NT><<<grid_cap(ceil_div(n_rows_bound, rows), 4), 128 * S, smem, st>>>(
       lr, hs, d, static_cast<const char*>(w), b, k, renorm, owner, ids, wts, stats);
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
@@ -477,7 +498,7 @@ int launch_gate(const LocalRows& lr, const ShardPtrs& hs, int64_t d, const void*
                 int64_t* stats, int64_t n_rows_bound, cudaStream_t st) {
   if (N < 1 || N > kGateMaxN || k < 1 || k > kGateMaxK || k > N || d % 2) return SMOE_ERR_UNSUPPORTED;
   if (n_rows_bound <= 0) return SMOE_OK;
-  if (d % kMmaKC == 0) {
+  if (d % (kMmaKC * 4) == 0) {
     switch (N) {   // tensor-core path for N in {8, 16, ..., 64}
       case 8: return launch_gate_mma<1>(lr, hs, d, w_gate, b_gate, k, renorm, slot_owner, topk_ids, topk_w, stats, n_rows_bound, st);
       case 16: return launch_gate_mma<2>(lr, hs, d, w_gate, b_gate, k, renorm, slot_owner, topk_ids, topk_w, stats, n_rows_bound, st);
@@ -494,55 +515,88 @@ int launch_gate(const LocalRows& lr, const ShardPtrs& hs, int64_t d, const void*
 }
 
 // ------------------------------------------------------------------ K5a route
+// Stable rank of every (token, slot) pair inside its expert slot, in two wide
+// passes over 1024-pair chunks (one CTA per chunk and shard):
+//   route_count: per-chunk pair counts per expert slot
+//   route_rank:  rank = sum of the counts of earlier chunks + rank inside the
+//                chunk (warp match_any + per-warp counts); chunk 0 publishes
+//                the shard's count row to every process's [G, N] matrix.
 constexpr int kRouteThreads = 1024;
 
 __global__ void __launch_bounds__(kRouteThreads)
-route_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids, ShardPtrs pair_rank,
-             ShardPtrs count_bufs, int32_t n_count_bufs) {
-  __shared__ int32_t s_run[kGateMaxN];
+route_count_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids,
+                   int32_t* __restrict__ chunk_counts, int32_t max_chunks) {
+  __shared__ int32_t s_cnt[kGateMaxN];
+  const int gl = blockIdx.y, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const int64_t P = (int64_t)lr.counts[lr.shard_begin + gl] * k;
+  if ((int64_t)b * kRouteThreads >= P) return;
+  for (int e = tid; e < N; e += kRouteThreads) s_cnt[e] = 0;
+  __syncthreads();
+  const int64_t p = (int64_t)b * kRouteThreads + tid;
+  const int32_t e = p < P ? reinterpret_cast<const int32_t*>(topk_ids.p[gl])[p] : -1;
+  const uint32_t peers = __match_any_sync(0xffffffffu, e);
+  if (e >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[e], __popc(peers));
+  __syncthreads();
+  int32_t* out = chunk_counts + ((int64_t)gl * max_chunks + b) * N;
+  for (int ee = tid; ee < N; ee += kRouteThreads) out[ee] = s_cnt[ee];
+}
+
+__global__ void __launch_bounds__(kRouteThreads)
+route_rank_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids, ShardPtrs pair_rank,
+                  const int32_t* __restrict__ chunk_counts, int32_t max_chunks,
+                  ShardPtrs count_bufs, int32_t n_count_bufs) {
+  __shared__ int32_t s_pre[kGateMaxN];
   __shared__ int32_t s_w[32 * kGateMaxN];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gl = blockIdx.x;
+  const int gl = blockIdx.y, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t g = lr.shard_begin + gl;
   const int64_t P = (int64_t)lr.counts[g] * k;
-  const int32_t* ids = reinterpret_cast<const int32_t*>(topk_ids.p[gl]);
-  int32_t* rank = reinterpret_cast<int32_t*>(pair_rank.p[gl]);
-  for (int e = tid; e < N; e += kRouteThreads) s_run[e] = 0;
+  const int32_t nchunks = (int32_t)((P + kRouteThreads - 1) / kRouteThreads);
+  if (b > 0 && b >= nchunks) return;
+  const int32_t* cc = chunk_counts + (int64_t)gl * max_chunks * N;
+  for (int e = tid; e < N; e += kRouteThreads) {
+    int32_t pre = 0;
+    for (int c = 0; c < b; ++c) pre += cc[c * N + e];
+    s_pre[e] = pre;
+    if (b == 0) {                     // publish row g of the [G, N] count matrix
+      int32_t tot = 0;
+      for (int c = 0; c < nchunks; ++c) tot += cc[c * N + e];
+      for (int i = 0; i < n_count_bufs; ++i)
+        reinterpret_cast<int32_t*>(count_bufs.p[i])[g * N + e] = tot;
+    }
+  }
   for (int e = tid; e < 32 * N; e += kRouteThreads) s_w[e] = 0;
   __syncthreads();
-  for (int64_t base = 0; base < P; base += kRouteThreads) {
-    const int64_t p = base + tid;
-    const int32_t e = p < P ? ids[p] : -1;
-    const uint32_t peers = __match_any_sync(0xffffffffu, e);
-    const int32_t rw = __popc(peers & lanemask_lt());
-    if (e >= 0 && lane == __ffs(peers) - 1) s_w[warp * N + e] = __popc(peers);
-    __syncthreads();
-    if (e >= 0) {
-      int32_t r = s_run[e] + rw;
-      for (int w = 0; w < warp; ++w) r += s_w[w * N + e];
-      rank[p] = r;
-    }
-    __syncthreads();
-    for (int ee = tid; ee < N; ee += kRouteThreads) {
-      int32_t s = 0;
-      for (int w = 0; w < 32; ++w) { s += s_w[w * N + ee]; s_w[w * N + ee] = 0; }
-      s_run[ee] += s;
-    }
-    __syncthreads();
+  if (b >= nchunks) return;
+  const int64_t p = (int64_t)b * kRouteThreads + tid;
+  const int32_t e = p < P ? reinterpret_cast<const int32_t*>(topk_ids.p[gl])[p] : -1;
+  const uint32_t peers = __match_any_sync(0xffffffffu, e);
+  const int32_t rw = __popc(peers & lanemask_lt());
+  if (e >= 0 && lane == __ffs(peers) - 1) s_w[warp * N + e] = __popc(peers);
+  __syncthreads();
+  if (e >= 0) {
+    int32_t r = s_pre[e] + rw;
+    for (int w = 0; w < warp; ++w) r += s_w[w * N + e];
+    reinterpret_cast<int32_t*>(pair_rank.p[gl])[p] = r;
   }
-  // publish row g of the [G, N] count matrix to every process's copy
-  for (int e = tid; e < N * n_count_bufs; e += kRouteThreads) {
-    const int b = e / N, ee = e - b * N;
-    reinterpret_cast<int32_t*>(count_bufs.p[b])[g * N + ee] = s_run[ee];
-  }
+}
+
+size_t route_workspace_bytes(int64_t max_tokens, int32_t k, int32_t N, int32_t shard_count) {
+  const int64_t chunks = ceil_div(std::max<int64_t>(max_tokens * k, 1), kRouteThreads);
+  return sizeof(int32_t) * (size_t)(chunks * N * shard_count);
 }
 
 int launch_route(const LocalRows& lr, int32_t N, int32_t k, const ShardPtrs& topk_ids,
                  const ShardPtrs& pair_rank, const ShardPtrs& count_bufs, int32_t n_count_bufs,
-                 cudaStream_t st) {
+                 int32_t* chunk_counts, int64_t n_rows_bound, cudaStream_t st) {
   if (N > kGateMaxN) return SMOE_ERR_UNSUPPORTED;
-  route_kernel<<<lr.shard_count, kRouteThreads, 0, st>>>(lr, N, k, topk_ids, pair_rank,
-                                                        count_bufs, n_count_bufs);
+  const int32_t max_chunks =
+      (int32_t)ceil_div(std::max<int64_t>(n_rows_bound * k, 1), kRouteThreads);
+  const dim3 grid(max_chunks, lr.shard_count);
+  route_count_kernel<<<grid, kRouteThreads, 0, st>>>(lr, N, k, topk_ids, chunk_counts,
+                                                      max_chunks);
+  SMOE_LAUNCH_CHECK();
+  route_rank_kernel<<<grid, kRouteThreads, 0, st>>>(lr, N, k, topk_ids, pair_rank, chunk_counts,
+                                                     max_chunks, count_bufs, n_count_bufs);
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }

@@ -26,9 +26,10 @@ int launch_gate(const LocalRows& lr, const ShardPtrs& hs, int64_t d, const void*
                 const int32_t* slot_owner, const ShardPtrs& topk_ids, const ShardPtrs& topk_w,
                 int64_t* stats, int64_t n_rows_bound, cudaStream_t st);
 
+size_t route_workspace_bytes(int64_t max_tokens, int32_t k, int32_t N, int32_t shard_count);
 int launch_route(const LocalRows& lr, int32_t N, int32_t k, const ShardPtrs& topk_ids,
                  const ShardPtrs& pair_rank, const ShardPtrs& count_bufs, int32_t n_count_bufs,
-                 cudaStream_t st);
+                 int32_t* chunk_counts, int64_t n_rows_bound, cudaStream_t st);
 
 int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
                     const int32_t* counts_mat, const int32_t* slot_owner,
