@@ -527,18 +527,21 @@ __global__ void __launch_bounds__(kRouteThreads)
 route_count_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids,
                    int32_t* __restrict__ chunk_counts, int32_t max_chunks) {
   __shared__ int32_t s_cnt[kGateMaxN];
-  const int gl = blockIdx.y, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const int gl = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
   const int64_t P = (int64_t)lr.counts[lr.shard_begin + gl] * k;
-  if ((int64_t)b * kRouteThreads >= P) return;
-  for (int e = tid; e < N; e += kRouteThreads) s_cnt[e] = 0;
-  __syncthreads();
-  const int64_t p = (int64_t)b * kRouteThreads + tid;
-  const int32_t e = p < P ? reinterpret_cast<const int32_t*>(topk_ids.p[gl])[p] : -1;
-  const uint32_t peers = __match_any_sync(0xffffffffu, e);
-  if (e >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[e], __popc(peers));
-  __syncthreads();
-  int32_t* out = chunk_counts + ((int64_t)gl * max_chunks + b) * N;
-  for (int ee = tid; ee < N; ee += kRouteThreads) out[ee] = s_cnt[ee];
+  const int32_t nchunks = (int32_t)((P + kRouteThreads - 1) / kRouteThreads);
+  for (int b = blockIdx.x; b < nchunks; b += gridDim.x) {
+    for (int e = tid; e < N; e += kRouteThreads) s_cnt[e] = 0;
+    __syncthreads();
+    const int64_t p = (int64_t)b * kRouteThreads + tid;
+    const int32_t e = p < P ? reinterpret_cast<const int32_t*>(topk_ids.p[gl])[p] : -1;
+    const uint32_t peers = __match_any_sync(0xffffffffu, e);
+    if (e >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[e], __popc(peers));
+    __syncthreads();
+    int32_t* out = chunk_counts + ((int64_t)gl * max_chunks + b) * N;
+    for (int ee = tid; ee < N; ee += kRouteThreads) out[ee] = s_cnt[ee];
+    __syncthreads();
+  }
 }
 
 __global__ void __launch_bounds__(kRouteThreads)
@@ -547,36 +550,39 @@ route_rank_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids, ShardP
                   ShardPtrs count_bufs, int32_t n_count_bufs) {
   __shared__ int32_t s_pre[kGateMaxN];
   __shared__ int32_t s_w[32 * kGateMaxN];
-  const int gl = blockIdx.y, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gl = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t g = lr.shard_begin + gl;
   const int64_t P = (int64_t)lr.counts[g] * k;
   const int32_t nchunks = (int32_t)((P + kRouteThreads - 1) / kRouteThreads);
-  if (b > 0 && b >= nchunks) return;
   const int32_t* cc = chunk_counts + (int64_t)gl * max_chunks * N;
-  for (int e = tid; e < N; e += kRouteThreads) {
-    int32_t pre = 0;
-    for (int c = 0; c < b; ++c) pre += cc[c * N + e];
-    s_pre[e] = pre;
-    if (b == 0) {                     // publish row g of the [G, N] count matrix
+  if (blockIdx.x == 0) {             // publish row g of the [G, N] count matrix
+    for (int e = tid; e < N; e += kRouteThreads) {
       int32_t tot = 0;
       for (int c = 0; c < nchunks; ++c) tot += cc[c * N + e];
       for (int i = 0; i < n_count_bufs; ++i)
         reinterpret_cast<int32_t*>(count_bufs.p[i])[g * N + e] = tot;
     }
   }
-  for (int e = tid; e < 32 * N; e += kRouteThreads) s_w[e] = 0;
-  __syncthreads();
-  if (b >= nchunks) return;
-  const int64_t p = (int64_t)b * kRouteThreads + tid;
-  const int32_t e = p < P ? reinterpret_cast<const int32_t*>(topk_ids.p[gl])[p] : -1;
-  const uint32_t peers = __match_any_sync(0xffffffffu, e);
-  const int32_t rw = __popc(peers & lanemask_lt());
-  if (e >= 0 && lane == __ffs(peers) - 1) s_w[warp * N + e] = __popc(peers);
-  __syncthreads();
-  if (e >= 0) {
-    int32_t r = s_pre[e] + rw;
-    for (int w = 0; w < warp; ++w) r += s_w[w * N + e];
-    reinterpret_cast<int32_t*>(pair_rank.p[gl])[p] = r;
+  for (int b = blockIdx.x; b < nchunks; b += gridDim.x) {
+    for (int e = tid; e < N; e += kRouteThreads) {
+      int32_t pre = 0;
+      for (int c = 0; c < b; ++c) pre += cc[c * N + e];
+      s_pre[e] = pre;
+    }
+    for (int e = tid; e < 32 * N; e += kRouteThreads) s_w[e] = 0;
+    __syncthreads();
+    const int64_t p = (int64_t)b * kRouteThreads + tid;
+    const int32_t e = p < P ? reinterpret_cast<const int32_t*>(topk_ids.p[gl])[p] : -1;
+    const uint32_t peers = __match_any_sync(0xffffffffu, e);
+    const int32_t rw = __popc(peers & lanemask_lt());
+    if (e >= 0 && lane == __ffs(peers) - 1) s_w[warp * N + e] = __popc(peers);
+    __syncthreads();
+    if (e >= 0) {
+      int32_t r = s_pre[e] + rw;
+      for (int w = 0; w < warp; ++w) r += s_w[w * N + e];
+      reinterpret_cast<int32_t*>(pair_rank.p[gl])[p] = r;
+    }
+    __syncthreads();
   }
 }
 
@@ -591,7 +597,10 @@ int launch_route(const LocalRows& lr, int32_t N, int32_t k, const ShardPtrs& top
   if (N > kGateMaxN) return SMOE_ERR_UNSUPPORTED;
   const int32_t max_chunks =
       (int32_t)ceil_div(std::max<int64_t>(n_rows_bound * k, 1), kRouteThreads);
-  const dim3 grid(max_chunks, lr.shard_count);
+  // grid-strided over a shard's chunks: enough CTAs for ~2 per SM in total
+  const int32_t per_shard = (int32_t)std::max<int64_t>(
+      1, std::min<int64_t>(max_chunks, ceil_div(2 * num_sms(), lr.shard_count)));
+  const dim3 grid(per_shard, lr.shard_count);
   route_count_kernel<<<grid, kRouteThreads, 0, st>>>(lr, N, k, topk_ids, chunk_counts,
                                                       max_chunks);
   SMOE_LAUNCH_CHECK();
