@@ -649,33 +649,37 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
       pr[0] = a_off; pr[1] = m; pr[2] = e - e0; pr[3] = a_off;
     }
   }
+  // one warp per token: the row is read once and written to its k slots
   const int64_t vecs = d / 8;
-  const int64_t total_pairs = (int64_t)rm.total * k;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t pq = blockIdx.x * (int64_t)(blockDim.x >> 5) + (tid >> 5); pq < total_pairs;
-       pq += nwarps) {
-    const int64_t q = pq / k;
-    const int32_t s = (int32_t)(pq - q * k);
+  for (int64_t q = blockIdx.x * (int64_t)(blockDim.x >> 5) + (tid >> 5); q < rm.total;
+       q += nwarps) {
     int32_t gl; int64_t j;
     decode_row(rm, lr.shard_count, q, gl, j);
     const int32_t g = lr.shard_begin + gl;
-    const int32_t e = reinterpret_cast<const int32_t*>(topk_ids.p[gl])[j * k + s];
-    const int32_t o = slot_owner[e];
-    const int64_t pos =
-        (int64_t)s_off[g * N + e] + reinterpret_cast<const int32_t*>(pair_rank.p[gl])[j * k + s];
-    if (pos >= expert_rows) { if (lane == 0) set_err(err, SMOE_ERRBIT_CAPACITY); continue; }
-    const char* src = hs.p[gl] + j * d * 2;
-    char* dst = xin.p[o] + pos * d * 2;
-    int64_t v = lane;
-    for (; v + 96 < vecs; v += 128) {
-      const uint4 a = ld_nc_v4(src + v * 16), b = ld_nc_v4(src + (v + 32) * 16),
-                  c = ld_nc_v4(src + (v + 64) * 16), e4 = ld_nc_v4(src + (v + 96) * 16);
-      st_v4(dst + v * 16, a); st_v4(dst + (v + 32) * 16, b);
-      st_v4(dst + (v + 64) * 16, c); st_v4(dst + (v + 96) * 16, e4);
+    const int32_t* ids = reinterpret_cast<const int32_t*>(topk_ids.p[gl]) + j * k;
+    const int32_t* rk = reinterpret_cast<const int32_t*>(pair_rank.p[gl]) + j * k;
+    char* dst[kGateMaxK];
+    int32_t nd = 0;
+    for (int s = 0; s < k; ++s) {
+      const int32_t e = ids[s];
+      const int32_t o = slot_owner[e];
+      const int64_t pos = (int64_t)s_off[g * N + e] + rk[s];
+      if (pos >= expert_rows) { if (lane == 0) set_err(err, SMOE_ERRBIT_CAPACITY); continue; }
+      dst[nd++] = xin.p[o] + pos * d * 2;
+      if (lane == 0)
+        reinterpret_cast<int64_t*>(xmeta.p[o])[pos] = ((int64_t)g << 40) | (j * k + s);
     }
-    for (; v < vecs; v += 32) st_v4(dst + v * 16, ld_nc_v4(src + v * 16));
-    if (lane == 0)
-      reinterpret_cast<int64_t*>(xmeta.p[o])[pos] = ((int64_t)g << 40) | (j * k + s);
+    const char* src = hs.p[gl] + j * d * 2;
+    int64_t v = lane;
+    for (; v + 32 < vecs; v += 64) {
+      const uint4 a = ld_nc_v4(src + v * 16), b = ld_nc_v4(src + (v + 32) * 16);
+      for (int i = 0; i < nd; ++i) { st_v4(dst[i] + v * 16, a); st_v4(dst[i] + (v + 32) * 16, b); }
+    }
+    for (; v < vecs; v += 32) {
+      const uint4 a = ld_nc_v4(src + v * 16);
+      for (int i = 0; i < nd; ++i) st_v4(dst[i] + v * 16, a);
+    }
   }
 }
 
@@ -686,7 +690,7 @@ int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
                     int64_t expert_rows, int64_t* problems, int32_t* err, int64_t n_rows_bound,
                     cudaStream_t st) {
   if (N > kGateMaxN || d % 8) return SMOE_ERR_UNSUPPORTED;
-  const int64_t blocks = std::max<int64_t>(1, ceil_div(n_rows_bound * k, 8));
+  const int64_t blocks = std::max<int64_t>(1, ceil_div(n_rows_bound, 8));
   dispatch_kernel<<<grid_cap(blocks, 16), 256, 0, st>>>(lr, N, k, d, counts_mat, slot_owner,
                                                         slot_first, hs, topk_ids, pair_rank, xin,
                                                         xmeta, expert_rows, problems, err);
