@@ -407,7 +407,17 @@ def main():
                "sample": f"first {ns} tokens of the step's batch through oracle/layer_ref "
                          f"(lookup, plan, SRS over {G} partials, fp32 gate, SwiGLU, combine)"}
 
-    launches_per_step = 2 + 1 + 1 + 1 + 1 + 2 + 1 + (4 if world > 1 else 0)
+    # plan 2 + srs 1 + gate 1 + route 2 + dispatch 1 + expert GEMMs 2 + combine/SAG 1
+    # (+ 4 signal-pad barriers when shards span processes)
+    launches_per_step = 2 + 1 + 1 + 2 + 1 + 2 + 1 + (4 if world > 1 else 0)
+    traffic = None
+    tf = ROOT / "profiles" / "r1_traffic.json"
+    if tf.exists():
+        t_info = json.loads(tf.read_text())
+        c = t_info["config"]
+        if (c["workload"], c["tokens_per_gpu"], c["n_gpus"]) == (args.config, args.tokens, world):
+            kk = t_info["kernels"]["grouped_gemm_kernel<SwiGLU> (expert up)"]
+            traffic = kk["dram_read_bytes"] + kk["dram_write_bytes"]
     if rank == 0:
         emit({"metric": "moe_layer_tokens_per_sec", "value": value, "unit": "tokens/s",
               "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -426,7 +436,10 @@ def main():
                             "rest": ms_step - up_ms - down_ms},
               "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel<SwiGLU> (expert up)",
                            "achieved": achieved, "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
-                           "frac": achieved / pk["bf16_sustained"], "traffic": None,
+                           "frac": achieved / pk["bf16_sustained"], "traffic": traffic,
+                           "traffic_unit": "bytes per launch (ncu dram read+write)",
+                           "algorithmic_bytes": 2 * (gemm_rows * d + 2 * f * d * layer.local_slots
+                                                     + gemm_rows * f),
                            "peak_src": pk["src"] + " sustained",
                            "down_gemm_tflops": down_flops / (down_ms / 1e3) / 1e12,
                            "layer_tflops": (up_flops + down_flops) / (ms_step / 1e3) / 1e12},
