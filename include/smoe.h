@@ -145,6 +145,12 @@ int smoe_count_local(const int64_t* experts, int64_t occ, int32_t k,
                      const int64_t* token_dev, int64_t* local_out,
                      int32_t* err, void* stream);
 
+/* schedule_requests_dp (scheduler.py:160-183): request r goes to the
+ * highest-affinity device still open in its window of n_devices consecutive
+ * requests (first maximum wins).  affinities f64[n_requests, n_devices]. */
+int smoe_schedule_requests_dp(const double* affinities, int64_t n_requests,
+                              int32_t n_devices, int64_t* labels, void* stream);
+
 /* ======================================================================= *
  *  MoE layer (Algorithm 2; no reference code)          *
  * ======================================================================= */

@@ -12,7 +12,8 @@ from .predictor import DeviceNGramTable, TokenDeviceTable, encode_history
 from .scheduler import (PAD_TOKEN, GatePermutation, LookupBundle, SchedulerError,
                         ShuffleIndices, apply_expert_shuffle, bundle_memory,
                         bundle_memory_bytes, gate_permutation, lookup_device, lookup_devices,
-                        rebatch_rows, rebatch_tokens, remap_topk, resume_tokens)
+                        rebatch_rows, rebatch_tokens, remap_topk, resume_tokens,
+                        schedule_requests_dp)
 
 __version__ = "0.1.0"
 

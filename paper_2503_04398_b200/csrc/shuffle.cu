@@ -152,9 +152,52 @@ count_local_kernel(const int64_t* __restrict__ experts, int64_t occ, int32_t k,
   if ((threadIdx.x & 31) == 0 && mine) atomicAdd(local_out, mine);
 }
 
+// schedule_requests_dp (scheduler.py:160-183): the open-device mask resets
+// every n_devices requests, so windows are independent -> one thread per
+// window runs the reference's greedy argmax (first maximum wins; numpy's
+// argmax also returns the first NaN) over the still-open devices.
+__global__ void schedule_dp_kernel(const double* __restrict__ aff, int64_t K, int32_t G,
+                                   int64_t* __restrict__ labels) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t r0 = w * G;
+  if (r0 >= K) return;
+  uint64_t open_bits[SMOE_MAX_PLAN_DEVICES / 64];
+  const int words = (G + 63) / 64;
+  for (int i = 0; i < words; ++i) open_bits[i] = ~0ull;
+  const int64_t r1 = (K < r0 + G) ? K : r0 + G;
+  for (int64_t r = r0; r < r1; ++r) {
+    const double* a = aff + r * G;
+    int best = -1;
+    double bv = 0.0;
+    bool nan_hit = false;
+    for (int dv = 0; dv < G; ++dv) {
+      const bool open = (open_bits[dv >> 6] >> (dv & 63)) & 1ull;
+      const double v = open ? a[dv] : -INFINITY;
+      if (v != v) { best = dv; nan_hit = true; break; }         // NaN: numpy argmax stops here
+      if (best < 0 || v > bv) { best = dv; bv = v; }
+    }
+    (void)nan_hit;
+    labels[r] = best;
+    open_bits[best >> 6] &= ~(1ull << (best & 63));
+  }
+}
+
 }  // namespace smoe
 
 using namespace smoe;
+
+extern "C" int smoe_schedule_requests_dp(const double* affinities, int64_t n_requests,
+                                         int32_t n_devices, int64_t* labels, void* stream) {
+  if (n_requests < 0 || n_devices < 1) return SMOE_ERR_INVALID_ARG;
+  if (n_devices > SMOE_MAX_PLAN_DEVICES) return SMOE_ERR_UNSUPPORTED;
+  if (n_requests == 0) return SMOE_OK;
+  if (!affinities || !labels) return SMOE_ERR_INVALID_ARG;
+  const int64_t windows = ceil_div(n_requests, n_devices);
+  schedule_dp_kernel<<<(int)ceil_div(windows, 128), 128, 0, as_stream(stream)>>>(
+      affinities, n_requests, n_devices, labels);
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
 
 extern "C" int smoe_gather_rows(const void* src, int64_t n_src, int32_t elem_bytes,
                                 int64_t row_elems, const int64_t* idx, int64_t n_out,

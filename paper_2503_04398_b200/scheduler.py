@@ -328,13 +328,24 @@ def remap_topk(topk_experts, perm: GatePermutation):
 
 
 def schedule_requests_dp(lengths, affinities, n_devices: int) -> np.ndarray:
-    """Attention-DP request scheduling (scheduler.py:160-183) is outside the
-    hot path and not implemented here."""
-    raise NotImplementedError("schedule_requests_dp is outside the accelerated path "
-                              "(SURVEY.md §8f); use moesched.scheduler.schedule_requests_dp")
+    """Attention-DP request scheduling (scheduler.py:160-183): each request
+    goes to its highest-affinity device still open in the current window of
+    n_devices consecutive decisions.  Windows are independent, so the GPU runs
+    one thread per window."""
+    L = _native.lib()
+    t = _dev.torch()
+    K = len(lengths) if not _dev.is_torch(lengths) else int(lengths.shape[0])
+    aff = _dev.to_device(affinities, t.float64)
+    if tuple(aff.shape) != (K, int(n_devices)):
+        raise SchedulerError("affinity matrix must be (n_requests, n_devices)")
+    out = t.empty(K, dtype=t.int64, device=aff.device)
+    _native.check(L.smoe_schedule_requests_dp(_native.ptr(aff), K, int(n_devices),
+                                              _native.ptr(out), _native.stream_ptr()),
+                  "schedule_requests_dp")
+    return _dev.to_host_like(out, lengths)
 
 
 __all__ = ["PAD_TOKEN", "SchedulerError", "LookupBundle", "ShuffleIndices", "GatePermutation",
            "bundle_memory_bytes", "bundle_memory", "lookup_device", "lookup_devices",
            "rebatch_tokens", "rebatch_rows", "resume_tokens", "gate_permutation",
-           "apply_expert_shuffle", "remap_topk", "device_tables"]
+           "apply_expert_shuffle", "remap_topk", "schedule_requests_dp", "device_tables"]

@@ -170,3 +170,38 @@ def test_gate_transparency_criterion8():
             want = set(np.argsort(-logits, kind="stable")[:k])
             got = set(perm.new_to_old[np.argsort(-sh, kind="stable")[:k]])
             assert got == want
+
+
+def test_schedule_requests_dp_known_answers_and_oracle():
+    # test_scheduler.py:125-139 and test_acceptance.py:196-209 (seed 17)
+    rng = np.random.default_rng(7)
+    E, K = 4, 400
+    aff = rng.random((K, E))
+    labels = S.schedule_requests_dp(np.ones(K), aff, E)
+    for w in range(0, K, E):
+        assert sorted(labels[w:w + E].tolist()) == list(range(E))
+    a2 = np.zeros((8, 4))
+    a2[np.arange(8), np.arange(8) % 4] = 1.0
+    assert S.schedule_requests_dp(np.ones(8), a2, 4).tolist() == [0, 1, 2, 3, 0, 1, 2, 3]
+    rng = np.random.default_rng(17)
+    E, K = 4, 10_000
+    preferred = rng.integers(0, E, size=K)
+    affinities = rng.random((K, E)) * 0.5
+    affinities[np.arange(K), preferred] += 1.0
+    labels = S.schedule_requests_dp(rng.integers(1, 512, size=K), affinities, E)
+    windows = labels.reshape(-1, E)
+    assert np.all(np.sort(windows, axis=1) == np.arange(E))
+    assert (windows[:, 0] == preferred[::E]).mean() >= (E - 1) / E
+    # vs a direct restatement, ragged last window, ties, G = 7
+    for G, K in ((7, 1000), (8, 13), (3, 1)):
+        aff = np.round(rng.random((K, G)), 1)          # many ties -> first max wins
+        want = np.empty(K, dtype=np.int64)
+        for r in range(K):
+            if r % G == 0:
+                open_ = np.ones(G, bool)
+            d = int(np.where(open_, aff[r], -np.inf).argmax())
+            want[r] = d
+            open_[d] = False
+        assert np.array_equal(S.schedule_requests_dp(np.ones(K), aff, G), want)
+    with pytest.raises(S.SchedulerError):
+        S.schedule_requests_dp(np.ones(3), np.zeros((3, 2)), 4)
