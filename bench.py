@@ -174,7 +174,8 @@ def run_reference(args, world, rank):
     # generate a small sample of the same workload on the host (same generator)
     steps = args.steps + args.warmup
     per_step_budget = max(2.0, min(args.cpu_budget, 150.0 / max(steps, 1)))
-    w = synth.make_workload(args.config, n=256, eps=args.eps, seed=args.seed, device=False,
+    n_host = 2048                       # host copy of the workload the samples are cut from
+    w = synth.make_workload(args.config, n=n_host, eps=args.eps, seed=args.seed, device=False,
                             cfg_override=cfg) if cfg["d"] * cfg["f"] * cfg["N"] < 2e9 else None
     if w is None:
         # big configs: numpy weight generation is slow; use torch's CPU RNG for the weights
@@ -212,7 +213,7 @@ def _host_workload_torch(args, cfg):
     from paper_2503_04398_b200 import synth
     small = dict(cfg)
     small["f"] = 128
-    w = synth.make_workload(args.config, n=256, eps=args.eps, seed=args.seed, device=False,
+    w = synth.make_workload(args.config, n=2048, eps=args.eps, seed=args.seed, device=False,
                             cfg_override=small)
     g = torch.Generator().manual_seed(args.seed)
     N, f, d = cfg["N"], cfg["f"], cfg["d"]
