@@ -286,28 +286,25 @@ def main():
         layer.run_device(tok, hist)
     torch.cuda.synchronize()
     layer.check_errors()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    NS = len(N.STAGE_NAMES)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(NS + 1)] for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    pre = [N.STAGE_PLAN, N.STAGE_SRS, N.STAGE_GATE, N.STAGE_ROUTE, N.STAGE_DISPATCH]
     barrier()
     torch.cuda.synchronize()
     with Clocks(local_rank) as clk:
         start.record(stream)
         for s in range(args.steps):
-            layer.run_device(tok, hist, stages=pre)
             ev[s][0].record(stream)
-            layer.run_device(tok, hist, stages=[N.STAGE_EXPERT_UP])
-            ev[s][1].record(stream)
-            layer.run_device(tok, hist, stages=[N.STAGE_EXPERT_DOWN])
-            ev[s][2].record(stream)
-            layer.run_device(tok, hist, stages=[N.STAGE_COMBINE_SAG])
-            ev[s][3].record(stream)
+            for j in range(NS):                 # one stage per launch group, event after each
+                layer.run_device(tok, hist, stages=[j])
+                ev[s][j + 1].record(stream)
         end.record(stream)
         torch.cuda.synchronize()
     barrier()
     ms_total = start.elapsed_time(end)
-    up_ms = np.mean([ev[s][0].elapsed_time(ev[s][1]) for s in range(args.steps)])
-    down_ms = np.mean([ev[s][1].elapsed_time(ev[s][2]) for s in range(args.steps)])
+    stage_ms = {nm: float(np.mean([ev[s][j].elapsed_time(ev[s][j + 1]) for s in range(args.steps)]))
+                for j, nm in enumerate(N.STAGE_NAMES)}
+    up_ms, down_ms = stage_ms["expert_up"], stage_ms["expert_down"]
     ms_total = max_over_ranks(ms_total)
     layer.check_errors()
     st = layer.stats(n)
@@ -327,6 +324,36 @@ def main():
     pk = peaks()
     up_flops = 2.0 * gemm_rows * d * (2 * f)
     down_flops = 2.0 * gemm_rows * f * d
+    # per-stage roofline of this process (algorithmic bytes / flops)
+    n_loc = float(sum(int(x) for x in layer.plan_counts.cpu().numpy()[
+        layer.shard_begin:layer.shard_begin + L]))
+    pairs_loc = n_loc * k
+    grp = int(layer.group_t.item())
+    h = w.hist.shape[1]
+    row = 2.0 * d
+    stage_bytes = {
+        "plan": n * (8 + 8 * h + 12) + 24.0 * n + 8.0 * G * grp,
+        "srs": (G + 1) * n_loc * row,
+        "gate": n_loc * row + pairs_loc * 8,
+        "route": 16.0 * pairs_loc,
+        "dispatch": n_loc * row + pairs_loc * (row + 8),
+        "combine_sag": pairs_loc * row + G * n_loc * row + 8 * n_loc,
+    }
+    stages_rf = []
+    for nm in N.STAGE_NAMES:
+        t_s = stage_ms[nm] / 1e3
+        if nm in ("expert_up", "expert_down"):
+            fl = up_flops if nm == "expert_up" else down_flops
+            stages_rf.append({"stage": nm, "ms": stage_ms[nm], "bound": "tensor",
+                              "algorithmic": fl, "unit": "TFLOP/s",
+                              "achieved": fl / t_s / 1e12, "peak": pk["bf16_sustained"],
+                              "frac": fl / t_s / 1e12 / pk["bf16_sustained"]})
+        else:
+            by = stage_bytes[nm]
+            stages_rf.append({"stage": nm, "ms": stage_ms[nm],
+                              "bound": "latency" if nm in ("plan", "route") else "hbm",
+                              "algorithmic": by, "unit": "GB/s", "achieved": by / t_s / 1e9,
+                              "peak": pk["hbm"], "frac": by / t_s / 1e9 / pk["hbm"]})
     achieved = up_flops / (up_ms / 1e3) / 1e12
     clocks = clk.summary()
 
@@ -433,8 +460,7 @@ def main():
               "local_activation_rate": st["measured_alpha"],
               "a2a_bytes_per_step": st["bytes"]["a2a_dispatch"] + st["bytes"]["a2a_combine"],
               "stage_bytes": st["bytes"], "group_size": st["group_size"],
-              "stages_ms": {"expert_up": up_ms, "expert_down": down_ms,
-                            "rest": ms_step - up_ms - down_ms},
+              "stages_ms": stage_ms, "stages_roofline": stages_rf,
               "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel<SwiGLU> (expert up)",
                            "achieved": achieved, "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
                            "frac": achieved / pk["bf16_sustained"], "traffic": traffic,

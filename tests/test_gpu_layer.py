@@ -175,3 +175,30 @@ def test_forward_async_pipeline_matches_sync():
     again = layer.forward(torch.from_numpy(ws[1].partials).to(torch.bfloat16), ws[1].tokens,
                           ws[1].hist).float().numpy()
     assert np.array_equal(again, want[1])
+
+
+def test_layer_errors_follow_the_reference():
+    from paper_2503_04398_b200.scheduler import SchedulerError
+    w = synth.make_workload("toy", n=200, eps=0.2, seed=4, cfg_override={"G": 4, "N": 16})
+    parts = torch.from_numpy(w.partials).to(torch.bfloat16)
+    # too many tokens for the buffers
+    small = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=100)
+    with pytest.raises(SchedulerError):
+        small.forward(parts, w.tokens, w.hist)
+    # wrong partial shape
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=200)
+    with pytest.raises(SchedulerError):
+        layer.forward(parts[:2], w.tokens, w.hist)
+    # token id outside the vocabulary: numpy IndexError in the reference lookup
+    bad = w.tokens.copy()
+    bad[7] = 10 ** 6
+    with pytest.raises(IndexError):
+        layer.forward(parts, bad, w.hist)
+    # expert-row capacity too small for the routed pairs
+    tight = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=200,
+                         expert_rows=16)
+    with pytest.raises(SchedulerError):
+        tight.forward(parts, w.tokens, w.hist)
+    # the layer recovers after errors
+    out = layer.forward(parts, w.tokens, w.hist)
+    assert torch.isfinite(out.float()).all()
