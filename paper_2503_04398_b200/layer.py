@@ -261,6 +261,8 @@ class SpecMoELayer:
 
         tok = dev_i64(token_ids).reshape(-1)
         n = int(tok.numel())
+        if n > self.max_tokens:
+            raise SchedulerError(f"{n} tokens exceed max_tokens={self.max_tokens}")
         hp = hidden_partials if isinstance(hidden_partials, t.Tensor) else t.as_tensor(
             np.asarray(hidden_partials))
         if hp.dim() == 2:
