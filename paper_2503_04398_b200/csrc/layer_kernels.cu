@@ -268,13 +268,13 @@ gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ 
 // W rows stream through a 4-stage cp.async ring in 128-B rows with a 16-B XOR
 // swizzle (conflict-free ldmatrix).
 constexpr int kMmaKC = 64;                       // bf16 per row per stage (128 B)
-constexpr int kMmaStages = 4;
 // 64 rows per CTA (4 row groups of 16) x S k-splits: warp (r, s) multiplies
 // row group r with k sub-chunk s of every stage, and the S partial logits are
 // summed through shared memory.  The split keeps 8-16 warps per CTA busy on
 // the short, latency-bound k loop (the gate reads only d*2 bytes per token).
 constexpr int kMmaRowsCTA = 64;
-__host__ __device__ constexpr int mma_splits(int nt) { return nt <= 2 ? 4 : 2; }
+__host__ __device__ constexpr int mma_splits(int nt) { return nt <= 2 ? 2 : 2; }
+__host__ __device__ constexpr int mma_stages(int nt) { return nt <= 2 ? 6 : 4; }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
@@ -308,6 +308,7 @@ gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ 
   constexpr int kMmaThreads = 128 * S;
   constexpr int kSubBytes = (kMmaRows + N) * kMmaKC * 2;        // H rows + W rows, 128 B each
   constexpr int kMmaStageBytes = S * kSubBytes;
+  constexpr int kMmaStages = mma_stages(NT);
   extern __shared__ __align__(128) uint8_t gsm[];
   __shared__ RowMap rm;
   __shared__ const char* s_row[kMmaRows];
@@ -478,7 +479,7 @@ static int launch_gate_mma(const LocalRows& lr, const ShardPtrs& hs, int64_t d, 
                            const ShardPtrs& ids, const ShardPtrs& wts, int64_t* stats,
                            int64_t n_rows_bound, cudaStream_t st) {
   constexpr int rows = kMmaRowsCTA, S = mma_splits(NT);
-  const size_t smem = (size_t)kMmaStages * S * ((rows + NT * 8) * kMmaKC * 2);
+  const size_t smem = (size_t)mma_stages(NT) * S * ((rows + NT * 8) * kMmaKC * 2);
   if (d % (kMmaKC * S)) return SMOE_ERR_UNSUPPORTED;
   static bool attr = false;
   if (!attr) {
@@ -672,9 +673,14 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
     }
     const char* src = hs.p[gl] + j * d * 2;
     int64_t v = lane;
-    for (; v + 32 < vecs; v += 64) {
-      const uint4 a = ld_nc_v4(src + v * 16), b = ld_nc_v4(src + (v + 32) * 16);
-      for (int i = 0; i < nd; ++i) { st_v4(dst[i] + v * 16, a); st_v4(dst[i] + (v + 32) * 16, b); }
+    for (; v + 224 < vecs; v += 256) {                 // 8 loads in flight per lane
+      uint4 a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = ld_nc_v4(src + (v + 32 * u) * 16);
+      for (int i = 0; i < nd; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) st_v4(dst[i] + (v + 32 * u) * 16, a[u]);
+      }
     }
     for (; v < vecs; v += 32) {
       const uint4 a = ld_nc_v4(src + v * 16);
