@@ -612,6 +612,9 @@ int launch_route(const LocalRows& lr, int32_t N, int32_t k, const ShardPtrs& top
 }
 
 // ------------------------------------------------------------------ K5b dispatch
+#ifndef DISPATCH_ST
+#define DISPATCH_ST st_cs_v4
+#endif
 __global__ void __launch_bounds__(256)
 dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __restrict__ C,
                 const int32_t* __restrict__ slot_owner, const int32_t* __restrict__ slot_first,
@@ -679,12 +682,12 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
       for (int u = 0; u < 8; ++u) a[u] = ld_nc_v4(src + (v + 32 * u) * 16);
       for (int i = 0; i < nd; ++i) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) st_v4(dst[i] + (v + 32 * u) * 16, a[u]);
+        for (int u = 0; u < 8; ++u) DISPATCH_ST(dst[i] + (v + 32 * u) * 16, a[u]);
       }
     }
     for (; v < vecs; v += 32) {
       const uint4 a = ld_nc_v4(src + v * 16);
-      for (int i = 0; i < nd; ++i) st_v4(dst[i] + v * 16, a);
+      for (int i = 0; i < nd; ++i) DISPATCH_ST(dst[i] + v * 16, a);
     }
   }
 }
