@@ -53,6 +53,18 @@ __device__ __forceinline__ void load_rowmap(RowMap& rm, const LocalRows& lr) {
   __syncthreads();
 }
 
+// Copy a pointer table out of kernel-parameter space with constant indices
+// (fully unrolled).  Indexing a parameter array with a runtime value makes
+// every thread copy the whole struct to its local stack -- hundreds of bytes
+// of local-memory traffic per thread, which showed up as 2x DRAM writes in
+// the dispatch kernel.  Callers index the shared copy instead.
+__device__ __forceinline__ void stage_ptrs(char** dst, const ShardPtrs& src) {
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < SMOE_MAX_SHARDS; ++i) dst[i] = src.p[i];
+  }
+}
+
 // q in [0, total) -> (local shard index, row inside the group)
 __device__ __forceinline__ void decode_row(const RowMap& rm, int32_t shard_count, int64_t q,
                                            int32_t& gl, int64_t& j) {
@@ -68,6 +80,8 @@ template <int G>
 __global__ void __launch_bounds__(256)
 srs_kernel(LocalRows lr, ShardPtrs partials, int64_t d, ShardPtrs hs) {
   __shared__ RowMap rm;
+  __shared__ char* s_hs[SMOE_MAX_SHARDS];
+  stage_ptrs(s_hs, hs);
   load_rowmap(rm, lr);
   const int lane = threadIdx.x & 31;
   const int64_t vecs = d / 8;
@@ -81,7 +95,7 @@ srs_kernel(LocalRows lr, ShardPtrs partials, int64_t d, ShardPtrs hs) {
     decode_row(rm, lr.shard_count, q, gl, j);
     const int64_t g = lr.shard_begin + gl;
     const int64_t row_off = lr.forward[g * rm.group + j] * d * 2;
-    char* out = hs.p[gl] + j * d * 2;
+    char* out = s_hs[gl] + j * d * 2;
     for (int64_t v = lane; v < vecs; v += 64) {
       const bool two = v + 32 < vecs;
       uint4 x[G], y[G];
@@ -138,6 +152,12 @@ gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ 
             const int32_t* __restrict__ slot_owner, ShardPtrs topk_ids, ShardPtrs topk_w,
             int64_t* stats) {
   __shared__ RowMap rm;
+  __shared__ char* s_hs[SMOE_MAX_SHARDS];
+  __shared__ char* s_ids[SMOE_MAX_SHARDS];
+  __shared__ char* s_wts[SMOE_MAX_SHARDS];
+  stage_ptrs(s_hs, hs);
+  stage_ptrs(s_ids, topk_ids);
+  stage_ptrs(s_wts, topk_w);
   __shared__ uint32_t s_h[kGateRows * kGatePad];
   __shared__ uint32_t s_w[kGateMaxN * kGatePad];
   __shared__ float s_logit[kGateRows * (kGateMaxN + 1)];
@@ -166,7 +186,7 @@ gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ 
         const int r = e / kGateWords, w = e - r * kGateWords;
         uint32_t v = 0;
         if (s_gl[r] >= 0 && kc + w < words)
-          v = reinterpret_cast<const uint32_t*>(hs.p[s_gl[r]] + s_j[r] * d * 2)[kc + w];
+          v = reinterpret_cast<const uint32_t*>(s_hs[s_gl[r]] + s_j[r] * d * 2)[kc + w];
         s_h[r * kGatePad + w] = v;
       }
       for (int e = tid; e < N * kGateWords; e += 256) {
@@ -239,8 +259,8 @@ gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ 
       }
       if (lane == 0) {
         const int64_t g = lr.shard_begin + gl;
-        int32_t* ids = reinterpret_cast<int32_t*>(topk_ids.p[gl]) + s_j[r] * k;
-        float* wts = reinterpret_cast<float*>(topk_w.p[gl]) + s_j[r] * k;
+        int32_t* ids = reinterpret_cast<int32_t*>(s_ids[gl]) + s_j[r] * k;
+        float* wts = reinterpret_cast<float*>(s_wts[gl]) + s_j[r] * k;
         const float scale = renorm ? 1.0f / psum : 1.0f;
         for (int s = 0; s < k; ++s) {
           ids[s] = sel_e[s];
@@ -311,6 +331,12 @@ gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ 
   constexpr int kMmaStages = mma_stages(NT);
   extern __shared__ __align__(128) uint8_t gsm[];
   __shared__ RowMap rm;
+  __shared__ char* s_hs[SMOE_MAX_SHARDS];
+  __shared__ char* s_ids[SMOE_MAX_SHARDS];
+  __shared__ char* s_wts[SMOE_MAX_SHARDS];
+  stage_ptrs(s_hs, hs);
+  stage_ptrs(s_ids, topk_ids);
+  stage_ptrs(s_wts, topk_w);
   __shared__ const char* s_row[kMmaRows];
   __shared__ int32_t s_gl[kMmaRows];
   __shared__ int64_t s_j[kMmaRows];
@@ -327,7 +353,7 @@ gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ 
       if (q < rm.total) decode_row(rm, lr.shard_count, q, gl, j);
       s_gl[tid] = gl;
       s_j[tid] = j;
-      s_row[tid] = gl >= 0 ? hs.p[gl] + j * d * 2 : nullptr;
+      s_row[tid] = gl >= 0 ? s_hs[gl] + j * d * 2 : nullptr;
     }
     if (tid == 0) { s_local = 0; s_remote = 0; }
     __syncthreads();
@@ -450,8 +476,8 @@ gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ 
 #pragma unroll
         for (int s = 0; s < kGateMaxK; ++s) if (s == lane) { p = sel_p[s]; e = sel_e[s]; }
         const int64_t g = lr.shard_begin + gl;
-        reinterpret_cast<int32_t*>(topk_ids.p[gl])[s_j[r] * k + lane] = e;
-        reinterpret_cast<float*>(topk_w.p[gl])[s_j[r] * k + lane] = renorm ? p / psum : p;
+        reinterpret_cast<int32_t*>(s_ids[gl])[s_j[r] * k + lane] = e;
+        reinterpret_cast<float*>(s_wts[gl])[s_j[r] * k + lane] = renorm ? p / psum : p;
         if (slot_owner[e] == g) ++my_local; else ++my_remote;
       }
     }
@@ -528,14 +554,17 @@ __global__ void __launch_bounds__(kRouteThreads)
 route_count_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids,
                    int32_t* __restrict__ chunk_counts, int32_t max_chunks) {
   __shared__ int32_t s_cnt[kGateMaxN];
+  __shared__ char* s_ids[SMOE_MAX_SHARDS];
+  stage_ptrs(s_ids, topk_ids);
   const int gl = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
   const int64_t P = (int64_t)lr.counts[lr.shard_begin + gl] * k;
   const int32_t nchunks = (int32_t)((P + kRouteThreads - 1) / kRouteThreads);
+  __syncthreads();
   for (int b = blockIdx.x; b < nchunks; b += gridDim.x) {
     for (int e = tid; e < N; e += kRouteThreads) s_cnt[e] = 0;
     __syncthreads();
     const int64_t p = (int64_t)b * kRouteThreads + tid;
-    const int32_t e = p < P ? reinterpret_cast<const int32_t*>(topk_ids.p[gl])[p] : -1;
+    const int32_t e = p < P ? reinterpret_cast<const int32_t*>(s_ids[gl])[p] : -1;
     const uint32_t peers = __match_any_sync(0xffffffffu, e);
     if (e >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[e], __popc(peers));
     __syncthreads();
@@ -551,6 +580,13 @@ route_rank_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids, ShardP
                   ShardPtrs count_bufs, int32_t n_count_bufs) {
   __shared__ int32_t s_pre[kGateMaxN];
   __shared__ int32_t s_w[32 * kGateMaxN];
+  __shared__ char* s_ids[SMOE_MAX_SHARDS];
+  __shared__ char* s_rank[SMOE_MAX_SHARDS];
+  __shared__ char* s_cb[SMOE_MAX_SHARDS];
+  stage_ptrs(s_ids, topk_ids);
+  stage_ptrs(s_rank, pair_rank);
+  stage_ptrs(s_cb, count_bufs);
+  __syncthreads();
   const int gl = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t g = lr.shard_begin + gl;
   const int64_t P = (int64_t)lr.counts[g] * k;
@@ -561,7 +597,7 @@ route_rank_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids, ShardP
       int32_t tot = 0;
       for (int c = 0; c < nchunks; ++c) tot += cc[c * N + e];
       for (int i = 0; i < n_count_bufs; ++i)
-        reinterpret_cast<int32_t*>(count_bufs.p[i])[g * N + e] = tot;
+        reinterpret_cast<int32_t*>(s_cb[i])[g * N + e] = tot;
     }
   }
   for (int b = blockIdx.x; b < nchunks; b += gridDim.x) {
@@ -573,7 +609,7 @@ route_rank_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids, ShardP
     for (int e = tid; e < 32 * N; e += kRouteThreads) s_w[e] = 0;
     __syncthreads();
     const int64_t p = (int64_t)b * kRouteThreads + tid;
-    const int32_t e = p < P ? reinterpret_cast<const int32_t*>(topk_ids.p[gl])[p] : -1;
+    const int32_t e = p < P ? reinterpret_cast<const int32_t*>(s_ids[gl])[p] : -1;
     const uint32_t peers = __match_any_sync(0xffffffffu, e);
     const int32_t rw = __popc(peers & lanemask_lt());
     if (e >= 0 && lane == __ffs(peers) - 1) s_w[warp * N + e] = __popc(peers);
@@ -581,7 +617,7 @@ route_rank_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids, ShardP
     if (e >= 0) {
       int32_t r = s_pre[e] + rw;
       for (int w = 0; w < warp; ++w) r += s_w[w * N + e];
-      reinterpret_cast<int32_t*>(pair_rank.p[gl])[p] = r;
+      reinterpret_cast<int32_t*>(s_rank[gl])[p] = r;
     }
     __syncthreads();
   }
@@ -624,6 +660,16 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
   __shared__ int32_t s_M[kGateMaxN];
   __shared__ int32_t s_seg[kGateMaxN];
   __shared__ int32_t s_off[SMOE_MAX_SHARDS * kGateMaxN];
+  __shared__ char* s_hs[SMOE_MAX_SHARDS];
+  __shared__ char* s_ids[SMOE_MAX_SHARDS];
+  __shared__ char* s_rank[SMOE_MAX_SHARDS];
+  __shared__ char* s_xin[SMOE_MAX_SHARDS];
+  __shared__ char* s_xmeta[SMOE_MAX_SHARDS];
+  stage_ptrs(s_hs, hs);
+  stage_ptrs(s_ids, topk_ids);
+  stage_ptrs(s_rank, pair_rank);
+  stage_ptrs(s_xin, xin);
+  stage_ptrs(s_xmeta, xmeta);
   const int G = lr.n_shards;
   const int tid = threadIdx.x, lane = tid & 31;
   for (int e = tid; e < N; e += blockDim.x) {
@@ -661,8 +707,8 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
     int32_t gl; int64_t j;
     decode_row(rm, lr.shard_count, q, gl, j);
     const int32_t g = lr.shard_begin + gl;
-    const int32_t* ids = reinterpret_cast<const int32_t*>(topk_ids.p[gl]) + j * k;
-    const int32_t* rk = reinterpret_cast<const int32_t*>(pair_rank.p[gl]) + j * k;
+    const int32_t* ids = reinterpret_cast<const int32_t*>(s_ids[gl]) + j * k;
+    const int32_t* rk = reinterpret_cast<const int32_t*>(s_rank[gl]) + j * k;
     char* dst[kGateMaxK];
     int32_t nd = 0;
     for (int s = 0; s < k; ++s) {
@@ -670,11 +716,11 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
       const int32_t o = slot_owner[e];
       const int64_t pos = (int64_t)s_off[g * N + e] + rk[s];
       if (pos >= expert_rows) { if (lane == 0) set_err(err, SMOE_ERRBIT_CAPACITY); continue; }
-      dst[nd++] = xin.p[o] + pos * d * 2;
+      dst[nd++] = s_xin[o] + pos * d * 2;
       if (lane == 0)
-        reinterpret_cast<int64_t*>(xmeta.p[o])[pos] = ((int64_t)g << 40) | (j * k + s);
+        reinterpret_cast<int64_t*>(s_xmeta[o])[pos] = ((int64_t)g << 40) | (j * k + s);
     }
-    const char* src = hs.p[gl] + j * d * 2;
+    const char* src = s_hs[gl] + j * d * 2;
     int64_t v = lane;
     for (; v + 224 < vecs; v += 256) {                 // 8 loads in flight per lane
       uint4 a[8];
@@ -713,6 +759,14 @@ __global__ void __launch_bounds__(256)
 combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtrs topk_w,
                    ShardPtrs outs, HistUpdate hu) {
   __shared__ RowMap rm;
+  __shared__ char* s_y[SMOE_MAX_SHARDS];
+  __shared__ char* s_wts[SMOE_MAX_SHARDS];
+  __shared__ char* s_ids[SMOE_MAX_SHARDS];
+  __shared__ char* s_hist[SMOE_MAX_SHARDS];
+  stage_ptrs(s_y, ypair);
+  stage_ptrs(s_wts, topk_w);
+  stage_ptrs(s_ids, hu.topk_ids);
+  stage_ptrs(s_hist, hu.hist_outs);
   load_rowmap(rm, lr);
   const int lane = threadIdx.x & 31;
   const int64_t vecs = d / 8;
@@ -732,19 +786,19 @@ combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtr
       const int64_t L = hu.hist_len;
       int64_t v;
       if (lane == L - 1) {
-        const int32_t top1 = reinterpret_cast<const int32_t*>(hu.topk_ids.p[gl])[j * k];
+        const int32_t top1 = reinterpret_cast<const int32_t*>(s_ids[gl])[j * k];
         v = hu.slot_owner[top1];
       } else {
         v = hu.hist_in ? hu.hist_in[i * L + lane + 1] : g;   // no history yet: this shard
       }
       for (int b = 0; b < hu.n_hist_outs; ++b)
-        reinterpret_cast<int64_t*>(hu.hist_outs.p[b])[i * L + lane] = v;
+        reinterpret_cast<int64_t*>(s_hist[b])[i * L + lane] = v;
     }
-    const float* w = reinterpret_cast<const float*>(topk_w.p[gl]) + j * k;
+    const float* w = reinterpret_cast<const float*>(s_wts[gl]) + j * k;
     float wk[kGateMaxK];
 #pragma unroll
     for (int s = 0; s < kGateMaxK; ++s) wk[s] = s < k ? w[s] : 0.f;
-    const char* y = ypair.p[gl] + j * k * d * 2;
+    const char* y = s_y[gl] + j * k * d * 2;
     for (int64_t v = lane; v < vecs; v += 32) {
       uint4 yv[kGateMaxK];
 #pragma unroll
