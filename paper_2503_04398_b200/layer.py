@@ -37,7 +37,9 @@ N = _native
 class SpecMoELayer:
     def __init__(self, bundle, gate_w, w1, w3, w2, *, top_k: int, max_tokens: int,
                  gate_b=None, renormalize: bool = True, expert_rows: int | None = None,
-                 group=None):
+                 group=None, shared_from: "SpecMoELayer | None" = None):
+        """shared_from: another layer whose s-EG-ordered weights this one
+        reuses (no copy, no repacking) -- micro-batches of one layer."""
         t = _dev.torch()
         self.lib = N.lib()
         self.bundle = bundle
@@ -46,7 +48,7 @@ class SpecMoELayer:
             raise SchedulerError(f"{self.G} shards exceed the supported {N.MAX_SHARDS}")
         gate_w = _dev.to_device(gate_w, t.bfloat16)
         self.N, self.d = int(gate_w.shape[0]), int(gate_w.shape[1])
-        self.f = int(w1.shape[1])
+        self.f = int((shared_from.f if shared_from is not None else w1.shape[1]))
         self.k = int(top_k)
         self.max_tokens = int(max_tokens)
         self.expert_rows = int(expert_rows or self.max_tokens * self.k)
@@ -63,7 +65,21 @@ class SpecMoELayer:
         self.shard_begin, self.shard_count = rank * spp, spp
         self.world, self.rank = world, rank
 
-        # ---- s-EG placement (scheduler.py:200-224), computed on the GPU
+        if shared_from is not None:
+            src = shared_from
+            for a in ("perm", "slot_owner", "slot_first", "local_slots", "w_gate", "b_gate",
+                      "w13", "w2"):
+                setattr(self, a, getattr(src, a))
+        else:
+            self._place_weights(labels, gate_w, gate_b, w1, w3, w2)
+        self.tables = device_tables(bundle)
+        self._alloc_buffers()
+        self._create_handle()
+
+    def _place_weights(self, labels, gate_w, gate_b, w1, w3, w2):
+        """s-EG placement (scheduler.py:200-224), computed on the GPU, and the
+        resident experts' weights in slot order."""
+        t = _dev.torch()
         self.perm = gate_permutation(labels, self.G)
         n2o = np.asarray(self.perm.new_to_old)
         self.slot_owner = labels[n2o].astype(np.int32)          # cluster of each slot
@@ -88,11 +104,6 @@ class SpecMoELayer:
         if self.local_slots:
             N.check(self.lib.smoe_pack_w13(N.ptr(w1l), N.ptr(w3l), self.local_slots, self.f,
                                            self.d, N.ptr(self.w13), N.stream_ptr()), "pack_w13")
-        del w1l, w3l
-
-        self.tables = device_tables(bundle)
-        self._alloc_buffers()
-        self._create_handle()
 
     # ------------------------------------------------------------ buffers
     def _alloc_buffers(self):
@@ -456,3 +467,111 @@ class _Done:
 
     def result(self):
         return self._out
+
+
+class MicroBatchedSpecMoE:
+    """One MoE layer run as M micro-batches on M streams, so the HBM/NVLink
+    stages of one micro-batch (SRS, gate, dispatch, combine+SAG) run while
+    the persistent tcgen05 GEMMs of another occupy the tensor cores (the
+    GEMM CTAs leave registers and shared memory for mover CTAs on every SM).
+
+    Every token's result is independent of how the batch is cut, so the
+    output is bit-identical to `SpecMoELayer`.  The micro-batch layers share
+    the packed weights and write their partial inputs / outputs / next-layer
+    histories through views of one full-size buffer (no copies).
+    Single-process (all shards resident) only.
+    """
+
+    def __init__(self, bundle, gate_w, w1, w3, w2, *, top_k: int, max_tokens: int,
+                 microbatches: int = 2, **kw):
+        t = _dev.torch()
+        if kw.get("group") is not None:
+            raise SchedulerError("micro-batching needs all shards in this process")
+        self.M = int(microbatches)
+        self.max_tokens = int(max_tokens)
+        self.chunk = -(-self.max_tokens // self.M)
+        first = SpecMoELayer(bundle, gate_w, w1, w3, w2, top_k=top_k, max_tokens=self.chunk, **kw)
+        self.layers = [first] + [
+            SpecMoELayer(bundle, gate_w, None, None, None, top_k=top_k, max_tokens=self.chunk,
+                         shared_from=first, **kw) for _ in range(self.M - 1)]
+        G, d = first.G, first.d
+        dev = first.w_gate.device
+        self.G, self.d = G, d
+        self.partial = t.zeros((G, self.max_tokens, d), dtype=t.bfloat16, device=dev)
+        self.out = t.empty((G, self.max_tokens, d), dtype=t.bfloat16, device=dev)
+        h = max(first.tables.ngram_n, 1)
+        self.hist_next = t.zeros((self.max_tokens, h), dtype=t.int64, device=dev)
+        for c, L in enumerate(self.layers):
+            lo = c * self.chunk
+            hi = min(self.max_tokens, lo + self.chunk)
+            P = self.partial[:, lo:hi]
+            L._bind_partial(P)
+            L.partial, L.out = P, self.out[:, lo:hi]       # drop the layer's own copies
+            L._bound_partial = P
+            for g in range(G):
+                N.check(L.lib.smoe_layer_bind(L._h, N.BUF_OUT, g, N.ptr(self.out[g, lo:])), "bind")
+                N.check(L.lib.smoe_layer_bind(L._h, N.BUF_HIST_OUT, g,
+                                              N.ptr(self.hist_next[lo:])), "bind")
+        self.streams = [t.cuda.current_stream()] + [t.cuda.Stream() for _ in range(self.M - 1)]
+        self.events = [t.cuda.Event() for _ in range(self.M)]
+
+    def partial_views(self, n: int):
+        return self.partial[:, :n]
+
+    def out_view(self, n: int, shard: int = 0):
+        return self.out[shard, :n]
+
+    def next_history(self, n: int):
+        return self.hist_next[:n]
+
+    def run_device(self, tokens_t, hist_t=None):
+        """All micro-batches of one forward; returns the output view.  The
+        GEMMs run in micro-batch order (each waits for the previous one's
+        down projection), the movers of neighbouring micro-batches overlap
+        them."""
+        t = _dev.torch()
+        n = int(tokens_t.shape[0])
+        if n > self.max_tokens:
+            raise SchedulerError(f"{n} tokens exceed max_tokens={self.max_tokens}")
+        main = t.cuda.current_stream()
+        for s in self.streams[1:]:
+            s.wait_stream(main)
+        pre = [N.STAGE_PLAN, N.STAGE_SRS, N.STAGE_GATE, N.STAGE_ROUTE, N.STAGE_DISPATCH]
+        parts = []
+        for c, L in enumerate(self.layers):
+            lo = c * self.chunk
+            hi = min(n, lo + self.chunk)
+            if hi <= lo:
+                continue
+            parts.append((c, L, lo, hi))
+        for c, L, lo, hi in parts:                    # movers of every micro-batch first
+            h = None if hist_t is None else hist_t[lo:hi]
+            L.run_device(tokens_t[lo:hi], h, stream=self.streams[c], stages=pre)
+        prev = None
+        for c, L, lo, hi in parts:                    # GEMMs in order, combine overlaps next
+            s = self.streams[c]
+            h = None if hist_t is None else hist_t[lo:hi]
+            if prev is not None:
+                s.wait_event(prev)
+            L.run_device(tokens_t[lo:hi], h, stream=s,
+                         stages=[N.STAGE_EXPERT_UP, N.STAGE_EXPERT_DOWN])
+            self.events[c].record(s)
+            prev = self.events[c]
+            L.run_device(tokens_t[lo:hi], h, stream=s, stages=[N.STAGE_COMBINE_SAG])
+        for s in self.streams[1:]:
+            main.wait_stream(s)
+        return self.out_view(n)
+
+    def check_errors(self):
+        for L in self.layers:
+            L.check_errors()
+
+    def stats(self, n: int | None = None) -> dict:
+        st = [L.stats() for L in self.layers]
+        loc = sum(x["local_tokens"] for x in st)
+        rem = sum(x["remote_tokens"] for x in st)
+        return {"local_tokens": loc, "remote_tokens": rem,
+                "measured_alpha": loc / max(loc + rem, 1),
+                "bytes": {k: sum(x["bytes"][k] for x in st) for k in st[0]["bytes"]},
+                "group_size": max(x["group_size"] for x in st),
+                "microbatches": self.M}

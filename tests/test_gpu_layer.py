@@ -202,3 +202,28 @@ def test_layer_errors_follow_the_reference():
     # the layer recovers after errors
     out = layer.forward(parts, w.tokens, w.hist)
     assert torch.isfinite(out.float()).all()
+
+
+@pytest.mark.parametrize("n,M", [(600, 2), (601, 3), (100, 2)])
+def test_microbatched_matches_single(n, M):
+    """Micro-batched streams give bit-identical outputs and histories."""
+    from paper_2503_04398_b200.layer import MicroBatchedSpecMoE
+    over = {"G": 4, "N": 16}
+    w = synth.make_workload("toy", n=n, eps=0.25, seed=40 + n, cfg_override=over)
+    ref_layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=n)
+    ref = ref_layer.forward(torch.from_numpy(w.partials).to(torch.bfloat16), w.tokens, w.hist)
+    ref_hist = ref_layer.next_history(n).clone()
+    mb = MicroBatchedSpecMoE(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=n,
+                             microbatches=M)
+    mb.partial_views(n).copy_(torch.from_numpy(w.partials).to(torch.bfloat16).cuda())
+    tok = torch.as_tensor(w.tokens, device="cuda")
+    hist = torch.as_tensor(w.hist, device="cuda")
+    for _ in range(2):
+        out = mb.run_device(tok, hist)
+        torch.cuda.synchronize()
+        mb.check_errors()
+        assert torch.equal(out.cpu(), ref.cpu() if ref.is_cuda else ref)
+        assert torch.equal(mb.next_history(n), ref_hist)
+    st = mb.stats()
+    rs = ref_layer.stats()
+    assert st["local_tokens"] + st["remote_tokens"] == rs["local_tokens"] + rs["remote_tokens"]

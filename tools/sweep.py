@@ -19,7 +19,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 
-def measure(name, tokens, eps, ep=None, steps=10, warmup=3, seed=0):
+def measure(name, tokens, eps, ep=None, steps=10, warmup=3, seed=0, microbatches=1):
     import torch
     from paper_2503_04398_b200 import SpecMoELayer, comm, synth
     from paper_2503_04398_b200 import _native as N
@@ -29,7 +29,12 @@ def measure(name, tokens, eps, ep=None, steps=10, warmup=3, seed=0):
     G, k, d, f = cfg["G"], cfg["k"], cfg["d"], cfg["f"]
     t0 = time.time()
     w = synth.make_workload(name, n=tokens, eps=eps, seed=seed, device=True, cfg_override=cfg)
-    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=k, max_tokens=tokens)
+    if microbatches > 1:
+        from paper_2503_04398_b200.layer import MicroBatchedSpecMoE
+        layer = MicroBatchedSpecMoE(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=k,
+                                    max_tokens=tokens, microbatches=microbatches)
+    else:
+        layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=k, max_tokens=tokens)
     layer.partial_views(tokens).copy_(w.partials)
     del w.partials
     tok = torch.as_tensor(w.tokens, device="cuda")
@@ -38,6 +43,22 @@ def measure(name, tokens, eps, ep=None, steps=10, warmup=3, seed=0):
         layer.run_device(tok, hist)
     torch.cuda.synchronize()
     layer.check_errors()
+    if microbatches > 1:
+        s = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(steps):
+            layer.run_device(tok, hist)
+        e1.record(s)
+        torch.cuda.synchronize()
+        step_ms = e0.elapsed_time(e1) / steps
+        st = layer.stats(tokens)
+        out = {"config": name, "ep": G, "tokens": tokens, "eps": eps, "microbatches": microbatches,
+               "alpha": st["measured_alpha"], "ms_per_step": step_ms,
+               "tokens_per_s": tokens / (step_ms / 1e3), "setup_s": time.time() - t0}
+        del layer
+        torch.cuda.empty_cache()
+        return out
     names = N.STAGE_NAMES
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
           for _ in range(steps)]
@@ -73,7 +94,19 @@ def measure(name, tokens, eps, ep=None, steps=10, warmup=3, seed=0):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--microbatch-ab", action="store_true",
+                    help="interleaved 1 vs 2 vs 4 micro-batches on the main configs")
     args = ap.parse_args()
+    if args.microbatch_ab:
+        for rep in range(2):
+            for name, tok in (("mixtral", 16384), ("dsv2_lite", 16384), ("qwen2_57b", 16384),
+                              ("mixtral", 65536)):
+                for mb in (1, 2, 4):
+                    r = measure(name, tok, 0.2, microbatches=mb)
+                    print(json.dumps({k: r[k] for k in ("config", "tokens", "ms_per_step",
+                                                        "tokens_per_s", "alpha")} |
+                                     {"microbatches": mb, "rep": rep}), flush=True)
+        return
     pts = [("mixtral", 4096, 0.2, None), ("mixtral", 16384, 0.2, None),
            ("mixtral", 65536, 0.2, None),
            ("dsv2_lite", 16384, 0.2, None), ("dsv2_lite", 65536, 0.2, None),
