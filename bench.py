@@ -124,9 +124,11 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
-def oracle_sample(bundle, partials, tokens, hist, gate_w, w1, w3, w2, k, budget, n_max):
-    """Time the CPU oracle (oracle/layer_ref) on the first n_s tokens, n_s
-    calibrated so one call costs about `budget` seconds."""
+def oracle_sample(bundle, partials, tokens, hist, gate_w, w1, w3, w2, k, budget, n_max,
+                  fixed: int | None = None):
+    """Time the CPU oracle (oracle/layer_ref) on the first n_s tokens: n_s =
+    `fixed` when given, else calibrated so one call costs about `budget`
+    seconds (capped at n_max)."""
     from oracle import layer_ref
     tab = bundle
 
@@ -141,6 +143,8 @@ def oracle_sample(bundle, partials, tokens, hist, gate_w, w1, w3, w2, k, budget,
                                 w1=w1, w3=w3, w2=w2, k=k)
         return time.perf_counter() - t0
 
+    if fixed is not None:
+        return fixed, run(fixed)
     ns = min(64, n_max)
     t = run(ns)
     ns2 = int(min(n_max, max(ns, ns * budget / max(t, 1e-3))))
@@ -187,7 +191,7 @@ def run_reference(args, world, rank):
     times = []
     for i in range(steps):
         _, t = oracle_sample(w.bundle, w.partials, w.tokens, w.hist, gw, w1, w3, w2, cfg["k"],
-                             0.0, ns)
+                             0.0, ns, fixed=ns)
         if i >= args.warmup:
             times.append(t)
     total = sum(times)
