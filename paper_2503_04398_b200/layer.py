@@ -307,7 +307,9 @@ class SpecMoELayer:
         released as soon as batch i's SRS has read it), and the D2H of batch
         i overlaps the first stages of batch i+1.  Single-process layers only
         (peer processes read the partial buffers in place).  Data-dependent
-        errors surface in `.result()` of a later batch at the latest.
+        errors of a batch surface in its own `.result()`, which waits for
+        that batch's D2H only (never drains the compute stream, so the H2D
+        of the next batch is already queued behind the running one).
         """
         t = _dev.torch()
         if self.group is not None:
@@ -345,6 +347,10 @@ class SpecMoELayer:
                                                                    N.STAGE_COMBINE_SAG))
             cs.wait_event(st["d2h_done"])          # previous output fully read out
             self.run_device(tok[:n], hp_t, stream=cs, stages=[N.STAGE_COMBINE_SAG])
+            # this batch's error flag, read out before the next batch's plan
+            # resets it (stream order); the host reads it in .result()
+            err = t.empty(1, dtype=t.int32, pin_memory=True)
+            err.copy_(self.err, non_blocking=True)
             st["free_ids"][slot].record(cs)
             st["done"].record(cs)
         # ---- D2H on its own stream
@@ -356,7 +362,7 @@ class SpecMoELayer:
             out.copy_(self.out_view(n), non_blocking=True)
             st["d2h_done"].record(st["d2h"])
             ev.record(st["d2h"])
-        return _Pending(self, out, ev)
+        return _Pending(self, out, ev, err)
 
     def _pipeline(self):
         st = getattr(self, "_pipe", None)
@@ -381,7 +387,10 @@ class SpecMoELayer:
 
     # ------------------------------------------------------------ results
     def check_errors(self):
-        bits = int(self.err.item())
+        self._raise_for(int(self.err.item()))
+
+    @staticmethod
+    def _raise_for(bits: int):
         if bits & N.ERRBIT_CAPACITY:
             raise SchedulerError("expert_rows capacity exceeded; raise expert_rows")
         if bits & N.ERRBIT_DEVICE_RANGE:
@@ -446,15 +455,17 @@ class SpecMoELayer:
 class _Pending:
     """Handle of a `forward_async` batch."""
 
-    def __init__(self, layer, out, event):
-        self._layer, self._out, self._event = layer, out, event
+    def __init__(self, layer, out, event, err):
+        self._layer, self._out, self._event, self._err = layer, out, event, err
 
     def done(self) -> bool:
         return self._event.query()
 
     def result(self):
+        # waits for this batch's D2H only: the compute stream keeps running
+        # the next batch (a device-flag .item() here would drain it)
         self._event.synchronize()
-        self._layer.check_errors()
+        self._layer._raise_for(int(self._err[0]))
         return self._out
 
 

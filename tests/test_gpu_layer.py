@@ -227,3 +227,24 @@ def test_microbatched_matches_single(n, M):
     st = mb.stats()
     rs = ref_layer.stats()
     assert st["local_tokens"] + st["remote_tokens"] == rs["local_tokens"] + rs["remote_tokens"]
+
+
+def test_forward_async_error_surfaces_in_its_own_batch():
+    """An out-of-vocabulary token in batch 1 raises in handle 1's result();
+    batches 0 and 2 (queued around it) are unaffected."""
+    over = {"G": 4, "N": 16}
+    w = synth.make_workload("toy", n=200, eps=0.2, seed=8, cfg_override=over)
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=200)
+    parts = torch.from_numpy(w.partials).to(torch.bfloat16)
+    want = layer.forward(parts, w.tokens, w.hist).float().numpy()
+    bad = w.tokens.copy()
+    bad[5] = 10 ** 6
+    pp = parts.pin_memory()
+    hh = torch.from_numpy(w.hist).pin_memory()
+    toks = [torch.from_numpy(x).pin_memory() for x in (w.tokens, bad, w.tokens)]
+    outs = [torch.empty((200, 256), dtype=torch.bfloat16).pin_memory() for _ in range(3)]
+    hs = [layer.forward_async(pp, t, hh, out=outs[i]) for i, t in enumerate(toks)]
+    assert np.array_equal(hs[0].result().float().numpy(), want)
+    with pytest.raises(IndexError):
+        hs[1].result()
+    assert np.array_equal(hs[2].result().float().numpy(), want)
