@@ -240,6 +240,27 @@ class SpecMoELayer:
                         f"layer stage {N.STAGE_NAMES[s]}")
         return self.out_view(n)
 
+    def capture(self, tokens_t, hist_t=None):
+        """Record one forward over these device tensors as a CUDA graph.
+
+        Replaying the returned `torch.cuda.CUDAGraph` re-runs the whole layer
+        (every stage, one graph launch) on whatever the bound partial buffers,
+        `tokens_t` and `hist_t` hold at replay time; the token count is fixed
+        at capture.  For small (decode-sized) batches, where the ten kernel
+        launches of `run_device` cost as much as the work."""
+        t = _dev.torch()
+        if self.group is not None:
+            raise SchedulerError("graph capture is single-process only (peer barriers spin)")
+        s = t.cuda.Stream()
+        s.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(s):                  # warm-up off the capture (lazy attributes)
+            self.run_device(tokens_t, hist_t, stream=s)
+        t.cuda.current_stream().wait_stream(s)
+        g = t.cuda.CUDAGraph()
+        with t.cuda.graph(g):
+            self.run_device(tokens_t, hist_t)
+        return g
+
     def out_view(self, n: int, shard: int | None = None):
         g = self.shard_begin if shard is None else shard
         if self.group is None:

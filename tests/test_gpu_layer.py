@@ -248,3 +248,27 @@ def test_forward_async_error_surfaces_in_its_own_batch():
     with pytest.raises(IndexError):
         hs[1].result()
     assert np.array_equal(hs[2].result().float().numpy(), want)
+
+
+def test_graph_capture_replays_the_layer():
+    """SpecMoELayer.capture: a CUDA-graph replay equals the eager forward,
+    and picks up new partials / tokens written into the captured buffers."""
+    over = {"G": 4, "N": 16}
+    wa = synth.make_workload("toy", n=128, eps=0.2, seed=21, cfg_override=over)
+    wb = synth.make_workload("toy", n=128, eps=0.2, seed=22, cfg_override=over)
+    wb.bundle, wb.gate_w, wb.w1, wb.w3, wb.w2 = wa.bundle, wa.gate_w, wa.w1, wa.w3, wa.w2
+    layer = SpecMoELayer(wa.bundle, wa.gate_w, wa.w1, wa.w3, wa.w2, top_k=2, max_tokens=128)
+    want = [layer.forward(torch.from_numpy(w.partials).to(torch.bfloat16), w.tokens,
+                          w.hist).clone() for w in (wa, wb)]
+    tok = torch.as_tensor(wa.tokens, device="cuda")
+    hist = torch.as_tensor(wa.hist, device="cuda")
+    layer.partial_views(128).copy_(torch.from_numpy(wa.partials).to(torch.bfloat16))
+    g = layer.capture(tok, hist)
+    for w, ref in ((wb, want[1]), (wa, want[0])):
+        layer.partial_views(128).copy_(torch.from_numpy(w.partials).to(torch.bfloat16))
+        tok.copy_(torch.as_tensor(w.tokens))
+        hist.copy_(torch.as_tensor(w.hist))
+        g.replay()
+        torch.cuda.synchronize()
+        layer.check_errors()
+        assert torch.equal(layer.out_view(128).cpu(), ref.cpu())
