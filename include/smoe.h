@@ -54,6 +54,8 @@ const char* smoe_version(void);
 /* Process-wide tuning switches. */
 #define SMOE_OPT_GEMM_CTA_GROUP_UP   0  /* SwiGLU GEMM: 1 = 128x256 tile per SM (default), */
 #define SMOE_OPT_GEMM_CTA_GROUP_DOWN 1  /* down GEMM: 2 = 256x256 tile per SM pair (default) */
+#define SMOE_OPT_GATE_TENSOR         2  /* layer gate: 1 = tcgen05 kernel (default), */
+                                        /* 0 = mma.sync / CUDA-core kernels          */
 int smoe_set_option(int32_t key, int32_t value);
 int smoe_get_option(int32_t key);
 const char* smoe_status_string(int status);

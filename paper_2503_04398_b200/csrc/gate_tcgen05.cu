@@ -1,0 +1,332 @@
+// gate_tcgen05.cu — K4 on the 5th-generation tensor cores: router logits,
+// softmax, top-k and the local/remote event count of every hidden row.
+//
+// The gate (semantics in DESIGN.md §2) multiplies each reduced
+// hidden row h (bf16, d) by the N gate rows.  With N = 64 (DeepSeek-V2-Lite,
+// Qwen2-MoE) the mma.sync kernel in layer_kernels.cu spends ~7x the HBM time
+// of the rows it reads; here the contraction is one tcgen05 MMA chain per
+// 128-row tile and the kernel streams h at HBM speed:
+//
+//   warp 0 lane 0  TMA producer: H tile 128 x 64 (from the resident shards'
+//                  hs arena) + W tile N' x 64 per 64-wide k-block, 2 k-blocks
+//                  per stage, 4-stage ring
+//   warp 1 lane 0  tcgen05.mma.cta_group::1.kind::f16 M128 x N' x K16 into
+//                  TMEM (fp32), two accumulators so the epilogue of tile t
+//                  overlaps the MMAs of tile t + 1
+//   warp 2         TMEM allocator
+//   warps 4..7     epilogue, ONE THREAD PER ROW: tcgen05.ld 32x32b gives the
+//                  thread its row's N' logits in registers; bias, max, softmax
+//                  sum, top-k (larger logit first, lowest expert on ties) and
+//                  the locality count need no shuffles or shared memory.
+//
+// N' = N rounded up to 16 (the MMA's N granularity at M = 128); W rows past
+// N are TMA out-of-bounds fills (zeros) and are masked to -inf.  Rows past a
+// shard's token count are computed and discarded.
+#include "common.cuh"
+#include "gemm.h"
+#include "layer_kernels.cuh"
+#include "tc_ptx.cuh"
+
+#include <algorithm>
+#include <cstdlib>
+
+namespace smoe {
+
+constexpr int kGtThreads = 256;
+constexpr int kGtRows = 128;                               // MMA M: rows per tile
+constexpr uint32_t kGtBoxBytes = kGtRows * kGemmBK * 2;   // one 128 x 64 H box: 16 KiB
+constexpr int kGtMaxK = 8;
+
+// NP = W rows (N rounded up to 16); SUB = 64-wide k-blocks per stage (one TMA
+// box each, so a stage reads SUB * 128 contiguous bytes of every hidden row);
+// ST = stages in the ring.
+template <int NP, int SUB, int ST> struct GtShape {
+  static constexpr int kStages = ST;
+  static constexpr uint32_t kHBytes = SUB * kGtBoxBytes;
+  static constexpr uint32_t kWBox = NP * kGemmBK * 2;     // NP rows of 128 B
+  static constexpr uint32_t kWBytes = SUB * kWBox;
+  static constexpr uint32_t kStageBytes = kHBytes + kWBytes;
+  static constexpr uint32_t kTmemCols = 2 * NP <= 32 ? 32 : (2 * NP <= 64 ? 64 : 128);
+  static constexpr uint32_t kAccCols = kTmemCols / 2;      // column stride of the 2 accumulators
+  static constexpr size_t kSmem = 1024 + ST * kStageBytes + 128;
+  // D f32, A/B bf16, both K-major, N = NP, M = 128
+  static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) |
+                                     (uint32_t(NP >> 3) << 17) | (uint32_t(kGtRows >> 4) << 24);
+};
+
+template <int NP, int SUB, int ST>
+__global__ void __launch_bounds__(kGtThreads, 1)
+gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
+               const __grid_constant__ CUtensorMap tmap_w, const GateTcArgs a) {
+  using S = GtShape<NP, SUB, ST>;
+  constexpr int kGtStages = S::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* smem_h = smem;
+  uint8_t* smem_w = smem + kGtStages * S::kHBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_w + kGtStages * S::kWBytes);
+  // bars: full[kGtStages], empty[kGtStages], tfull[2], tempty[2]
+  __shared__ uint32_t tmem_holder;
+  __shared__ int32_t s_cnt[SMOE_MAX_SHARDS];
+  __shared__ int32_t s_prefix[SMOE_MAX_SHARDS + 1];
+  __shared__ char* s_ids[SMOE_MAX_SHARDS];
+  __shared__ char* s_wts[SMOE_MAX_SHARDS];
+  __shared__ float s_bias[NP];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    int32_t acc = 0;
+    for (int i = 0; i < a.shard_count; ++i) {
+      const int32_t c = a.counts ? a.counts[a.shard_begin + i] : (i == 0 ? (int32_t)a.single_rows : 0);
+      s_cnt[i] = c;
+      s_prefix[i] = acc;
+      acc += (c + kGtRows - 1) / kGtRows;
+    }
+    s_prefix[a.shard_count] = acc;
+#pragma unroll
+    for (int i = 0; i < SMOE_MAX_SHARDS; ++i) {
+      s_ids[i] = a.topk_ids.p[i];
+      s_wts[i] = a.topk_w.p[i];
+    }
+  }
+  if (threadIdx.x < NP)
+    s_bias[threadIdx.x] = (a.b_gate && threadIdx.x < a.n_experts) ? a.b_gate[threadIdx.x] : 0.f;
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kGtStages; ++s) {
+      mbar_init(smem_addr(&bars[s]), 1);
+      mbar_init(smem_addr(&bars[kGtStages + s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_addr(&bars[2 * kGtStages + b]), 1);
+      mbar_init(smem_addr(&bars[2 * kGtStages + 2 + b]), 4);   // one arrival per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&tmap_h) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&tmap_w) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_addr(&tmem_holder)), "r"(S::kTmemCols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_holder;
+  const int32_t total = s_prefix[a.shard_count];
+  const uint32_t full0 = smem_addr(&bars[0]);
+  const uint32_t empty0 = smem_addr(&bars[kGtStages]);
+  const uint32_t tfull0 = smem_addr(&bars[2 * kGtStages]);
+  const uint32_t tempty0 = smem_addr(&bars[2 * kGtStages + 2]);
+
+  auto decode = [&](int32_t t, int32_t& gl, int32_t& blk) {
+    gl = 0;
+    while (gl + 1 < a.shard_count && s_prefix[gl + 1] <= t) ++gl;
+    blk = t - s_prefix[gl];
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      int32_t stage = 0;
+      uint32_t phase = 0;
+      for (int32_t t = blockIdx.x; t < total; t += gridDim.x) {
+        int32_t gl, blk;
+        decode(t, gl, blk);
+        const int32_t row = (int32_t)(gl * a.rows_per_shard + (int64_t)blk * kGtRows);
+        for (int32_t kb = 0; kb < a.num_k_blocks; kb += SUB) {
+          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          const uint32_t fb = full0 + 8 * stage;
+          mbar_expect_tx(fb, S::kStageBytes);
+#pragma unroll
+          for (int u = 0; u < SUB; ++u) {
+            tma_load_2d(smem_addr(smem_h + stage * S::kHBytes + u * kGtBoxBytes), &tmap_h, fb,
+                        (kb + u) * kGemmBK, row);
+            tma_load_2d(smem_addr(smem_w + stage * S::kWBytes + u * S::kWBox), &tmap_w, fb,
+                        (kb + u) * kGemmBK, 0);
+          }
+          if (++stage == kGtStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer =====
+      int32_t stage = 0;
+      uint32_t phase = 0, acc = 0, acc_phase = 0;
+      for (int32_t t = blockIdx.x; t < total; t += gridDim.x) {
+        mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * S::kAccCols;
+        for (int32_t kb = 0; kb < a.num_k_blocks; kb += SUB) {
+          mbar_wait(full0 + 8 * stage, phase);
+          tc_fence_after();
+#pragma unroll
+          for (int u = 0; u < SUB; ++u) {
+            const uint64_t hd = sdesc(smem_addr(smem_h + stage * S::kHBytes + u * kGtBoxBytes));
+            const uint64_t wd = sdesc(smem_addr(smem_w + stage * S::kWBytes + u * S::kWBox));
+#pragma unroll
+            for (int k = 0; k < kGemmBK / 16; ++k)
+              tc_mma(d_tmem, hd + 2 * k, wd + 2 * k, S::kIdesc, (kb | u | k) != 0);
+          }
+          tc_commit(empty0 + 8 * stage);
+          if (++stage == kGtStages) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(tfull0 + 8 * acc);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue: thread = row =====
+    const int ew = warp - 4;
+    const int N = a.n_experts, K = a.k;
+    uint32_t acc = 0, acc_phase = 0;
+    unsigned long long my_local = 0, my_remote = 0;
+    for (int32_t t = blockIdx.x; t < total; t += gridDim.x) {
+      int32_t gl, blk;
+      decode(t, gl, blk);
+      mbar_wait(tfull0 + 8 * acc, acc_phase);
+      tc_fence_after();
+      uint32_t v[NP];
+      const uint32_t taddr = tmem_base + acc * S::kAccCols + ((uint32_t)(ew * 32) << 16);
+#pragma unroll
+      for (int c = 0; c < NP / 16; ++c) SMOE_TMEM_LD16(taddr + c * 16, (v + c * 16));
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty0 + 8 * acc);     // accumulator free for tile t + 2
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+
+      const int64_t j = (int64_t)blk * kGtRows + ew * 32 + lane;
+      if (j >= s_cnt[gl]) continue;
+      float lg[NP];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < NP; ++e) {
+        lg[e] = e < N ? __uint_as_float(v[e]) + s_bias[e] : -INFINITY;
+        mx = fmaxf(mx, lg[e]);
+      }
+      float ex = 0.f;
+#pragma unroll
+      for (int e = 0; e < NP; ++e) ex += e < N ? __expf(lg[e] - mx) : 0.f;
+      const float inv = 1.0f / ex;
+      int sel_e[kGtMaxK];
+      float sel_p[kGtMaxK];
+      float psum = 0.f;
+#pragma unroll
+      for (int s = 0; s < kGtMaxK; ++s) {
+        sel_e[s] = 0;
+        sel_p[s] = 0.f;
+        if (s < K) {
+          float bv = -INFINITY;
+          int bi = 0;
+#pragma unroll
+          for (int e = 0; e < NP; ++e)
+            if (lg[e] > bv) { bv = lg[e]; bi = e; }      // strict: lowest expert on ties
+#pragma unroll
+          for (int e = 0; e < NP; ++e)
+            if (e == bi) lg[e] = -INFINITY;
+          sel_e[s] = bi;
+          sel_p[s] = __expf(bv - mx) * inv;
+          psum += sel_p[s];
+        }
+      }
+      const int32_t g = a.shard_begin + gl;
+      int32_t* ids = reinterpret_cast<int32_t*>(s_ids[gl]) + j * K;
+      float* wts = reinterpret_cast<float*>(s_wts[gl]) + j * K;
+#pragma unroll
+      for (int s = 0; s < kGtMaxK; ++s) {
+        if (s < K) {
+          ids[s] = sel_e[s];
+          wts[s] = a.renorm ? sel_p[s] / psum : sel_p[s];
+          if (a.slot_owner[sel_e[s]] == g) ++my_local; else ++my_remote;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      my_local += __shfl_xor_sync(0xffffffffu, my_local, o);
+      my_remote += __shfl_xor_sync(0xffffffffu, my_remote, o);
+    }
+    if (lane == 0 && a.stats && (my_local | my_remote)) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + SMOE_STAT_LOCAL_PAIRS), my_local);
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + SMOE_STAT_REMOTE_PAIRS),
+                my_remote);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
+                 :: "r"(tmem_base), "r"(S::kTmemCols) : "memory");
+  }
+}
+
+template <int NP, int SUB, int ST>
+static int launch_cfg(const CUtensorMap& mh, const CUtensorMap& mw, const GateTcArgs& a,
+                      int64_t n_rows_bound, cudaStream_t st) {
+  using S = GtShape<NP, SUB, ST>;
+  static bool attr = false;
+  if (!attr) {
+    SMOE_CUDA_TRY(cudaFuncSetAttribute(gate_tc_kernel<NP, SUB, ST>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::kSmem));
+    attr = true;
+  }
+  const int64_t tiles = ceil_div(n_rows_bound, kGtRows) + a.shard_count;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms()));
+  gate_tc_kernel<NP, SUB, ST><<<grid, kGtThreads, S::kSmem, st>>>(mh, mw, a);
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
+// Ring shape (SMOE_GATE_RING=<k-blocks per stage>x<stages>, tuning only):
+// 1x8, 2x4 (default) or 4x2.
+static int ring_sub() {
+  static int sub = [] {
+    const char* e = getenv("SMOE_GATE_RING");
+    const int v = e ? atoi(e) : 2;
+    return (v == 1 || v == 2 || v == 4) ? v : 2;
+  }();
+  return sub;
+}
+
+template <int NP>
+static int launch_np(const CUtensorMap& mh, const CUtensorMap& mw, const GateTcArgs& a,
+                     int64_t n_rows_bound, cudaStream_t st) {
+  switch (ring_sub()) {
+    case 1: return launch_cfg<NP, 1, 8>(mh, mw, a, n_rows_bound, st);
+    case 4: return launch_cfg<NP, 4, 2>(mh, mw, a, n_rows_bound, st);
+    default: return launch_cfg<NP, 2, 4>(mh, mw, a, n_rows_bound, st);
+  }
+}
+
+static int g_gate_tc = 1;
+int gate_tc_enabled() { return g_gate_tc; }
+void set_gate_tc_enabled(int on) { g_gate_tc = on ? 1 : 0; }
+
+int gate_tc_rows(int32_t n_experts) { return std::max(16, (n_experts + 15) / 16 * 16); }
+
+bool gate_tc_supported(int32_t n_experts, int32_t top_k, int64_t d) {
+  return n_experts >= 1 && n_experts <= 64 && top_k >= 1 && top_k <= kGtMaxK &&
+         top_k <= n_experts && d % (4 * kGemmBK) == 0;
+}
+
+int launch_gate_tc(const CUtensorMap& map_h, const CUtensorMap& map_w, const GateTcArgs& a,
+                   int64_t n_rows_bound, cudaStream_t st) {
+  if (n_rows_bound <= 0) return SMOE_OK;
+  switch (gate_tc_rows(a.n_experts)) {
+    case 16: return launch_np<16>(map_h, map_w, a, n_rows_bound, st);
+    case 32: return launch_np<32>(map_h, map_w, a, n_rows_bound, st);
+    case 48: return launch_np<48>(map_h, map_w, a, n_rows_bound, st);
+    case 64: return launch_np<64>(map_h, map_w, a, n_rows_bound, st);
+    default: return SMOE_ERR_UNSUPPORTED;
+  }
+}
+
+}  // namespace smoe

@@ -39,6 +39,9 @@ struct smoe_layer {
   bool maps_ready = false;
   int maps_cg_up = 0, maps_cg_down = 0;
   CUtensorMap map_x, map_w13, map_h, map_w2;
+  // tensor-core gate: hidden rows of the resident shards (one arena) and W_g
+  bool gate_tc = false;
+  CUtensorMap map_hs, map_wg;
 };
 
 static bool valid_cfg(const smoe_layer_config* c) {
@@ -213,6 +216,19 @@ static int ensure_maps(smoe_layer* L) {
   if ((rc = make_tmap_bf16(&L->map_w2, L->w2, nl * c.hidden, c.ffn,
                            gemm_b_box_rows(gemm_cta_group(1)))))
     return rc;
+  // the tcgen05 gate needs the resident shards' hs buffers as one arena
+  const int64_t hs_stride = c.max_tokens * (int64_t)c.hidden * 2;
+  bool arena = gate_tc_supported(c.n_experts, c.top_k, c.hidden);
+  for (int i = 1; i < c.shard_count && arena; ++i)
+    arena = static_cast<char*>(L->buf[SMOE_BUF_HS][i]) ==
+            static_cast<char*>(L->buf[SMOE_BUF_HS][0]) + i * hs_stride;
+  L->gate_tc = false;
+  if (arena &&
+      make_tmap_bf16(&L->map_hs, L->buf[SMOE_BUF_HS][0], c.shard_count * (int64_t)c.max_tokens,
+                     c.hidden, 128) == SMOE_OK &&
+      make_tmap_bf16(&L->map_wg, L->w_gate, c.n_experts, c.hidden,
+                     gate_tc_rows(c.n_experts)) == SMOE_OK)
+    L->gate_tc = true;
   L->maps_ready = true;
   L->maps_cg_up = gemm_cta_group(0);
   L->maps_cg_down = gemm_cta_group(1);
@@ -272,6 +288,23 @@ extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tok
       return launch_srs(lr, peer_ptrs(L, SMOE_BUF_PARTIAL), c.hidden, local_ptrs(L, SMOE_BUF_HS),
                         n, st);
     case SMOE_STAGE_GATE:
+      if (L->gate_tc && gate_tc_enabled()) {
+        GateTcArgs g{};
+        g.counts = lr.counts;
+        g.shard_begin = c.shard_begin;
+        g.shard_count = c.shard_count;
+        g.rows_per_shard = c.max_tokens;
+        g.num_k_blocks = c.hidden / kGemmBK;
+        g.n_experts = c.n_experts;
+        g.k = c.top_k;
+        g.renorm = c.renormalize;
+        g.b_gate = L->b_gate;
+        g.slot_owner = L->slot_owner_d;
+        g.topk_ids = local_ptrs(L, SMOE_BUF_TOPK_IDS);
+        g.topk_w = local_ptrs(L, SMOE_BUF_TOPK_W);
+        g.stats = stats;
+        return launch_gate_tc(L->map_hs, L->map_wg, g, n, st);
+      }
       return launch_gate(lr, local_ptrs(L, SMOE_BUF_HS), c.hidden, L->w_gate, L->b_gate,
                          c.n_experts, c.top_k, c.renormalize, L->slot_owner_d,
                          local_ptrs(L, SMOE_BUF_TOPK_IDS), local_ptrs(L, SMOE_BUF_TOPK_W), stats,
@@ -400,6 +433,10 @@ extern "C" int smoe_set_option(int32_t key, int32_t value) {
       if (value != 1 && value != 2) return SMOE_ERR_INVALID_ARG;
       set_gemm_cta_group(key == SMOE_OPT_GEMM_CTA_GROUP_DOWN, value);
       return SMOE_OK;
+    case SMOE_OPT_GATE_TENSOR:
+      if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
+      set_gate_tc_enabled(value);
+      return SMOE_OK;
     default:
       return SMOE_ERR_INVALID_ARG;
   }
@@ -408,5 +445,6 @@ extern "C" int smoe_set_option(int32_t key, int32_t value) {
 extern "C" int smoe_get_option(int32_t key) {
   if (key == SMOE_OPT_GEMM_CTA_GROUP_UP) return gemm_cta_group(0);
   if (key == SMOE_OPT_GEMM_CTA_GROUP_DOWN) return gemm_cta_group(1);
+  if (key == SMOE_OPT_GATE_TENSOR) return gate_tc_enabled();
   return -1;
 }

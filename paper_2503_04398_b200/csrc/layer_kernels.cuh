@@ -1,5 +1,6 @@
 // layer_kernels.cuh — launch interface of the layer stages (K3, K4, K5, K8).
 #pragma once
+#include <cuda.h>
 #include "common.cuh"
 
 namespace smoe {
@@ -25,6 +26,27 @@ int launch_gate(const LocalRows& lr, const ShardPtrs& hs, int64_t d, const void*
                 const float* b_gate, int32_t N, int32_t k, int32_t renorm,
                 const int32_t* slot_owner, const ShardPtrs& topk_ids, const ShardPtrs& topk_w,
                 int64_t* stats, int64_t n_rows_bound, cudaStream_t st);
+
+// K4 on tcgen05 (gate_tcgen05.cu): the hidden rows of the resident shards
+// come from ONE arena (shard i at row i * rows_per_shard) through a TMA map.
+struct GateTcArgs {
+  const int32_t* counts;     // [G] plan counts (nullptr: single_rows rows in shard 0)
+  int64_t single_rows;
+  int32_t shard_begin, shard_count;
+  int64_t rows_per_shard;    // arena row stride between resident shards
+  int32_t num_k_blocks;      // d / 64
+  int32_t n_experts, k, renorm;
+  const float* b_gate;
+  const int32_t* slot_owner;
+  ShardPtrs topk_ids, topk_w;
+  int64_t* stats;
+};
+bool gate_tc_supported(int32_t n_experts, int32_t top_k, int64_t d);
+int gate_tc_enabled();                 // SMOE_OPT_GATE_TENSOR
+void set_gate_tc_enabled(int on);
+int gate_tc_rows(int32_t n_experts);   // W box rows (N rounded up to 16)
+int launch_gate_tc(const CUtensorMap& map_h, const CUtensorMap& map_w, const GateTcArgs& a,
+                   int64_t n_rows_bound, cudaStream_t st);
 
 size_t route_workspace_bytes(int64_t max_tokens, int32_t k, int32_t N, int32_t shard_count);
 int launch_route(const LocalRows& lr, int32_t N, int32_t k, const ShardPtrs& topk_ids,

@@ -33,13 +33,25 @@ CASES = [
     ("toy", 500, 0.1, {"G": 4, "N": 64, "k": 8, "d": 256, "f": 384}),
     ("toy", 300, 0.1, {"G": 1, "N": 8, "k": 2}),
     ("toy", 512, 0.2, {"G": 8, "N": 8, "k": 1, "d": 4096, "f": 512}),
-    ("toy", 333, 0.2, {"G": 4, "N": 24, "k": 3}),          # CUDA-core gate path (N % 8 != 0 tiles)
+    ("toy", 333, 0.2, {"G": 4, "N": 24, "k": 3}),          # N' = 32 (tcgen05) / CUDA-core gate
     ("toy", 2000, 0.4, {"G": 8, "N": 32, "k": 4, "d": 1024, "f": 256}),
 ]
 
 
+@pytest.fixture(params=[1, 0], ids=["gate_tcgen05", "gate_mma_sync"])
+def gate_kernel(request):
+    """Run a test with the tcgen05 gate (default) and with the mma.sync /
+    CUDA-core gate kernels (SMOE_OPT_GATE_TENSOR = 0)."""
+    from paper_2503_04398_b200 import _native as N
+    lib = N.lib()
+    old = lib.smoe_get_option(N.OPT_GATE_TENSOR)
+    N.check(lib.smoe_set_option(N.OPT_GATE_TENSOR, request.param), "set_option")
+    yield request.param
+    N.check(lib.smoe_set_option(N.OPT_GATE_TENSOR, old), "set_option")
+
+
 @pytest.mark.parametrize("name,n,eps,over", CASES)
-def test_layer_matches_oracle(name, n, eps, over):
+def test_layer_matches_oracle(name, n, eps, over, gate_kernel):
     w = synth.make_workload(name, n=n, eps=eps, seed=n, cfg_override=over)
     G = w.cfg["G"]
     layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=w.cfg["k"],
@@ -272,3 +284,30 @@ def test_graph_capture_replays_the_layer():
         torch.cuda.synchronize()
         layer.check_errors()
         assert torch.equal(layer.out_view(128).cpu(), ref.cpu())
+
+
+@pytest.mark.parametrize("over", [{"G": 8, "N": 64, "k": 6, "d": 2048, "f": 256},
+                                  {"G": 8, "N": 64, "k": 8, "d": 3584, "f": 256},
+                                  {"G": 8, "N": 8, "k": 2, "d": 4096, "f": 256},
+                                  {"G": 4, "N": 40, "k": 5, "d": 512, "f": 256}])
+def test_tcgen05_gate_matches_mma_gate(over):
+    """Both gate kernels on the same layer: identical top-k ids and event
+    counts, weights within fp32 accumulation-order noise (model-sized d)."""
+    from paper_2503_04398_b200 import _native as N
+    lib = N.lib()
+    n = 3000
+    w = synth.make_workload("toy", n=n, eps=0.3, seed=77, cfg_override=over)
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=over["k"], max_tokens=n)
+    parts = torch.from_numpy(w.partials).to(torch.bfloat16)
+    res = {}
+    try:
+        for opt in (1, 0):
+            N.check(lib.smoe_set_option(N.OPT_GATE_TENSOR, opt), "set_option")
+            layer.forward(parts, w.tokens, w.hist)
+            res[opt] = (layer.routing(n), layer.stats())
+    finally:
+        N.check(lib.smoe_set_option(N.OPT_GATE_TENSOR, 1), "set_option")
+    (ra, sa), (rb, sb) = res[1], res[0]
+    assert np.array_equal(ra["experts"], rb["experts"])
+    assert np.allclose(ra["weights"], rb["weights"], rtol=1e-4, atol=1e-6)
+    assert (sa["local_tokens"], sa["remote_tokens"]) == (sb["local_tokens"], sb["remote_tokens"])

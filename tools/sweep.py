@@ -96,7 +96,24 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--microbatch-ab", action="store_true",
                     help="interleaved 1 vs 2 vs 4 micro-batches on the main configs")
+    ap.add_argument("--gate-ab", action="store_true",
+                    help="interleaved tcgen05 gate vs mma.sync gate (SMOE_OPT_GATE_TENSOR)")
     args = ap.parse_args()
+    if args.gate_ab:
+        from paper_2503_04398_b200 import _native as N
+        lib = N.lib()
+        for rep in range(2):
+            for name, tok, ep in (("mixtral", 16384, None), ("dsv2_lite", 16384, None),
+                                  ("dsv2_lite", 65536, None), ("qwen2_57b", 65536, 8)):
+                for opt in (1, 0):
+                    N.check(lib.smoe_set_option(N.OPT_GATE_TENSOR, opt), "opt")
+                    r = measure(name, tok, 0.2, ep)
+                    print(json.dumps({k: r[k] for k in ("config", "tokens", "ms_per_step",
+                                                        "tokens_per_s", "alpha")} |
+                                     {"gate_ms": r["stage_ms"]["gate"], "gate_tensor": opt,
+                                      "rep": rep}), flush=True)
+        N.check(lib.smoe_set_option(N.OPT_GATE_TENSOR, 1), "opt")
+        return
     if args.microbatch_ab:
         for rep in range(2):
             for name, tok in (("mixtral", 16384), ("dsv2_lite", 16384), ("qwen2_57b", 16384),
