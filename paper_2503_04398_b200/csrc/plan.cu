@@ -5,7 +5,7 @@
 // stable argsort plus a Python loop over devices; with G <= 1024 labels a
 // stable partition is a counting sort:
 //
-//   pass 1 (plan_count):   per 2048-token tile, look the device up and count
+//   pass 1 (plan_count):   per 512-token tile, look the device up and count
 //                          tokens per device (warp match_any aggregation).
 //   pass 2 (plan_scatter): prefix the tile counts per device, take the global
 //                          max group (scheduler.py:135), and give every token
@@ -21,8 +21,8 @@
 namespace smoe {
 
 constexpr int kPlanThreads = 256;
-constexpr int kPlanChunks = 8;
-constexpr int kPlanTile = kPlanThreads * kPlanChunks;   // 2048 tokens per CTA
+constexpr int kPlanChunks = 2;
+constexpr int kPlanTile = kPlanThreads * kPlanChunks;   // 512 tokens per CTA
 
 struct LookupTables {
   const int16_t* t_labels;
