@@ -99,7 +99,8 @@ def load(path: str | os.PathLike | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else _LIB_PATH
+    # SMOE_LIB: an alternative in-tree build (A/B experiments between builds)
+    p = Path(path) if path else Path(os.environ.get("SMOE_LIB", _LIB_PATH))
     if not p.exists():
         raise ImportError(f"{p} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
     handle = C.CDLL(str(p))

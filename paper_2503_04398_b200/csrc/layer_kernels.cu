@@ -22,6 +22,7 @@
 //                          to the token's original position (resume fused)
 #include "layer_kernels.cuh"
 #include <algorithm>
+#include <cstdlib>
 
 namespace smoe {
 
@@ -74,11 +75,56 @@ __device__ __forceinline__ void decode_row(const RowMap& rm, int32_t shard_count
 }
 
 // ------------------------------------------------------------------ K3 SRS
-// One warp per output row; G is a template parameter so the 2*G 16-B loads
-// of an iteration (two vectors per lane) are all in flight before the sum.
+// One warp per work item, two 16-B vectors per lane per shard per step, so
+// the 2*G loads of a step are all in flight before the sum (G is a template
+// parameter).  An item is a whole output row when there are at least as many
+// rows as resident warps (kWholeRows), else a 1 KiB column chunk of a row: decode-sized batches
+// (64 rows x 8 chunks = 512 items) then keep every warp busy instead of 64
+// warps walking their rows serially.
+constexpr int64_t kChunkVecs = 64;           // 16-B vectors per chunk item (1 KiB)
+constexpr int32_t kWholeRows = 2048;         // rows from which an item is a whole row
+                                             // (~ the warps resident on 148 SMs)
+static int32_t whole_rows_from() {           // SMOE_WHOLE_ROWS: tuning experiments only
+  static int32_t v = [] {
+    const char* e = getenv("SMOE_WHOLE_ROWS");
+    return e ? (int32_t)atoi(e) : kWholeRows;
+  }();
+  return v;
+}
+static int grid_items(int64_t rows, int64_t d) {
+  return grid_cap(ceil_div(rows >= whole_rows_from() ? rows : rows * ceil_div(d / 8, kChunkVecs), 8), 16);
+}
+
+// Sum of row `row_off` over the G partials for vectors [v0, v1), written to
+// `out` (two 16-B vectors per lane per shard in flight per step).
+template <int G>
+__device__ __forceinline__ void srs_span(const char* const (&src_base)[G], int64_t row_off,
+                                         char* out, int64_t v0, int64_t v1, int lane) {
+  for (int64_t v = v0 + lane; v < v1; v += 64) {
+    const bool two = v + 32 < v1;
+    uint4 x[G], y[G];
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+      x[r] = ld_nc_v4(src_base[r] + row_off + v * 16);
+      if (two) y[r] = ld_nc_v4(src_base[r] + row_off + (v + 32) * 16);
+    }
+    float a[8], b[8];
+    set_bf16x8(a, x[0]);
+#pragma unroll
+    for (int r = 1; r < G; ++r) acc_bf16x8(a, x[r]);
+    st_v4(out + v * 16, pack_bf16x8(a));
+    if (two) {
+      set_bf16x8(b, y[0]);
+#pragma unroll
+      for (int r = 1; r < G; ++r) acc_bf16x8(b, y[r]);
+      st_v4(out + (v + 32) * 16, pack_bf16x8(b));
+    }
+  }
+}
+
 template <int G>
 __global__ void __launch_bounds__(256)
-srs_kernel(LocalRows lr, ShardPtrs partials, int64_t d, ShardPtrs hs) {
+srs_kernel(LocalRows lr, ShardPtrs partials, int64_t d, ShardPtrs hs, int32_t whole_rows) {
   __shared__ RowMap rm;
   __shared__ char* s_hs[SMOE_MAX_SHARDS];
   stage_ptrs(s_hs, hs);
@@ -86,35 +132,27 @@ srs_kernel(LocalRows lr, ShardPtrs partials, int64_t d, ShardPtrs hs) {
   const int lane = threadIdx.x & 31;
   const int64_t vecs = d / 8;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t w0 = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const char* src_base[G];
 #pragma unroll
   for (int r = 0; r < G; ++r) src_base[r] = partials.p[r];
-  for (int64_t q = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); q < rm.total;
-       q += nwarps) {
-    int32_t gl; int64_t j;
-    decode_row(rm, lr.shard_count, q, gl, j);
-    const int64_t g = lr.shard_begin + gl;
-    const int64_t row_off = lr.forward[g * rm.group + j] * d * 2;
-    char* out = s_hs[gl] + j * d * 2;
-    for (int64_t v = lane; v < vecs; v += 64) {
-      const bool two = v + 32 < vecs;
-      uint4 x[G], y[G];
-#pragma unroll
-      for (int r = 0; r < G; ++r) {
-        x[r] = ld_nc_v4(src_base[r] + row_off + v * 16);
-        if (two) y[r] = ld_nc_v4(src_base[r] + row_off + (v + 32) * 16);
-      }
-      float a[8], b[8];
-      set_bf16x8(a, x[0]);
-#pragma unroll
-      for (int r = 1; r < G; ++r) acc_bf16x8(a, x[r]);
-      st_v4(out + v * 16, pack_bf16x8(a));
-      if (two) {
-        set_bf16x8(b, y[0]);
-#pragma unroll
-        for (int r = 1; r < G; ++r) acc_bf16x8(b, y[r]);
-        st_v4(out + (v + 32) * 16, pack_bf16x8(b));
-      }
+  if (rm.total >= whole_rows) {
+    for (int64_t q = w0; q < rm.total; q += nwarps) {            // warp = row
+      int32_t gl; int64_t j;
+      decode_row(rm, lr.shard_count, q, gl, j);
+      const int64_t g = lr.shard_begin + gl;
+      srs_span<G>(src_base, lr.forward[g * rm.group + j] * d * 2, s_hs[gl] + j * d * 2, 0,
+                  vecs, lane);
+    }
+  } else {
+    const int64_t chunks = (vecs + kChunkVecs - 1) / kChunkVecs;
+    for (int64_t it = w0; it < (int64_t)rm.total * chunks; it += nwarps) {  // warp = 1 KiB chunk
+      const int64_t q = it / chunks, c = it - q * chunks;
+      int32_t gl; int64_t j;
+      decode_row(rm, lr.shard_count, q, gl, j);
+      const int64_t g = lr.shard_begin + gl;
+      srs_span<G>(src_base, lr.forward[g * rm.group + j] * d * 2, s_hs[gl] + j * d * 2,
+                  c * kChunkVecs, min(vecs, (c + 1) * kChunkVecs), lane);
     }
   }
 }
@@ -123,10 +161,11 @@ int launch_srs(const LocalRows& lr, const ShardPtrs& partials, int64_t d, const 
                int64_t n_rows_bound, cudaStream_t st) {
   if (d % 8) return SMOE_ERR_UNSUPPORTED;
   if (n_rows_bound <= 0) return SMOE_OK;
-  const int grid = grid_cap(ceil_div(n_rows_bound, 8), 16);
+  const int grid = grid_items(n_rows_bound, d);
+  const int32_t wr = whole_rows_from();
   switch (lr.n_shards) {
 #define SMOE_SRS_CASE(G_) \
-    case G_: srs_kernel<G_><<<grid, 256, 0, st>>>(lr, partials, d, hs); break;
+    case G_: srs_kernel<G_><<<grid, 256, 0, st>>>(lr, partials, d, hs, wr); break;
     SMOE_SRS_CASE(1) SMOE_SRS_CASE(2) SMOE_SRS_CASE(3) SMOE_SRS_CASE(4) SMOE_SRS_CASE(5)
     SMOE_SRS_CASE(6) SMOE_SRS_CASE(7) SMOE_SRS_CASE(8) SMOE_SRS_CASE(9) SMOE_SRS_CASE(10)
     SMOE_SRS_CASE(11) SMOE_SRS_CASE(12) SMOE_SRS_CASE(13) SMOE_SRS_CASE(14) SMOE_SRS_CASE(15)
@@ -754,10 +793,39 @@ int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
 }
 
 // ------------------------------------------------------------------ K8 combine + SAG
+// Weighted sum of the k expert outputs of one row for vectors [v0, v1), stored
+// to the token's original position in every shard's output (the SAG).
+template <int G>
+__device__ __forceinline__ void combine_span(char* const (&dst_base)[G], const char* y,
+                                             const float (&wk)[kGateMaxK], int32_t k, int64_t d,
+                                             int64_t i, int64_t v0, int64_t v1, int lane) {
+  for (int64_t v = v0 + lane; v < v1; v += 32) {
+    uint4 yv[kGateMaxK];
+#pragma unroll
+    for (int s = 0; s < kGateMaxK; ++s)
+      if (s < k) yv[s] = ld_nc_v4(y + ((int64_t)s * d + v * 8) * 2);
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int s = 0; s < kGateMaxK; ++s) {
+      if (s < k) {
+        float t[8];
+        set_bf16x8(t, yv[s]);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) a[c] += wk[s] * t[c];
+      }
+    }
+    const uint4 o = pack_bf16x8(a);
+#pragma unroll
+    for (int r = 0; r < G; ++r) st_v4(dst_base[r] + (i * d + v * 8) * 2, o);
+  }
+}
+
+// Work items: whole rows, or 1 KiB column chunks for small batches (as in the
+// SRS); the first chunk of a row also writes the next layer's history window.
 template <int G>
 __global__ void __launch_bounds__(256)
 combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtrs topk_w,
-                   ShardPtrs outs, HistUpdate hu) {
+                   ShardPtrs outs, HistUpdate hu, int32_t whole_rows) {
   __shared__ RowMap rm;
   __shared__ char* s_y[SMOE_MAX_SHARDS];
   __shared__ char* s_wts[SMOE_MAX_SHARDS];
@@ -771,16 +839,21 @@ combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtr
   const int lane = threadIdx.x & 31;
   const int64_t vecs = d / 8;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t w0 = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   char* dst_base[G];
 #pragma unroll
   for (int r = 0; r < G; ++r) dst_base[r] = outs.p[r];
-  for (int64_t q = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); q < rm.total;
-       q += nwarps) {
+  const bool whole = rm.total >= whole_rows;
+  const int64_t chunks = whole ? 1 : (vecs + kChunkVecs - 1) / kChunkVecs;
+  const int64_t cv = whole ? vecs : kChunkVecs;
+  for (int64_t it = w0; it < (int64_t)rm.total * chunks; it += nwarps) {
+    const int64_t q = whole ? it : it / chunks;
+    const int64_t c = it - q * chunks;
     int32_t gl; int64_t j;
     decode_row(rm, lr.shard_count, q, gl, j);
     const int64_t g = lr.shard_begin + gl;
     const int64_t i = lr.forward[g * rm.group + j];    // original token position
-    if (hu.n_hist_outs > 0 && lane < hu.hist_len) {
+    if (c == 0 && hu.n_hist_outs > 0 && lane < hu.hist_len) {
       // next layer's window: drop the oldest digit, append the cluster of the
       // top-1 expert (the device of this routing event, predictor.py:165-166)
       const int64_t L = hu.hist_len;
@@ -798,26 +871,8 @@ combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtr
     float wk[kGateMaxK];
 #pragma unroll
     for (int s = 0; s < kGateMaxK; ++s) wk[s] = s < k ? w[s] : 0.f;
-    const char* y = s_y[gl] + j * k * d * 2;
-    for (int64_t v = lane; v < vecs; v += 32) {
-      uint4 yv[kGateMaxK];
-#pragma unroll
-      for (int s = 0; s < kGateMaxK; ++s)
-        if (s < k) yv[s] = ld_nc_v4(y + ((int64_t)s * d + v * 8) * 2);
-      float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int s = 0; s < kGateMaxK; ++s) {
-        if (s < k) {
-          float t[8];
-          set_bf16x8(t, yv[s]);
-#pragma unroll
-          for (int c = 0; c < 8; ++c) a[c] += wk[s] * t[c];
-        }
-      }
-      const uint4 o = pack_bf16x8(a);
-#pragma unroll
-      for (int r = 0; r < G; ++r) st_v4(dst_base[r] + (i * d + v * 8) * 2, o);
-    }
+    combine_span<G>(dst_base, s_y[gl] + j * k * d * 2, wk, k, d, i, c * cv,
+                    min(vecs, (c + 1) * cv), lane);
   }
 }
 
@@ -826,10 +881,11 @@ int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtr
                        int64_t n_rows_bound, cudaStream_t st) {
   if (k > kGateMaxK || d % 8) return SMOE_ERR_UNSUPPORTED;
   if (n_rows_bound <= 0) return SMOE_OK;
-  const int grid = grid_cap(ceil_div(n_rows_bound, 8), 16);
+  const int grid = grid_items(n_rows_bound, d);
+  const int32_t wr = whole_rows_from();
   switch (lr.n_shards) {
 #define SMOE_CMB_CASE(G_) \
-    case G_: combine_sag_kernel<G_><<<grid, 256, 0, st>>>(lr, k, d, ypair, topk_w, outs, hu); break;
+    case G_: combine_sag_kernel<G_><<<grid, 256, 0, st>>>(lr, k, d, ypair, topk_w, outs, hu, wr); break;
     SMOE_CMB_CASE(1) SMOE_CMB_CASE(2) SMOE_CMB_CASE(3) SMOE_CMB_CASE(4) SMOE_CMB_CASE(5)
     SMOE_CMB_CASE(6) SMOE_CMB_CASE(7) SMOE_CMB_CASE(8) SMOE_CMB_CASE(9) SMOE_CMB_CASE(10)
     SMOE_CMB_CASE(11) SMOE_CMB_CASE(12) SMOE_CMB_CASE(13) SMOE_CMB_CASE(14) SMOE_CMB_CASE(15)

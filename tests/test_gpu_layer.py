@@ -35,6 +35,7 @@ CASES = [
     ("toy", 512, 0.2, {"G": 8, "N": 8, "k": 1, "d": 4096, "f": 512}),
     ("toy", 333, 0.2, {"G": 4, "N": 24, "k": 3}),          # N' = 32 (tcgen05) / CUDA-core gate
     ("toy", 2000, 0.4, {"G": 8, "N": 32, "k": 4, "d": 1024, "f": 256}),
+    ("toy", 4100, 0.2, {"G": 4, "N": 16, "k": 2, "d": 512, "f": 256}),   # whole-row movers (>= 2048 rows)
 ]
 
 
