@@ -312,3 +312,29 @@ def test_tcgen05_gate_matches_mma_gate(over):
     assert np.array_equal(ra["experts"], rb["experts"])
     assert np.allclose(ra["weights"], rb["weights"], rtol=1e-4, atol=1e-6)
     assert (sa["local_tokens"], sa["remote_tokens"]) == (sb["local_tokens"], sb["remote_tokens"])
+
+
+def test_layer_all_tokens_on_one_shard_of_sixteen():
+    """G = 16 shards, every token looked up to shard 3: fifteen empty groups
+    (count 0), one full group; plan, routing, counts and output vs the oracle."""
+    from paper_2503_04398_b200.predictor import TokenDeviceTable
+    from paper_2503_04398_b200.scheduler import LookupBundle
+    over = {"G": 16, "N": 64, "k": 4, "d": 256, "f": 256}
+    n = 500
+    w = synth.make_workload("toy", n=n, eps=0.3, seed=9, cfg_override=over)
+    tt = w.bundle.token_table
+    w.bundle = LookupBundle(
+        token_table=TokenDeviceTable(labels=np.full_like(tt.labels, 3),
+                                     confidence=np.full_like(tt.confidence, 2.0),
+                                     provenance=tt.provenance, n_clusters=16),
+        ngram_table=w.bundle.ngram_table, expert_labels=w.bundle.expert_labels, layers=1)
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=4, max_tokens=n)
+    out = layer.forward(torch.from_numpy(w.partials), w.tokens, w.hist).float().numpy()
+    ref = oracle_for(w)
+    counts = layer.plan_counts.cpu().numpy()
+    assert counts[3] == n and counts.sum() == n
+    assert np.array_equal(layer.plan_indices(n).forward, ref["forward"])
+    assert np.array_equal(layer.routing(n)["experts"], ref["experts"])
+    st = layer.stats()
+    assert st["local_tokens"] == ref["local"] and st["remote_tokens"] == ref["remote"]
+    assert np.linalg.norm(out - ref["out"]) / np.linalg.norm(ref["out"]) <= TOL
