@@ -23,10 +23,15 @@ def main():
     from paper_2503_04398_b200 import SpecMoELayer, _native as N, synth
     ap = argparse.ArgumentParser()
     ap.add_argument("--stages", default="gate")
+    ap.add_argument("--tokens", type=int, default=0, help="override every config's token count")
     args = ap.parse_args()
     knobs = {k: v for k, v in os.environ.items() if k.startswith("SMOE_")}
     for name, n, ep in (("mixtral", 16384, None), ("dsv2_lite", 16384, None),
                         ("dsv2_lite", 65536, None), ("qwen2_57b", 65536, 8)):
+        if args.tokens:
+            if n == 65536 and name == "dsv2_lite":
+                continue
+            n = args.tokens
         over = {"G": ep} if ep else None
         w = synth.make_workload(name, n=n, eps=0.2, seed=0, device=True, cfg_override=over)
         layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=w.cfg["k"],
