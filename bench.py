@@ -440,8 +440,8 @@ def main():
                          f"(lookup, plan, SRS over {G} partials, fp32 gate, SwiGLU, combine)"}
 
     # plan 2 + srs 1 + gate 1 + route 2 + dispatch 1 + expert GEMMs 2 + combine/SAG 1
-    # (+ 4 signal-pad barriers when shards span processes)
-    launches_per_step = 2 + 1 + 1 + 2 + 1 + 2 + 1 + (4 if world > 1 else 0)
+    # (+ 5 signal-pad barriers when shards span processes)
+    launches_per_step = 2 + 1 + 1 + 2 + 1 + 2 + 1 + (5 if world > 1 else 0)
     traffic = None
     tf = ROOT / "profiles" / "r1_traffic.json"
     if tf.exists():

@@ -4,7 +4,8 @@
 // small device-side placement tables, and sequences the stages of Algorithm 2
 // on one stream.  With world_size > 1 a cross-process
 // barrier over NVLink-mapped signal pads separates the stages whose inputs are
-// written by other processes (after ROUTE, DISPATCH, EXPERT_DOWN, COMBINE_SAG).
+// written by other processes (before SRS; after ROUTE, DISPATCH, EXPERT_DOWN,
+// COMBINE_SAG).
 #include "common.cuh"
 #include "gemm.h"
 #include "layer_kernels.cuh"
@@ -285,6 +286,10 @@ extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tok
                               L->buf[SMOE_BUF_WORKSPACE][0], plan_ws_aligned(&c), stream);
     }
     case SMOE_STAGE_SRS:
+      // every process's partials for this batch are written before any peer
+      // reads them (and the previous batch's reads ended at its ROUTE barrier)
+      rc = smoe_layer_barrier(L, stream);
+      if (rc) return rc;
       return launch_srs(lr, peer_ptrs(L, SMOE_BUF_PARTIAL), c.hidden, local_ptrs(L, SMOE_BUF_HS),
                         n, st);
     case SMOE_STAGE_GATE:

@@ -95,8 +95,10 @@ class ShardGroup:
         import torch
         G, L = layer.G, layer.shard_count
         n, d, k, R = layer.max_tokens, layer.d, layer.k, layer.expert_rows
-        per_shard = {"partial": n * d * 2, "xin": R * d * 2, "xmeta": R * 8,
-                     "ypair": n * k * d * 2, "out": n * d * 2}
+        # two partial-input buffers: forward_async fills one while the peers'
+        # SRS reads the other
+        per_shard = {"partial": n * d * 2, "partial_b": n * d * 2, "xin": R * d * 2,
+                     "xmeta": R * 8, "ypair": n * k * d * 2, "out": n * d * 2}
         h = max(int(layer.tables.ngram_n), 1)
         peer, local = self.peer_tables(G, layer.N, per_shard, {"hist": n * h * 8})
 
@@ -105,11 +107,14 @@ class ShardGroup:
 
         # bf16 has no array-interface typestr: view int16 storage as bfloat16
         peer["partial_local"] = tensor(local["partial"], (L, n, d), "<i2").view(torch.bfloat16)
+        peer["partial_b_local"] = tensor(local["partial_b"], (L, n, d),
+                                         "<i2").view(torch.bfloat16)
         peer["out_local"] = tensor(local["out"], (L, n, d), "<i2").view(torch.bfloat16)
         peer["counts_local"] = tensor(local["counts"], (G, layer.N), "<i4")
         peer["hist_local"] = tensor(local["hist"], (n, h), "<i8")
         tensor(local["signal"], (64,), "<i4").zero_()
         peer["partial_local"].zero_()
+        peer["partial_b_local"].zero_()
         torch.cuda.synchronize()
         self._allgather(0)                 # every pad is zero before anyone signals
         return peer

@@ -214,11 +214,15 @@ class SpecMoELayer:
         avoid a copy)."""
         return getattr(self, "_bound_partial", self.partial)[:, :n]
 
-    def _bind_partial(self, P):
+    def _bind_partial(self, P, peer_ptrs=None):
+        """Bind the partial-input buffers: P is this process's [L, n, d] view;
+        peer_ptrs the G per-shard addresses (every process's copy of the same
+        slot) when shards span processes."""
         if getattr(self, "_bound_partial", self.partial) is P:
             return
         for g in range(self.G):
-            N.check(self.lib.smoe_layer_bind(self._h, N.BUF_PARTIAL, g, N.ptr(P[g])), "bind")
+            ptr = N.ptr(P[g]) if peer_ptrs is None else int(peer_ptrs[g])
+            N.check(self.lib.smoe_layer_bind(self._h, N.BUF_PARTIAL, g, ptr), "bind")
         self._bound_partial = P
 
     def run_device(self, tokens_t, hist_t=None, stream=None, stages=None):
@@ -326,16 +330,14 @@ class SpecMoELayer:
         `out` a pinned [n, d] bf16 tensor.  Partials are double-buffered:
         the H2D of batch i+1 overlaps the layer of batch i (the buffer is
         released as soon as batch i's SRS has read it), and the D2H of batch
-        i overlaps the first stages of batch i+1.  Single-process layers only
-        (peer processes read the partial buffers in place).  Data-dependent
+        i overlaps the first stages of batch i+1.  With shards spread over
+        processes (a ShardGroup) both partial slots are peer-visible and every
+        process must issue the same sequence of batches.  Data-dependent
         errors of a batch surface in its own `.result()`, which waits for
         that batch's D2H only (never drains the compute stream, so the H2D
         of the next batch is already queued behind the running one).
         """
         t = _dev.torch()
-        if self.group is not None:
-            res = self.forward(hidden_partials, token_ids, histories, out)
-            return _Done(res)
         st = self._pipeline()
         i = st["count"]
         st["count"] += 1
@@ -358,16 +360,30 @@ class SpecMoELayer:
             st["in"][slot].record(st["h2d"])
         # ---- the layer on the compute stream
         cs = st["compute"]
-        self._bind_partial(P)
+        self._bind_partial(P, st["peer_P"][slot])
         with t.cuda.stream(cs):
             cs.wait_event(st["in"][slot])
             hp_t = hist[:n] if histories is not None else None
-            self.run_device(tok[:n], hp_t, stream=cs, stages=[N.STAGE_PLAN, N.STAGE_SRS])
-            st["free_p"][slot].record(cs)
-            self.run_device(tok[:n], hp_t, stream=cs, stages=range(N.STAGE_GATE,
-                                                                   N.STAGE_COMBINE_SAG))
-            cs.wait_event(st["d2h_done"])          # previous output fully read out
-            self.run_device(tok[:n], hp_t, stream=cs, stages=[N.STAGE_COMBINE_SAG])
+            if self.group is None:
+                self.run_device(tok[:n], hp_t, stream=cs, stages=[N.STAGE_PLAN, N.STAGE_SRS])
+                st["free_p"][slot].record(cs)
+                self.run_device(tok[:n], hp_t, stream=cs,
+                                stages=range(N.STAGE_GATE, N.STAGE_COMBINE_SAG))
+                cs.wait_event(st["d2h_done"])      # previous output fully read out
+                self.run_device(tok[:n], hp_t, stream=cs, stages=[N.STAGE_COMBINE_SAG])
+            else:
+                # peers read this process's partial slot in their SRS and write
+                # its output buffer in their SAG: the slot is free once every
+                # process passed this batch's ROUTE barrier, and the previous
+                # D2H must end before the barrier that closes EXPERT_DOWN
+                self.run_device(tok[:n], hp_t, stream=cs,
+                                stages=range(N.STAGE_PLAN, N.STAGE_DISPATCH))
+                st["free_p"][slot].record(cs)
+                self.run_device(tok[:n], hp_t, stream=cs,
+                                stages=[N.STAGE_DISPATCH, N.STAGE_EXPERT_UP])
+                cs.wait_event(st["d2h_done"])
+                self.run_device(tok[:n], hp_t, stream=cs,
+                                stages=[N.STAGE_EXPERT_DOWN, N.STAGE_COMBINE_SAG])
             # this batch's error flag, read out before the next batch's plan
             # resets it (stream order); the host reads it in .result()
             err = t.empty(1, dtype=t.int32, pin_memory=True)
@@ -391,7 +407,13 @@ class SpecMoELayer:
             t = _dev.torch()
             dev = self.w_gate.device
             h = max(self.tables.ngram_n, 1)
-            st = {"P": [self.partial, t.zeros_like(self.partial)],
+            if self.group is None:
+                P = [self.partial, t.zeros_like(self.partial)]
+                peer_P = [None, None]
+            else:                              # both slots are peer-visible (IPC)
+                P = [self._peer["partial_local"], self._peer["partial_b_local"]]
+                peer_P = [self._peer["partial"], self._peer["partial_b"]]
+            st = {"P": P, "peer_P": peer_P,
                   "tok": [t.zeros(self.max_tokens, dtype=t.int64, device=dev) for _ in range(2)],
                   "hist": [t.zeros((self.max_tokens, h), dtype=t.int64, device=dev)
                            for _ in range(2)],
@@ -487,17 +509,6 @@ class _Pending:
         # the next batch (a device-flag .item() here would drain it)
         self._event.synchronize()
         self._layer._raise_for(int(self._err[0]))
-        return self._out
-
-
-class _Done:
-    def __init__(self, out):
-        self._out = out
-
-    def done(self) -> bool:
-        return True
-
-    def result(self):
         return self._out
 
 

@@ -31,3 +31,35 @@ def layer_worker(rank, world, port, cfg_over, n, result_q):
         grp.close()
     finally:
         dist.destroy_process_group()
+
+
+def async_worker(rank, world, port, cfg_over, sizes, result_q):
+    """forward_async over several batches with FRESH partials each (every
+    process writes its slot while peers may still read the other one)."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2503_04398_b200 import SpecMoELayer, synth
+        from paper_2503_04398_b200.dist import ShardGroup
+        ws = [synth.make_workload("toy", n=n, eps=0.3, seed=20 + i, cfg_override=cfg_over)
+              for i, n in enumerate(sizes)]
+        base = ws[0]
+        grp = ShardGroup.from_torch_distributed()
+        layer = SpecMoELayer(base.bundle, base.gate_w, base.w1, base.w3, base.w2,
+                             top_k=base.cfg["k"], max_tokens=max(sizes), group=grp)
+        L, b0 = layer.shard_count, layer.shard_begin
+        pins = [(torch.from_numpy(w.partials[b0:b0 + L]).to(torch.bfloat16).pin_memory(),
+                 torch.from_numpy(w.tokens).pin_memory(), torch.from_numpy(w.hist).pin_memory())
+                for w in ws]
+        outs = [torch.empty((len(w.tokens), base.cfg["d"]), dtype=torch.bfloat16).pin_memory()
+                for w in ws]
+        handles = [layer.forward_async(p, t, h, out=outs[i]) for i, (p, t, h) in enumerate(pins)]
+        got = [hd.result().float().numpy() for hd in handles]
+        result_q.put((rank, got))
+        dist.barrier()
+        grp.close()
+    finally:
+        dist.destroy_process_group()

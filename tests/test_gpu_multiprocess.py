@@ -56,3 +56,36 @@ def test_two_process_layer_matches_single_process(world, over):
             assert np.array_equal(o, ref)
         tot += np.asarray(s)
     assert tot.tolist() == st.tolist()
+
+
+@pytest.mark.timeout(600)
+def test_two_process_forward_async_matches_single_process():
+    """Pipelined serving across processes: double-buffered peer-visible
+    partial slots, fresh inputs per batch; every batch equals the
+    single-process synchronous forward bit for bit."""
+    world, over = 2, {"G": 4, "N": 16}
+    sizes = (300, 257, 300, 12, 299)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=mp_worker.async_worker, args=(r, world, port, over, sizes, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, got = q.get(timeout=540)
+        res[r] = got
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ws = [synth.make_workload("toy", n=n, eps=0.3, seed=20 + i, cfg_override=over)
+          for i, n in enumerate(sizes)]
+    base = ws[0]
+    ref_layer = SpecMoELayer(base.bundle, base.gate_w, base.w1, base.w3, base.w2,
+                             top_k=base.cfg["k"], max_tokens=max(sizes))
+    for i, w in enumerate(ws):
+        want = ref_layer.forward(torch.from_numpy(w.partials).to(torch.bfloat16), w.tokens,
+                                 w.hist).float().numpy()
+        for r in range(world):
+            assert np.array_equal(res[r][i], want), (r, i)
