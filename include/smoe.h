@@ -245,6 +245,19 @@ int smoe_layer_set_weights(smoe_layer* layer, const void* w_gate,
                            const float* b_gate, const void* w13,
                            const void* w2);
 
+/* Same as smoe_layer_set_weights, with w13 and w2 in the TMA-box-tiled
+ * layout of smoe_tile_weights (every 256 x 64 weight box the expert GEMMs
+ * load is one contiguous 32 KiB run of HBM). */
+int smoe_layer_set_weights_tiled(smoe_layer* layer, const void* w_gate,
+                                 const float* b_gate, const void* w13_tiled,
+                                 const void* w2_tiled);
+
+/* Box-tile a row-major bf16 matrix [rows, cols] (rows % 256 == 0,
+ * cols % 64 == 0): dst[((rb * cols/64 + kb) * 256 + r) * 64 + c] =
+ * src[(rb * 256 + r) * cols + kb * 64 + c].  Experts stack along rows. */
+int smoe_tile_weights(const void* src, int64_t rows, int64_t cols, void* dst,
+                      void* stream);
+
 /* Pack per-expert gate_proj [f, d] and up_proj [f, d] (both bf16, expert e at
  * w1[e], w3[e]) into the w13 layout the SwiGLU GEMM reads. */
 int smoe_pack_w13(const void* w1, const void* w3, int32_t n_local_experts,

@@ -29,6 +29,8 @@ struct GemmArgs {
                              // n-group); 0: derive from K
   char* c;                   // store / swiglu output
   int64_t ldc;               // elements
+  int32_t b_tiled;           // B in smoe_tile_weights layout (one contiguous box per
+                             // (problem b_index, n-block, k-block)); else row-major
   const int64_t* meta;       // scatter: per A row
   char* dst_base[SMOE_MAX_SHARDS];
   int64_t ldd;               // elements

@@ -189,20 +189,27 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
             (int32_t)(sp.a_off[tc.p] + (int64_t)tc.m_blk * kTileM + rank * kGemmBM);
         const int32_t b_row =
             sp.b_idx[tc.p] * args.n_b + tc.n_blk * kGemmBN + rank * (kGemmBN / CG);
+        // tiled B: box (b_index, n-block, k-block) starts at row
+        // ((b_index * n_tiles_n + n_blk) * num_k_blocks + kb) * 256 of a [*, 64] tensor
+        const int32_t b_box0 =
+            ((sp.b_idx[tc.p] * args.n_tiles_n + tc.n_blk) * args.num_k_blocks) * kGemmBN +
+            rank * (kGemmBN / CG);
         for (int32_t kb = 0; kb < args.num_k_blocks; ++kb) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
           const uint32_t sa = smem_addr(smem_a + stage * kABytes);
           const uint32_t sb = smem_addr(smem_b + stage * kBBytes);
+          const int32_t bc0 = args.b_tiled ? 0 : kb * kGemmBK;
+          const int32_t bc1 = args.b_tiled ? b_box0 + kb * kGemmBN : b_row;
           if (CG == 1) {
             mbar_expect_tx(fb, S::kStageBytes);
             tma_load_2d(sa, &tmap_a, fb, kb * kGemmBK, a_row);
-            tma_load_2d(sb, &tmap_b, fb, kb * kGemmBK, b_row);
+            tma_load_2d(sb, &tmap_b, fb, bc0, bc1);
           } else {
             if (rank == 0) mbar_expect_tx(fb, 2 * S::kStageBytes);
             const uint32_t fb0 = map_to_rank(fb, 0);
             tma_load_2d_cg2(sa, &tmap_a, fb0, kb * kGemmBK, a_row);
-            tma_load_2d_cg2(sb, &tmap_b, fb0, kb * kGemmBK, b_row);
+            tma_load_2d_cg2(sb, &tmap_b, fb0, bc0, bc1);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -465,9 +472,36 @@ __global__ void pack_w13_kernel(const uint4* __restrict__ w1, const uint4* __res
   }
 }
 
+// dst box (rb, kb) = src rows [rb*256, +256) x cols [kb*64, +64), one 32 KiB run
+__global__ void tile_weights_kernel(const uint4* __restrict__ src, int64_t rows, int64_t cols,
+                                    uint4* __restrict__ dst) {
+  const int64_t kbs = cols / kGemmBK;
+  const int64_t total = rows * cols / 8;                  // 16-B vectors
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c8 = i & 7;                             // vector within a 64-element row
+    const int64_t r = (i >> 3) & (kGemmBN - 1);           // row within the box
+    const int64_t box = i >> 11;                          // 256 rows x 8 vectors per box
+    const int64_t rb = box / kbs, kb = box - rb * kbs;
+    dst[i] = src[((rb * kGemmBN + r) * cols + kb * kGemmBK) / 8 + c8];
+  }
+}
+
 }  // namespace smoe
 
 using namespace smoe;
+
+extern "C" int smoe_tile_weights(const void* src, int64_t rows, int64_t cols, void* dst,
+                                 void* stream) {
+  if (!src || !dst || rows <= 0 || cols <= 0) return SMOE_ERR_INVALID_ARG;
+  if (rows % kGemmBN || cols % kGemmBK) return SMOE_ERR_UNSUPPORTED;
+  const int64_t vecs = rows * cols / 8;
+  const int blocks = (int)std::min<int64_t>(ceil_div(vecs, 256), 148 * 32);
+  tile_weights_kernel<<<blocks, 256, 0, as_stream(stream)>>>(static_cast<const uint4*>(src), rows,
+                                                              cols, static_cast<uint4*>(dst));
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
 
 extern "C" int smoe_pack_w13(const void* w1, const void* w3, int32_t n_local_experts,
                              int32_t ffn, int32_t hidden, void* w13, void* stream) {

@@ -36,6 +36,7 @@ struct smoe_layer {
   const float* b_gate = nullptr;
   const void* w13 = nullptr;
   const void* w2 = nullptr;
+  bool w_tiled = false;              // w13 / w2 in smoe_tile_weights layout
   // GEMM descriptors
   bool maps_ready = false;
   int maps_cg_up = 0, maps_cg_down = 0;
@@ -130,8 +131,17 @@ extern "C" int smoe_layer_set_weights(smoe_layer* L, const void* w_gate, const f
                                       const void* w13, const void* w2) {
   if (!L || !w_gate || !w13 || !w2) return SMOE_ERR_INVALID_ARG;
   L->w_gate = w_gate; L->b_gate = b_gate; L->w13 = w13; L->w2 = w2;
+  L->w_tiled = false;
   L->maps_ready = false;
   return SMOE_OK;
+}
+
+extern "C" int smoe_layer_set_weights_tiled(smoe_layer* L, const void* w_gate,
+                                            const float* b_gate, const void* w13_tiled,
+                                            const void* w2_tiled) {
+  int rc = smoe_layer_set_weights(L, w_gate, b_gate, w13_tiled, w2_tiled);
+  if (rc == SMOE_OK) L->w_tiled = true;
+  return rc;
 }
 
 static ShardPtrs local_ptrs(const smoe_layer* L, int slot) {
@@ -210,12 +220,16 @@ static int ensure_maps(smoe_layer* L) {
   if ((rc = make_tmap_bf16(&L->map_x, L->buf[SMOE_BUF_XIN][c.shard_begin], rows, c.hidden,
                            kGemmBM)))
     return rc;
-  if ((rc = make_tmap_bf16(&L->map_w13, L->w13, nl * 2 * c.ffn, c.hidden,
-                           gemm_b_box_rows(gemm_cta_group(0)))))
+  // tiled weights: a [rows * (K / 64), 64] tensor whose boxes are contiguous
+  const int64_t w13_rows = nl * 2 * c.ffn, w2_rows = nl * c.hidden;
+  if ((rc = make_tmap_bf16(&L->map_w13, L->w13,
+                           L->w_tiled ? w13_rows * (c.hidden / kGemmBK) : w13_rows,
+                           L->w_tiled ? kGemmBK : c.hidden, gemm_b_box_rows(gemm_cta_group(0)))))
     return rc;
   if ((rc = make_tmap_bf16(&L->map_h, L->buf[SMOE_BUF_HMID][0], rows, c.ffn, kGemmBM))) return rc;
-  if ((rc = make_tmap_bf16(&L->map_w2, L->w2, nl * c.hidden, c.ffn,
-                           gemm_b_box_rows(gemm_cta_group(1)))))
+  if ((rc = make_tmap_bf16(&L->map_w2, L->w2,
+                           L->w_tiled ? w2_rows * (c.ffn / kGemmBK) : w2_rows,
+                           L->w_tiled ? kGemmBK : c.ffn, gemm_b_box_rows(gemm_cta_group(1)))))
     return rc;
   // the tcgen05 gate needs the resident shards' hs buffers as one arena
   const int64_t hs_stride = c.max_tokens * (int64_t)c.hidden * 2;
@@ -344,6 +358,7 @@ extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tok
       a.n_b = 2 * c.ffn;
       a.c = static_cast<char*>(L->buf[SMOE_BUF_HMID][0]);
       a.ldc = c.ffn;
+      a.b_tiled = L->w_tiled;
       return launch_grouped_gemm(L->map_x, L->map_w13, a, kEpiSwiGLU, L->maps_cg_up, st);
     }
     case SMOE_STAGE_EXPERT_DOWN: {
@@ -356,6 +371,7 @@ extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tok
       a.meta = static_cast<const int64_t*>(L->buf[SMOE_BUF_XMETA][c.shard_begin]);
       for (int g = 0; g < c.n_shards; ++g) a.dst_base[g] = static_cast<char*>(L->buf[SMOE_BUF_YPAIR][g]);
       a.ldd = c.hidden;
+      a.b_tiled = L->w_tiled;
       rc = launch_grouped_gemm(L->map_h, L->map_w2, a, kEpiScatter, L->maps_cg_down, st);
       if (rc) return rc;
       return smoe_layer_barrier(L, stream);

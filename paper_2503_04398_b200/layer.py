@@ -68,7 +68,7 @@ class SpecMoELayer:
         if shared_from is not None:
             src = shared_from
             for a in ("perm", "slot_owner", "slot_first", "local_slots", "w_gate", "b_gate",
-                      "w13", "w2"):
+                      "w13", "w2", "w_tiled"):
                 setattr(self, a, getattr(src, a))
         else:
             self._place_weights(labels, gate_w, gate_b, w1, w3, w2)
@@ -104,6 +104,20 @@ class SpecMoELayer:
         if self.local_slots:
             N.check(self.lib.smoe_pack_w13(N.ptr(w1l), N.ptr(w3l), self.local_slots, self.f,
                                            self.d, N.ptr(self.w13), N.stream_ptr()), "pack_w13")
+        del w1l, w3l
+        # box-tiled copies: every 256 x 64 weight box the GEMMs load is one
+        # contiguous 32 KiB run (SMOE_UNTILED_WEIGHTS=1 keeps row-major, A/B only)
+        import os
+        self.w_tiled = bool(self.local_slots) and os.environ.get("SMOE_UNTILED_WEIGHTS") != "1"
+        if self.w_tiled:
+            for name, rows, cols in (("w13", self.local_slots * 2 * self.f, self.d),
+                                     ("w2", self.local_slots * self.d, self.f)):
+                src = getattr(self, name)
+                dst = t.empty_like(src)
+                N.check(self.lib.smoe_tile_weights(N.ptr(src), rows, cols, N.ptr(dst),
+                                                   N.stream_ptr()), "tile_weights")
+                setattr(self, name, dst)
+                del src
 
     # ------------------------------------------------------------ buffers
     def _alloc_buffers(self):
@@ -195,8 +209,9 @@ class SpecMoELayer:
         N.check(self.lib.smoe_layer_set_tables(
             h, N.ptr(tb.t_labels), N.ptr(tb.t_conf), tb.vocab, N.ptr(tb.a_best), N.ptr(tb.a_conf),
             tb.a_rows, tb.ngram_n, owner), "layer_set_tables")
-        N.check(self.lib.smoe_layer_set_weights(h, N.ptr(self.w_gate), N.ptr(self.b_gate),
-                                                N.ptr(self.w13), N.ptr(self.w2)),
+        set_w = (self.lib.smoe_layer_set_weights_tiled if self.w_tiled
+                 else self.lib.smoe_layer_set_weights)
+        N.check(set_w(h, N.ptr(self.w_gate), N.ptr(self.b_gate), N.ptr(self.w13), N.ptr(self.w2)),
                 "layer_set_weights")
 
     def __del__(self):

@@ -85,3 +85,31 @@ def test_swiglu_epilogue():
         u = x @ w3[e].float().T
         ref = torch.nn.functional.silu(g) * u
         assert rel(H[offs[e]:offs[e] + ms[e]], ref) < 1e-2, e
+
+
+def test_tile_weights_layout():
+    """smoe_tile_weights: box (rb, kb) = rows [256 rb, +256) x cols [64 kb, +64),
+    one contiguous run, boxes ordered rb-major."""
+    lib = N.lib()
+    rows, cols = 512, 192
+    src = torch.randn(rows, cols, device="cuda").to(torch.bfloat16)
+    dst = torch.empty_like(src)
+    N.check(lib.smoe_tile_weights(N.ptr(src), rows, cols, N.ptr(dst), N.stream_ptr()), "tile")
+    want = src.view(rows // 256, 256, cols // 64, 64).permute(0, 2, 1, 3).reshape(rows, cols)
+    assert torch.equal(dst.view(-1), want.contiguous().view(-1))
+    assert lib.smoe_tile_weights(N.ptr(src), 100, cols, N.ptr(dst), N.stream_ptr()) != N.OK
+
+
+def test_layer_tiled_weights_bit_identical_to_row_major(monkeypatch):
+    """Box-tiled expert weights change only where the GEMMs' TMA reads from."""
+    from paper_2503_04398_b200 import SpecMoELayer, synth
+    over = {"G": 4, "N": 16, "k": 2, "d": 512, "f": 384}
+    w = synth.make_workload("toy", n=700, eps=0.3, seed=5, cfg_override=over)
+    parts = torch.from_numpy(w.partials).to(torch.bfloat16)
+    outs = []
+    for untiled in ("0", "1"):
+        monkeypatch.setenv("SMOE_UNTILED_WEIGHTS", untiled)
+        layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=700)
+        assert layer.w_tiled == (untiled == "0")
+        outs.append(layer.forward(parts, w.tokens, w.hist).clone())
+    assert torch.equal(outs[0], outs[1])
