@@ -307,6 +307,31 @@ int smoe_combine_rows(const void* y, const int32_t* pair_pos, const float* topk_
                       int64_t rows, int32_t top_k, int32_t hidden, void* out, void* stream);
 
 /* ======================================================================= *
+ *  Standalone SRS / SAG collectives (the paper's drop-in replacements for  *
+ *  reduce-scatter and all-gather, Algorithm 2)               *
+ * ======================================================================= */
+/* Shuffled reduce-scatter over n_shards partial buffers (every partial
+ * [n_tokens, hidden] bf16, all addressable from this GPU: local or peer):
+ *   outs[g - shard_begin][j, :] = bf16( sum_{r < n_shards} partials[r][forward[g*group + j], :] )
+ * for every shard g in [shard_begin, shard_begin + shard_count) and
+ * j < counts[g]; fp32 sum in shard order.  forward / counts / group are the
+ * plan of smoe_rebatch_plan or smoe_lookup_plan (device memory).  partials
+ * and outs are HOST arrays of device pointers (n_shards <= 16). */
+int smoe_srs(const void* const* partials, int32_t n_shards, int32_t shard_begin,
+             int32_t shard_count, const int64_t* forward, const int32_t* counts,
+             const int64_t* group, int64_t n_tokens, int32_t hidden, void* const* outs,
+             void* stream);
+
+/* Shuffled all-gather (resume fused with the all-gather): for every shard g,
+ * row j < counts[g] of blocks[g] ([group, hidden] bf16) is stored at the
+ * token's original position forward[g*group + j] of every outs[o]
+ * ([n_tokens, hidden], o < n_outs).  blocks / outs are HOST arrays of device
+ * pointers (n_shards, n_outs <= 16). */
+int smoe_sag(const void* const* blocks, int32_t n_shards, const int64_t* forward,
+             const int32_t* counts, const int64_t* group, int64_t n_tokens, int32_t hidden,
+             void* const* outs, int32_t n_outs, void* stream);
+
+/* ======================================================================= *
  *  Grouped GEMM (K6) — exposed for tests and microbenchmarks                *
  * ======================================================================= */
 /* For problem p: C[c_off_p + i, :] = epilogue(A[a_off_p + i, :K] . B_p^T)

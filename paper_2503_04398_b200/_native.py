@@ -44,6 +44,8 @@ SIGNATURES = [
     ("smoe_layer_set_weights", C.c_int, [P, P, P, P, P]),
     ("smoe_layer_set_weights_tiled", C.c_int, [P, P, P, P, P]),
     ("smoe_tile_weights", C.c_int, [P, c_i64, c_i64, P, P]),
+    ("smoe_srs", C.c_int, [P, c_i32, c_i32, c_i32, P, P, P, c_i64, c_i32, P, P]),
+    ("smoe_sag", C.c_int, [P, c_i32, P, P, P, c_i64, c_i32, P, c_i32, P]),
     ("smoe_pack_w13", C.c_int, [P, P, c_i32, c_i32, c_i32, P, P]),
     ("smoe_layer_stage", C.c_int, [P, c_i32, P, P, c_i64, P]),
     ("smoe_layer_forward", C.c_int, [P, P, P, c_i64, P]),

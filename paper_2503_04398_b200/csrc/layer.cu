@@ -469,3 +469,38 @@ extern "C" int smoe_get_option(int32_t key) {
   if (key == SMOE_OPT_GATE_TENSOR) return gate_tc_enabled();
   return -1;
 }
+
+// ---------------------------------------------------------------- standalone SRS / SAG
+extern "C" int smoe_srs(const void* const* partials, int32_t n_shards, int32_t shard_begin,
+                        int32_t shard_count, const int64_t* forward, const int32_t* counts,
+                        const int64_t* group, int64_t n_tokens, int32_t hidden,
+                        void* const* outs, void* stream) {
+  if (!partials || !outs || !forward || !counts || !group || n_tokens < 0 || hidden <= 0)
+    return SMOE_ERR_INVALID_ARG;
+  if (n_shards < 1 || n_shards > SMOE_MAX_SHARDS || shard_begin < 0 || shard_count < 1 ||
+      shard_begin + shard_count > n_shards)
+    return SMOE_ERR_INVALID_ARG;
+  LocalRows lr{};
+  lr.counts = counts; lr.group = group; lr.forward = forward;
+  lr.shard_begin = shard_begin; lr.shard_count = shard_count; lr.n_shards = n_shards;
+  ShardPtrs p{}, o{};
+  for (int g = 0; g < n_shards; ++g) p.p[g] = static_cast<char*>(const_cast<void*>(partials[g]));
+  for (int i = 0; i < shard_count; ++i) o.p[i] = static_cast<char*>(outs[i]);
+  return launch_srs(lr, p, hidden, o, n_tokens, as_stream(stream));
+}
+
+extern "C" int smoe_sag(const void* const* blocks, int32_t n_shards, const int64_t* forward,
+                        const int32_t* counts, const int64_t* group, int64_t n_tokens,
+                        int32_t hidden, void* const* outs, int32_t n_outs, void* stream) {
+  if (!blocks || !outs || !forward || !counts || !group || n_tokens < 0 || hidden <= 0)
+    return SMOE_ERR_INVALID_ARG;
+  if (n_shards < 1 || n_shards > SMOE_MAX_SHARDS || n_outs < 1 || n_outs > SMOE_MAX_SHARDS)
+    return SMOE_ERR_INVALID_ARG;
+  LocalRows lr{};
+  lr.counts = counts; lr.group = group; lr.forward = forward;
+  lr.shard_begin = 0; lr.shard_count = n_shards; lr.n_shards = n_shards;
+  ShardPtrs b{}, o{};
+  for (int g = 0; g < n_shards; ++g) b.p[g] = static_cast<char*>(const_cast<void*>(blocks[g]));
+  for (int i = 0; i < n_outs; ++i) o.p[i] = static_cast<char*>(outs[i]);
+  return launch_sag(lr, hidden, b, o, n_outs, n_tokens, as_stream(stream));
+}

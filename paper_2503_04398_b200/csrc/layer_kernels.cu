@@ -897,6 +897,51 @@ int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtr
   return SMOE_OK;
 }
 
+// ------------------------------------------------------------------ standalone SAG
+// Warp per source row (whole rows, or 1 KiB chunks for small batches as in
+// the SRS): one 16-B load, n_outs stores to the token's original position.
+__global__ void __launch_bounds__(256)
+sag_kernel(LocalRows lr, int64_t d, ShardPtrs blocks, ShardPtrs outs, int32_t n_outs,
+           int32_t whole_rows) {
+  __shared__ RowMap rm;
+  __shared__ char* s_in[SMOE_MAX_SHARDS];
+  __shared__ char* s_out[SMOE_MAX_SHARDS];
+  stage_ptrs(s_in, blocks);
+  stage_ptrs(s_out, outs);
+  load_rowmap(rm, lr);
+  const int lane = threadIdx.x & 31;
+  const int64_t vecs = d / 8;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const bool whole = rm.total >= whole_rows;
+  const int64_t chunks = whole ? 1 : (vecs + kChunkVecs - 1) / kChunkVecs;
+  const int64_t cv = whole ? vecs : kChunkVecs;
+  for (int64_t it = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+       it < (int64_t)rm.total * chunks; it += nwarps) {
+    const int64_t q = whole ? it : it / chunks;
+    const int64_t c = it - q * chunks;
+    int32_t gl; int64_t j;
+    decode_row(rm, lr.shard_count, q, gl, j);
+    const int64_t g = lr.shard_begin + gl;
+    const int64_t i = lr.forward[g * rm.group + j];
+    const char* src = s_in[gl] + j * d * 2;
+    const int64_t v1 = min(vecs, (c + 1) * cv);
+    for (int64_t v = c * cv + lane; v < v1; v += 32) {
+      const uint4 x = ld_nc_v4(src + v * 16);
+      for (int o = 0; o < n_outs; ++o) st_v4(s_out[o] + (i * d + v * 8) * 2, x);
+    }
+  }
+}
+
+int launch_sag(const LocalRows& lr, int64_t d, const ShardPtrs& blocks, const ShardPtrs& outs,
+               int32_t n_outs, int64_t n_rows_bound, cudaStream_t st) {
+  if (d % 8) return SMOE_ERR_UNSUPPORTED;
+  if (n_rows_bound <= 0) return SMOE_OK;
+  sag_kernel<<<grid_items(n_rows_bound, d), 256, 0, st>>>(lr, d, blocks, outs, n_outs,
+                                                           whole_rows_from());
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
 // ------------------------------------------------------------------ single-rank helpers
 // Pair offsets in expert-major send order (DS-MoE all2allv packing):
 //   pos(j, s) = sum_{e' < e} counts[e'] + #{earlier pairs with the same expert e}

@@ -73,6 +73,11 @@ int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtr
                        const ShardPtrs& topk_w, const ShardPtrs& outs, const HistUpdate& hu,
                        int64_t n_rows_bound, cudaStream_t st);
 
+// Standalone shuffled all-gather (smoe_sag): row j of blocks[g] -> every
+// outs[o] at forward[g*group + j].
+int launch_sag(const LocalRows& lr, int64_t d, const ShardPtrs& blocks, const ShardPtrs& outs,
+               int32_t n_outs, int64_t n_rows_bound, cudaStream_t st);
+
 // Single-rank building blocks (DS-MoE baseline, smoe_gate_topk & co.)
 int launch_pair_offsets(const int32_t* topk_ids, int64_t rows, int32_t k, int32_t N,
                         int32_t* pair_pos, int32_t* counts, cudaStream_t st);
