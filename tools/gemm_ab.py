@@ -10,7 +10,7 @@ import numpy as np
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 
-def main(name="mixtral", tokens=16384, reps=6, steps=5):
+def main(name="mixtral", tokens=16384, reps=6, steps=5, which="both"):
     import torch
     from paper_2503_04398_b200 import SpecMoELayer, synth
     from paper_2503_04398_b200 import _native as N
@@ -27,7 +27,10 @@ def main(name="mixtral", tokens=16384, reps=6, steps=5):
     ref = None
     for rep in range(reps):
         for cg in (1, 2) if rep % 2 == 0 else (2, 1):
-            for key in (N.OPT_GEMM_CTA_GROUP_UP, N.OPT_GEMM_CTA_GROUP_DOWN):
+            keys = {"both": (N.OPT_GEMM_CTA_GROUP_UP, N.OPT_GEMM_CTA_GROUP_DOWN),
+                    "up": (N.OPT_GEMM_CTA_GROUP_UP,),
+                    "down": (N.OPT_GEMM_CTA_GROUP_DOWN,)}[which]
+            for key in keys:
                 N.check(lib.smoe_set_option(key, cg), "set_option")
             layer.run_device(tok, hist)       # warm (maps rebuilt on switch)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -55,7 +58,7 @@ def main(name="mixtral", tokens=16384, reps=6, steps=5):
     d, f = w.cfg["d"], w.cfg["f"]
     for cg in (1, 2):
         up, dn = np.median(res[cg]["up"]), np.median(res[cg]["down"])
-        print(json.dumps({"config": name, "tokens": tokens, "cta_group": cg,
+        print(json.dumps({"config": name, "tokens": tokens, "cta_group": cg, "which": which,
                           "up_ms": up, "down_ms": dn,
                           "up_tflops": 4.0 * pairs * d * f / up / 1e9,
                           "down_tflops": 2.0 * pairs * d * f / dn / 1e9,
@@ -64,4 +67,5 @@ def main(name="mixtral", tokens=16384, reps=6, steps=5):
 
 if __name__ == "__main__":
     a = sys.argv[1:]
-    main(a[0] if a else "mixtral", int(a[1]) if len(a) > 1 else 16384)
+    main(a[0] if a else "mixtral", int(a[1]) if len(a) > 1 else 16384,
+         reps=int(a[3]) if len(a) > 3 else 6, which=a[2] if len(a) > 2 else "both")
