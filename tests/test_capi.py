@@ -68,3 +68,32 @@ def test_layer_config_struct_matches_header():
     assert [f[1] for f in fields] == [f[0] for f in _native.LayerConfig._fields_]
     for (bits, name), (fname, ctype) in zip(fields, _native.LayerConfig._fields_):
         assert ctypes.sizeof(ctype) * 8 == int(bits), name
+
+
+def test_new_entry_points_validate_before_device_work(lib):
+    """smoe_srs / smoe_sag / smoe_tile_weights / options reject bad arguments
+    on the host (no CUDA call is made, so this runs without a GPU)."""
+    from paper_2503_04398_b200 import _native as N
+    h = N.load()
+    fake = 256
+    arr = (ctypes.c_void_p * 17)(*([fake] * 17))
+    p = ctypes.cast(arr, ctypes.c_void_p)
+    # too many shards, bad shard range, null plan
+    assert h.smoe_srs(p, 17, 0, 1, fake, fake, fake, 10, 64, p, None) == N.ERR_INVALID_ARG
+    assert h.smoe_srs(p, 4, 3, 2, fake, fake, fake, 10, 64, p, None) == N.ERR_INVALID_ARG
+    assert h.smoe_srs(p, 4, 0, 4, None, fake, fake, 10, 64, p, None) == N.ERR_INVALID_ARG
+    assert h.smoe_sag(p, 4, fake, fake, fake, 10, 64, p, 0, None) == N.ERR_INVALID_ARG
+    assert h.smoe_sag(p, 4, fake, fake, fake, 10, 64, p, 17, None) == N.ERR_INVALID_ARG
+    # tile geometry: rows % 256, cols % 64
+    assert h.smoe_tile_weights(fake, 100, 64, fake, None) == N.ERR_UNSUPPORTED
+    assert h.smoe_tile_weights(fake, 256, 100, fake, None) == N.ERR_UNSUPPORTED
+    assert h.smoe_tile_weights(None, 256, 64, fake, None) == N.ERR_INVALID_ARG
+    # options: known keys round-trip, unknown keys / values are rejected
+    for key, vals in ((N.OPT_GEMM_CTA_GROUP_UP, (1, 2)), (N.OPT_GEMM_CTA_GROUP_DOWN, (1, 2)),
+                      (N.OPT_GATE_TENSOR, (0, 1))):
+        old = h.smoe_get_option(key)
+        for v in vals:
+            assert h.smoe_set_option(key, v) == N.OK and h.smoe_get_option(key) == v
+        assert h.smoe_set_option(key, 7) == N.ERR_INVALID_ARG
+        assert h.smoe_set_option(key, old) == N.OK
+    assert h.smoe_set_option(99, 1) == N.ERR_INVALID_ARG and h.smoe_get_option(99) == -1
