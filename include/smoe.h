@@ -56,6 +56,8 @@ const char* smoe_version(void);
 #define SMOE_OPT_GEMM_CTA_GROUP_DOWN 1  /* down GEMM: 2 = 256x256 tile per SM pair (default) */
 #define SMOE_OPT_GATE_TENSOR         2  /* layer gate: 1 = tcgen05 kernel (default), */
                                         /* 0 = mma.sync / CUDA-core kernels          */
+#define SMOE_OPT_GEMM_PAIR_MIN_ROWS  3  /* layer down GEMM: one SM per tile while    */
+                                        /* n*k <= this * n_experts (default 64)      */
 int smoe_set_option(int32_t key, int32_t value);
 int smoe_get_option(int32_t key);
 const char* smoe_status_string(int status);

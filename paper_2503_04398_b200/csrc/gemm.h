@@ -43,6 +43,10 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t col
 // cta_group of the up (which = 0) / down (which = 1) GEMM: 1 = one SM per
 // 128x256 tile, 2 = SM pair per 256x256 tile (tcgen05 cta_group::2).
 int gemm_cta_group(int which);
+// The layer's down GEMM uses the SM pair only above this many routed rows per
+// expert on average (SMOE_OPT_GEMM_PAIR_MIN_ROWS).
+int gemm_pair_min_rows();
+void set_gemm_pair_min_rows(int rows);
 void set_gemm_cta_group(int which, int cg);
 // Rows of B staged per CTA per k-block: the box height of B's tensor map.
 int gemm_b_box_rows(int cg);

@@ -437,6 +437,9 @@ static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
 static int g_cta_group[2] = {1, 2};
 
 int gemm_cta_group(int which) { return g_cta_group[which ? 1 : 0]; }
+static int g_pair_min_rows = 64;
+int gemm_pair_min_rows() { return g_pair_min_rows; }
+void set_gemm_pair_min_rows(int rows) { g_pair_min_rows = rows; }
 void set_gemm_cta_group(int which, int cg) { g_cta_group[which ? 1 : 0] = (cg == 2) ? 2 : 1; }
 int gemm_b_box_rows(int cg) { return kGemmBN / cg; }
 

@@ -41,6 +41,7 @@ struct smoe_layer {
   bool maps_ready = false;
   int maps_cg_up = 0, maps_cg_down = 0;
   CUtensorMap map_x, map_w13, map_h, map_w2;
+  CUtensorMap map_w2_single;         // w2 with one-SM boxes (small batches, see EXPERT_DOWN)
   // tensor-core gate: hidden rows of the resident shards (one arena) and W_g
   bool gate_tc = false;
   CUtensorMap map_hs, map_wg;
@@ -231,6 +232,10 @@ static int ensure_maps(smoe_layer* L) {
                            L->w_tiled ? w2_rows * (c.ffn / kGemmBK) : w2_rows,
                            L->w_tiled ? kGemmBK : c.ffn, gemm_b_box_rows(gemm_cta_group(1)))))
     return rc;
+  if ((rc = make_tmap_bf16(&L->map_w2_single, L->w2,
+                           L->w_tiled ? w2_rows * (c.ffn / kGemmBK) : w2_rows,
+                           L->w_tiled ? kGemmBK : c.ffn, gemm_b_box_rows(1))))
+    return rc;
   // the tcgen05 gate needs the resident shards' hs buffers as one arena
   const int64_t hs_stride = c.max_tokens * (int64_t)c.hidden * 2;
   bool arena = gate_tc_supported(c.n_experts, c.top_k, c.hidden);
@@ -372,7 +377,12 @@ extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tok
       for (int g = 0; g < c.n_shards; ++g) a.dst_base[g] = static_cast<char*>(L->buf[SMOE_BUF_YPAIR][g]);
       a.ldd = c.hidden;
       a.b_tiled = L->w_tiled;
-      rc = launch_grouped_gemm(L->map_h, L->map_w2, a, kEpiScatter, L->maps_cg_down, st);
+      // decode-sized batches (<= gemm_pair_min_rows() routed rows per expert on
+      // average): one SM per tile streams w2 in a single wave; the SM pair's
+      // second, partial wave costs 5-16% there (profiles/r1_down_cta_group_small.jsonl)
+      const bool small = n * (int64_t)c.top_k <= (int64_t)gemm_pair_min_rows() * c.n_experts;
+      rc = small ? launch_grouped_gemm(L->map_h, L->map_w2_single, a, kEpiScatter, 1, st)
+                 : launch_grouped_gemm(L->map_h, L->map_w2, a, kEpiScatter, L->maps_cg_down, st);
       if (rc) return rc;
       return smoe_layer_barrier(L, stream);
     }
@@ -458,6 +468,10 @@ extern "C" int smoe_set_option(int32_t key, int32_t value) {
       if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
       set_gate_tc_enabled(value);
       return SMOE_OK;
+    case SMOE_OPT_GEMM_PAIR_MIN_ROWS:
+      if (value < 0) return SMOE_ERR_INVALID_ARG;
+      set_gemm_pair_min_rows(value);
+      return SMOE_OK;
     default:
       return SMOE_ERR_INVALID_ARG;
   }
@@ -467,6 +481,7 @@ extern "C" int smoe_get_option(int32_t key) {
   if (key == SMOE_OPT_GEMM_CTA_GROUP_UP) return gemm_cta_group(0);
   if (key == SMOE_OPT_GEMM_CTA_GROUP_DOWN) return gemm_cta_group(1);
   if (key == SMOE_OPT_GATE_TENSOR) return gate_tc_enabled();
+  if (key == SMOE_OPT_GEMM_PAIR_MIN_ROWS) return gemm_pair_min_rows();
   return -1;
 }
 

@@ -113,3 +113,23 @@ def test_layer_tiled_weights_bit_identical_to_row_major(monkeypatch):
         assert layer.w_tiled == (untiled == "0")
         outs.append(layer.forward(parts, w.tokens, w.hist).clone())
     assert torch.equal(outs[0], outs[1])
+
+
+def test_small_batch_down_gemm_single_sm_matches_pair():
+    """Decode-sized batches run the down GEMM on one SM per tile; the output is
+    bit-identical to the SM-pair kernel (SMOE_OPT_GEMM_PAIR_MIN_ROWS = 0)."""
+    from paper_2503_04398_b200 import SpecMoELayer, synth
+    lib = N.lib()
+    over = {"G": 4, "N": 16, "k": 2, "d": 512, "f": 384}
+    w = synth.make_workload("toy", n=64, eps=0.3, seed=6, cfg_override=over)
+    parts = torch.from_numpy(w.partials).to(torch.bfloat16)
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=64)
+    old = lib.smoe_get_option(N.OPT_GEMM_PAIR_MIN_ROWS)
+    outs = []
+    try:
+        for rows in (64, 0):
+            N.check(lib.smoe_set_option(N.OPT_GEMM_PAIR_MIN_ROWS, rows), "opt")
+            outs.append(layer.forward(parts, w.tokens, w.hist).clone())
+    finally:
+        N.check(lib.smoe_set_option(N.OPT_GEMM_PAIR_MIN_ROWS, old), "opt")
+    assert torch.equal(outs[0], outs[1])
