@@ -246,8 +246,8 @@ class SpecMoELayer:
         n = int(tokens_t.shape[0])
         if n > self.max_tokens:
             raise SchedulerError(f"{n} tokens exceed max_tokens={self.max_tokens}")
-        if hist_t is not None and hist_t.shape[1] != self.tables.ngram_n:
-            pass  # like the vectorised reference, any history width is accepted
+        # like the vectorised reference, any history width is accepted (a row
+        # code outside the n-gram table raises IndexError via the error flag)
         sp = N.stream_ptr(stream)
         hp = N.ptr(hist_t)
         if stages is None:
