@@ -21,7 +21,7 @@ def test_reference_arm_json_line():
     assert r.returncode == 0, r.stderr
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference"
-    assert line["metric"] == "moe_layer_tokens_per_sec" and line["higher_is_better"] is True
+    assert line["metric"] == "MoE-layer tokens/sec" and line["higher_is_better"] is True
     assert line["e2e"]["value"] == line["value"]
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     cb = line["cpu_baseline"]
