@@ -26,6 +26,12 @@
 #include <algorithm>
 #include <cstdlib>
 
+// Ring depth of the SM-pair variant (compile-time; profiles/r1_gemm_l2/
+// cg2_ring_depth_scan.csv: 4 stages read ~algorithmic DRAM bytes at higher
+// clocks but lower tensor-pipe occupancy, 6 the reverse; within +-2% in time).
+#ifndef SMOE_CG2_STAGES
+#define SMOE_CG2_STAGES 6
+#endif
 namespace smoe {
 
 constexpr int kThreads = 256;
@@ -39,7 +45,7 @@ constexpr uint32_t kStagingBytes = 4 * 32 * 64;        // 4 epilogue warps x 32 
 template <int CG> struct GemmShape {
   static constexpr uint32_t kBBytes = (kGemmBN / CG) * kGemmBK * 2;   // B rows staged per CTA
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = CG == 1 ? 4 : 6;
+  static constexpr int kStages = CG == 1 ? 4 : SMOE_CG2_STAGES;
   static constexpr int kTileM = kGemmBM * CG;
   static constexpr size_t kSmem = 1024 + kStages * kStageBytes + kStagingBytes + 1024 +
                                   kGemmMaxProblems * 32 + 4 * (kGemmMaxProblems + 1);
