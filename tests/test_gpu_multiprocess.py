@@ -25,7 +25,8 @@ def free_port():
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("world,over", [(2, {"G": 2, "N": 8}), (2, {"G": 4, "N": 16})])
+@pytest.mark.parametrize("world,over", [(2, {"G": 2, "N": 8}), (2, {"G": 4, "N": 16}),
+                                        (4, {"G": 8, "N": 16}), (8, {"G": 8, "N": 16})])
 def test_two_process_layer_matches_single_process(world, over):
     n = 300
     ctx = mp.get_context("spawn")
@@ -59,11 +60,11 @@ def test_two_process_layer_matches_single_process(world, over):
 
 
 @pytest.mark.timeout(600)
-def test_two_process_forward_async_matches_single_process():
+@pytest.mark.parametrize("world,over", [(2, {"G": 4, "N": 16}), (4, {"G": 8, "N": 16})])
+def test_multi_process_forward_async_matches_single_process(world, over):
     """Pipelined serving across processes: double-buffered peer-visible
     partial slots, fresh inputs per batch; every batch equals the
     single-process synchronous forward bit for bit."""
-    world, over = 2, {"G": 4, "N": 16}
     sizes = (300, 257, 300, 12, 299)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
