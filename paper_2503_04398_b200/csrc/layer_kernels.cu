@@ -816,7 +816,7 @@ __device__ __forceinline__ void combine_span(char* const (&dst_base)[G], const c
     }
     const uint4 o = pack_bf16x8(a);
 #pragma unroll
-    for (int r = 0; r < G; ++r) st_v4(dst_base[r] + (i * d + v * 8) * 2, o);
+    for (int r = 0; r < G; ++r) st_cs_v4(dst_base[r] + (i * d + v * 8) * 2, o);
   }
 }
 
