@@ -266,10 +266,10 @@ class SpecMoELayer:
         (every stage, one graph launch) on whatever the bound partial buffers,
         `tokens_t` and `hist_t` hold at replay time; the token count is fixed
         at capture.  For small (decode-sized) batches, where the ten kernel
-        launches of `run_device` cost as much as the work."""
+        launches of `run_device` cost as much as the work.  With a ShardGroup
+        every process captures and replays in lockstep: the signal-pad barriers
+        count epochs in device memory, so replays stay ordered across processes."""
         t = _dev.torch()
-        if self.group is not None:
-            raise SchedulerError("graph capture is single-process only (peer barriers spin)")
         s = t.cuda.Stream()
         s.wait_stream(t.cuda.current_stream())
         with t.cuda.stream(s):                  # warm-up off the capture (lazy attributes)

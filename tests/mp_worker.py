@@ -63,3 +63,37 @@ def async_worker(rank, world, port, cfg_over, sizes, result_q):
         grp.close()
     finally:
         dist.destroy_process_group()
+
+
+def capture_worker(rank, world, port, cfg_over, seeds, n, result_q):
+    """CUDA-graph capture of a multi-process layer; replays with new partials."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2503_04398_b200 import SpecMoELayer, synth
+        from paper_2503_04398_b200.dist import ShardGroup
+        ws = [synth.make_workload("toy", n=n, eps=0.3, seed=s, cfg_override=cfg_over) for s in seeds]
+        base = ws[0]
+        grp = ShardGroup.from_torch_distributed()
+        layer = SpecMoELayer(base.bundle, base.gate_w, base.w1, base.w3, base.w2,
+                             top_k=base.cfg["k"], max_tokens=n, group=grp)
+        L, b0 = layer.shard_count, layer.shard_begin
+        tok = torch.as_tensor(base.tokens, device="cuda")
+        hist = torch.as_tensor(base.hist, device="cuda")
+        layer.partial_views(n).copy_(torch.from_numpy(base.partials[b0:b0 + L]))
+        g = layer.capture(tok, hist)
+        got = []
+        for w in ws:
+            layer.partial_views(n).copy_(torch.from_numpy(w.partials[b0:b0 + L]))
+            g.replay()
+            torch.cuda.synchronize()
+            layer.check_errors()
+            got.append(layer.out_view(n).float().cpu().numpy())
+        result_q.put((rank, got))
+        dist.barrier()
+        grp.close()
+    finally:
+        dist.destroy_process_group()

@@ -90,3 +90,33 @@ def test_multi_process_forward_async_matches_single_process(world, over):
                                  w.hist).float().numpy()
         for r in range(world):
             assert np.array_equal(res[r][i], want), (r, i)
+
+
+@pytest.mark.timeout(600)
+def test_two_process_graph_capture():
+    """Both processes capture the layer as a CUDA graph and replay it with new
+    partials (same tokens): every replay equals the single-process forward."""
+    world, over, n, seeds = 2, {"G": 4, "N": 16}, 200, (41, 42, 43)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=mp_worker.capture_worker, args=(r, world, port, over, seeds, n, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, got = q.get(timeout=540)
+        res[r] = got
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ws = [synth.make_workload("toy", n=n, eps=0.3, seed=s, cfg_override=over) for s in seeds]
+    base = ws[0]
+    ref_layer = SpecMoELayer(base.bundle, base.gate_w, base.w1, base.w3, base.w2,
+                             top_k=base.cfg["k"], max_tokens=n)
+    for i, w in enumerate(ws):
+        want = ref_layer.forward(torch.from_numpy(w.partials).to(torch.bfloat16), base.tokens,
+                                 base.hist).float().numpy()
+        for r in range(world):
+            assert np.array_equal(res[r][i], want), (r, i)
