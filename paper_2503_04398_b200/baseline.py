@@ -59,22 +59,35 @@ class DSMoELayer:
             self.w13[r] = packed
             self.w2[r] = _dev.to_device(w2[sl] if not isinstance(w2, t.Tensor) else w2[sl],
                                         t.bfloat16).contiguous()
+        # the local ranks' experts stacked in rank order: one grouped GEMM covers
+        # every resident rank (as SpecMoELayer does for its resident shards)
+        self.w13_all = t.cat([self.w13[r] for r in self.local_ranks]).contiguous()
+        self.w2_all = t.cat([self.w2[r] for r in self.local_ranks]).contiguous()
+        self.w13 = {r: self.w13_all[i * self.npc:(i + 1) * self.npc]
+                    for i, r in enumerate(self.local_ranks)}
+        self.w2 = {r: self.w2_all[i * self.npc:(i + 1) * self.npc]
+                   for i, r in enumerate(self.local_ranks)}
         n, k, d = self.max_tokens, self.k, self.d
         cap = n * k
+        self.cap = cap
+        L = len(self.local_ranks)
+        self.recv_all = t.empty((L, cap, d), dtype=t.bfloat16, device=dev)
+        self.hmid_all = t.empty((L, cap, self.f), dtype=t.bfloat16, device=dev)
+        self.yrecv_all = t.empty((L, cap, d), dtype=t.bfloat16, device=dev)
         self.buf = {r: {"hs": t.empty((n, d), dtype=t.bfloat16, device=dev),
                         "ids": t.empty((n, k), dtype=t.int32, device=dev),
                         "w": t.empty((n, k), dtype=t.float32, device=dev),
                         "pos": t.empty((n, k), dtype=t.int32, device=dev),
                         "cnt": t.zeros(self.N, dtype=t.int32, device=dev),
                         "send": t.empty((cap, d), dtype=t.bfloat16, device=dev),
-                        "recv": t.empty((cap, d), dtype=t.bfloat16, device=dev),
-                        "hmid": t.empty((cap, self.f), dtype=t.bfloat16, device=dev),
-                        "yrecv": t.empty((cap, d), dtype=t.bfloat16, device=dev),
+                        "recv": self.recv_all[i],
+                        "hmid": self.hmid_all[i],
+                        "yrecv": self.yrecv_all[i],
                         "yback": t.empty((cap, d), dtype=t.bfloat16, device=dev),
                         "out": t.empty((n, d), dtype=t.bfloat16, device=dev)}
-                    for r in self.local_ranks}
+                    for i, r in enumerate(self.local_ranks)}
         self.stats_t = t.zeros(N.STAT_COUNT, dtype=t.int64, device=dev)
-        self.problems = {r: t.zeros((256, 4), dtype=t.int64, device=dev) for r in self.local_ranks}
+        self.problems = t.zeros((512, 4), dtype=t.int64, device=dev)
         self.last = {}
 
     # ------------------------------------------------------------ collectives
@@ -85,10 +98,24 @@ class DSMoELayer:
             h = partials[0].clone()
             dist.all_reduce(h, group=self.pg)
             return {self.rank: h}
-        s = partials[0].float()
-        for p in partials[1:]:
-            s += p.float()
-        h = s.to(t.bfloat16)
+        import ctypes as C
+        n = int(partials[0].shape[0])
+        dev = partials[0].device
+        h = t.empty_like(partials[0])
+        if n:
+            # reduce: fp32 sum of the G partials in rank order (the SRS kernel with
+            # every token in one group = a plain sum), then the all-gather half:
+            # every rank receives the full sum
+            fwd = t.arange(n, dtype=t.int64, device=dev)
+            counts = t.zeros(self.G, dtype=t.int32, device=dev)
+            counts[0] = n
+            grp = t.full((1,), n, dtype=t.int64, device=dev)
+            parts = [p.contiguous() for p in partials]
+            pa = (C.c_void_p * self.G)(*[N.ptr(p) for p in parts])
+            po = (C.c_void_p * 1)(N.ptr(h))
+            N.check(self.lib.smoe_srs(C.cast(pa, C.c_void_p), self.G, 0, 1, N.ptr(fwd),
+                                      N.ptr(counts), N.ptr(grp), n, self.d,
+                                      C.cast(po, C.c_void_p), N.stream_ptr()), "all_reduce")
         return {r: h.clone() for r in self.local_ranks}        # every rank holds the sum
 
     def _gather_counts(self):
@@ -175,26 +202,30 @@ class DSMoELayer:
         recv = {o: [send[r][o] for r in range(G)] for o in range(G)}
         # 8. dispatch all-to-all
         self._all_to_all("send", "recv", send, recv)
-        # 9. experts: one grouped GEMM per rank, problems = (source rank, local expert)
-        for o in self.local_ranks:
-            b = self.buf[o]
-            probs, off = [], 0
+        # 9. experts: ONE grouped GEMM over every local rank, problems =
+        #    (local rank o, source rank r, expert of o) in o's source-major rows
+        probs = []
+        for i, o in enumerate(self.local_ranks):
+            off = 0
             for r in range(G):
                 for e in range(o * npc, (o + 1) * npc):
                     m = int(C[r, e])
-                    probs.append([off, m, e - o * npc, off])
+                    probs.append([i * self.cap + off, m, i * npc + (e - o * npc),
+                                  i * self.cap + off])
                     off += m
-            rows_in = off
-            self.problems[o][: len(probs)].copy_(t.as_tensor(probs, dtype=t.int64))
-            if rows_in:
-                N.check(L.smoe_grouped_gemm(N.ptr(b["recv"]), b["recv"].shape[0], d,
-                                            N.ptr(self.w13[o]), npc * 2 * self.f, 2 * self.f,
-                                            N.ptr(self.problems[o]), len(probs), 1, N.ptr(b["hmid"]),
-                                            b["hmid"].shape[0], self.f, sp), "gemm_up")
-                N.check(L.smoe_grouped_gemm(N.ptr(b["hmid"]), b["hmid"].shape[0], self.f,
-                                            N.ptr(self.w2[o]), npc * d, d, N.ptr(self.problems[o]),
-                                            len(probs), 0, N.ptr(b["yrecv"]), b["yrecv"].shape[0],
-                                            d, sp), "gemm_down")
+        if len(probs) > self.problems.shape[0]:
+            raise ValueError("too many (rank, source, expert) problems for one launch")
+        if probs:
+            self.problems[: len(probs)].copy_(t.as_tensor(probs, dtype=t.int64))
+            La = len(self.local_ranks)
+            N.check(L.smoe_grouped_gemm(N.ptr(self.recv_all), La * self.cap, d,
+                                        N.ptr(self.w13_all), La * npc * 2 * self.f, 2 * self.f,
+                                        N.ptr(self.problems), len(probs), 1,
+                                        N.ptr(self.hmid_all), La * self.cap, self.f, sp), "gemm_up")
+            N.check(L.smoe_grouped_gemm(N.ptr(self.hmid_all), La * self.cap, self.f,
+                                        N.ptr(self.w2_all), La * npc * d, d, N.ptr(self.problems),
+                                        len(probs), 0, N.ptr(self.yrecv_all), La * self.cap, d,
+                                        sp), "gemm_down")
         # 10. combine all-to-all (reverse splits)
         self._all_to_all("yrecv", "yback", recv, send)
         # 11. weighted combine of the k expert outputs

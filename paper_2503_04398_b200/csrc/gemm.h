@@ -16,7 +16,7 @@ enum GemmEpilogue : int32_t {
 constexpr int kGemmBM = 128;
 constexpr int kGemmBN = 256;
 constexpr int kGemmBK = 64;
-constexpr int kGemmMaxProblems = 256;
+constexpr int kGemmMaxProblems = 512;
 constexpr int64_t kMetaSlotMask = (int64_t(1) << 40) - 1;
 
 struct GemmArgs {
