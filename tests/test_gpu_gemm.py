@@ -133,3 +133,29 @@ def test_small_batch_down_gemm_single_sm_matches_pair():
     finally:
         N.check(lib.smoe_set_option(N.OPT_GEMM_PAIR_MIN_ROWS, old), "opt")
     assert torch.equal(outs[0], outs[1])
+
+
+def test_grouped_512_problems_and_limit():
+    """The problem table holds up to 512 problems (DS-MoE batches every
+    emulated rank's (source, expert) segments into one launch); 513 is
+    rejected before any device work."""
+    torch.manual_seed(7)
+    K, NB, E = 128, 256, 16
+    rng = np.random.default_rng(0)
+    ms = rng.integers(0, 9, size=512)
+    offs = np.concatenate([[0], np.cumsum(ms)])[:-1]
+    A = torch.randn(int(ms.sum()) + 8, K, device="cuda").to(torch.bfloat16)
+    B = torch.randn(E * NB, K, device="cuda").to(torch.bfloat16)
+    probs = [[int(offs[p]), int(ms[p]), p % E, int(offs[p])] for p in range(512)]
+    C = run_gemm(A, B, probs, NB, 0, NB)
+    ref = torch.zeros_like(C, dtype=torch.float32)
+    for p in range(512):
+        if ms[p]:
+            e = p % E
+            ref[offs[p]:offs[p] + ms[p]] = A[offs[p]:offs[p] + ms[p]].float() @ \
+                B[e * NB:(e + 1) * NB].float().T
+    assert rel(C[: int(ms.sum())], ref[: int(ms.sum())]) < 1e-2
+    lib = N.lib()
+    pt = torch.zeros((513, 4), dtype=torch.int64, device="cuda")
+    assert lib.smoe_grouped_gemm(N.ptr(A), A.shape[0], K, N.ptr(B), B.shape[0], NB, N.ptr(pt),
+                                 513, 0, N.ptr(C), C.shape[0], NB, N.stream_ptr()) != N.OK
