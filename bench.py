@@ -52,6 +52,7 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-dsmoe", action="store_true", help="skip the DS-MoE baseline timing")
+    p.add_argument("--no-decode", action="store_true", help="skip the 64-token decode timing")
     return p.parse_args()
 
 
@@ -402,6 +403,32 @@ def main():
                "api": "SpecMoELayer.forward_async (pinned host partials/ids/hist in, host "
                       "output out; H2D, layer and D2H of neighbouring steps overlap)"}
 
+    # ---------------- decode-sized batch on the same layer (serving latency)
+    # 64 tokens, the whole layer replayed from a CUDA graph (single process);
+    # the layer has already run full batches, as a serving loop would have
+    decode = None
+    if world == 1 and not args.no_decode:
+        nd = min(64, n)
+        tok_d, hist_d = tok[:nd].clone(), hist[:nd].clone()
+        g = layer.capture(tok_d, hist_d)
+        for _ in range(5):
+            g.replay()
+        torch.cuda.synchronize()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 50
+        d0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        d1.record(stream)
+        torch.cuda.synchronize()
+        layer.check_errors()
+        us = d0.elapsed_time(d1) / reps * 1e3
+        w_bytes = 2.0 * 3 * cfg["N"] * d * f          # every expert's weights, bf16
+        decode = {"tokens": nd, "us_per_step": us, "tokens_per_s": nd / (us / 1e6),
+                  "weight_stream_roofline_us": w_bytes / (pk["hbm"] * 1e3),
+                  "mode": "CUDA-graph replay of the whole layer (SpecMoELayer.capture)"}
+        del g
+
     # ---------------- DS-MoE pipeline baseline (AR -> A2A -> A2A -> AG), same kernels
     dsm = None
     if not args.no_dsmoe and world in (1, G):
@@ -480,7 +507,8 @@ def main():
                            "peak_src": pk["src"] + " sustained",
                            "down_gemm_tflops": down_flops / (down_ms / 1e3) / 1e12,
                            "layer_tflops": (up_flops + down_flops) / (ms_step / 1e3) / 1e12},
-              "e2e": e2e, "cpu_baseline": cpu, "dsmoe_baseline": dsm, "clocks": clocks,
+              "e2e": e2e, "cpu_baseline": cpu, "dsmoe_baseline": dsm, "decode": decode,
+              "clocks": clocks,
               "gpu_launches": launches_per_step * args.steps})
     if world > 1:
         torch.distributed.destroy_process_group()
