@@ -312,7 +312,9 @@ int smoe_combine_rows(const void* y, const int32_t* pair_pos, const float* topk_
  *  Standalone SRS / SAG collectives (the paper's drop-in replacements for  *
  *  reduce-scatter and all-gather, Algorithm 2)               *
  * ======================================================================= */
-/* Shuffled reduce-scatter over n_shards partial buffers (every partial
+/* Shuffled reduce-scatter (reduce-scatter priced at comm.py:83-84, fused with
+ * the rebatch_tokens permutation scheduler.py:119-149) over n_shards partial
+ * buffers (every partial
  * [n_tokens, hidden] bf16, all addressable from this GPU: local or peer):
  *   outs[g - shard_begin][j, :] = bf16( sum_{r < n_shards} partials[r][forward[g*group + j], :] )
  * for every shard g in [shard_begin, shard_begin + shard_count) and
@@ -324,7 +326,8 @@ int smoe_srs(const void* const* partials, int32_t n_shards, int32_t shard_begin,
              const int64_t* group, int64_t n_tokens, int32_t hidden, void* const* outs,
              void* stream);
 
-/* Shuffled all-gather (resume fused with the all-gather): for every shard g,
+/* Shuffled all-gather (resume_tokens, scheduler.py:152-157, fused with the
+ * all-gather the reference prices at comm.py:83-84): for every shard g,
  * row j < counts[g] of blocks[g] ([group, hidden] bf16) is stored at the
  * token's original position forward[g*group + j] of every outs[o]
  * ([n_tokens, hidden], o < n_outs).  blocks / outs are HOST arrays of device
