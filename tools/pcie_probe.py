@@ -99,6 +99,24 @@ def main():
                                      0, d.data_ptr(), err.data_ptr(), N.stream_ptr()), "gather")
     res["h2d_zero_copy_kernel"] = nb / timed(lambda: zc(h)) / 1e9
     res["d2d_gather_kernel"] = 2 * nb / timed(lambda: zc(d2)) / 1e9
+    # DMA engine and a zero-copy kernel sharing one H2D transfer (half each,
+    # concurrently): does the link carry more than either alone?
+    half = nb // 2
+    rows_h = half // row
+    idx_h = torch.arange(rows_h, dtype=torch.int64, device="cuda")
+    s_dma = torch.cuda.Stream()
+
+    def split_dma_kernel():
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        s_dma.wait_event(ev)
+        with torch.cuda.stream(s_dma):
+            d[:half].copy_(h[:half], non_blocking=True)
+        N.check(lib.smoe_gather_rows(h[half:].data_ptr(), rows_h, 2, row // 2, idx_h.data_ptr(),
+                                     rows_h, 1, 0, d[half:].data_ptr(), err.data_ptr(),
+                                     N.stream_ptr()), "gather")
+        cur.wait_stream(s_dma)
+    res["h2d_dma_plus_zero_copy"] = nb / timed(split_dma_kernel) / 1e9
     res["bytes"] = nb
     print(json.dumps({k: (round(v, 2) if isinstance(v, float) else v) for k, v in res.items()}))
 
