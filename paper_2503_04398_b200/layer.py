@@ -535,16 +535,22 @@ class MicroBatchedSpecMoE:
 
     Every token's result is independent of how the batch is cut, so the
     output is bit-identical to `SpecMoELayer`.  The micro-batch layers share
-    the packed weights and write their partial inputs / outputs / next-layer
-    histories through views of one full-size buffer (no copies).
-    Single-process (all shards resident) only.
+    the packed weights.  Single process: they write their partial inputs /
+    outputs / next-layer histories through views of one full-size buffer (no
+    copies).  With a ShardGroup each micro-batch layer has its own
+    peer-visible (CUDA IPC) buffers and barrier epochs, every process builds
+    the same micro-batches in the same order, and `forward` scatters the
+    partials into them and gathers the outputs.
+
+    On one GPU this is slower (the power cap); it exists for the
+    multi-GPU case, where SRS / SAG are NVLink-bound and can overlap the
+    power-bound GEMMs of the neighbouring micro-batch.
     """
 
     def __init__(self, bundle, gate_w, w1, w3, w2, *, top_k: int, max_tokens: int,
                  microbatches: int = 2, **kw):
         t = _dev.torch()
-        if kw.get("group") is not None:
-            raise SchedulerError("micro-batching needs all shards in this process")
+        self.group = kw.get("group")
         self.M = int(microbatches)
         self.max_tokens = int(max_tokens)
         self.chunk = -(-self.max_tokens // self.M)
@@ -555,6 +561,11 @@ class MicroBatchedSpecMoE:
         G, d = first.G, first.d
         dev = first.w_gate.device
         self.G, self.d = G, d
+        self.shard_count, self.shard_begin = first.shard_count, first.shard_begin
+        self.streams = [t.cuda.current_stream()] + [t.cuda.Stream() for _ in range(self.M - 1)]
+        self.events = [t.cuda.Event() for _ in range(self.M)]
+        if self.group is not None:
+            return                       # every micro-batch layer keeps its own IPC buffers
         self.partial = t.zeros((G, self.max_tokens, d), dtype=t.bfloat16, device=dev)
         self.out = t.empty((G, self.max_tokens, d), dtype=t.bfloat16, device=dev)
         h = max(first.tables.ngram_n, 1)
@@ -570,17 +581,58 @@ class MicroBatchedSpecMoE:
                 N.check(L.lib.smoe_layer_bind(L._h, N.BUF_OUT, g, N.ptr(self.out[g, lo:])), "bind")
                 N.check(L.lib.smoe_layer_bind(L._h, N.BUF_HIST_OUT, g,
                                               N.ptr(self.hist_next[lo:])), "bind")
-        self.streams = [t.cuda.current_stream()] + [t.cuda.Stream() for _ in range(self.M - 1)]
-        self.events = [t.cuda.Event() for _ in range(self.M)]
+
+    def _pieces(self, n: int):
+        out = []
+        for c, L in enumerate(self.layers):
+            lo = c * self.chunk
+            hi = min(n, lo + self.chunk)
+            if hi > lo:
+                out.append((c, L, lo, hi))
+        return out
 
     def partial_views(self, n: int):
+        if self.group is not None:
+            raise SchedulerError("with a ShardGroup each micro-batch has its own partial "
+                                 "buffer: use forward() or load_partials()")
         return self.partial[:, :n]
 
+    def load_partials(self, partials):
+        """Copy this process's [L, n, d] partials into the micro-batch buffers."""
+        n = int(partials.shape[1])
+        for c, L, lo, hi in self._pieces(n):
+            L.partial_views(hi - lo).copy_(partials[:, lo:hi], non_blocking=True)
+
     def out_view(self, n: int, shard: int = 0):
+        if self.group is not None:
+            t = _dev.torch()
+            return t.cat([L.out_view(hi - lo) for c, L, lo, hi in self._pieces(n)])
         return self.out[shard, :n]
 
     def next_history(self, n: int):
+        if self.group is not None:
+            t = _dev.torch()
+            return t.cat([L.next_history(hi - lo) for c, L, lo, hi in self._pieces(n)])
         return self.hist_next[:n]
+
+    def forward(self, hidden_partials, token_ids, histories=None):
+        """[L, n, d] partials (device or host), token ids [n], histories
+        [n, h]: the layer output [n, d] on the device."""
+        t = _dev.torch()
+        dev = self.layers[0].w_gate.device
+        hp = t.as_tensor(hidden_partials)
+        if hp.dim() == 2:
+            hp = hp.unsqueeze(0)
+        tok = t.as_tensor(token_ids).to(device=dev, dtype=t.int64)
+        hist = None if histories is None else t.as_tensor(histories).to(device=dev,
+                                                                         dtype=t.int64)
+        if self.group is None:
+            self.partial_views(int(tok.numel())).copy_(hp)
+        else:
+            self.load_partials(hp.to(device=dev, dtype=t.bfloat16))
+        out = self.run_device(tok, hist)
+        self.check_errors()
+        return out
 
     def run_device(self, tokens_t, hist_t=None):
         """All micro-batches of one forward; returns the output view.  The
@@ -595,13 +647,7 @@ class MicroBatchedSpecMoE:
         for s in self.streams[1:]:
             s.wait_stream(main)
         pre = [N.STAGE_PLAN, N.STAGE_SRS, N.STAGE_GATE, N.STAGE_ROUTE, N.STAGE_DISPATCH]
-        parts = []
-        for c, L in enumerate(self.layers):
-            lo = c * self.chunk
-            hi = min(n, lo + self.chunk)
-            if hi <= lo:
-                continue
-            parts.append((c, L, lo, hi))
+        parts = self._pieces(n)
         for c, L, lo, hi in parts:                    # movers of every micro-batch first
             h = None if hist_t is None else hist_t[lo:hi]
             L.run_device(tokens_t[lo:hi], h, stream=self.streams[c], stages=pre)

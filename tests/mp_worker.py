@@ -97,3 +97,31 @@ def capture_worker(rank, world, port, cfg_over, seeds, n, result_q):
         grp.close()
     finally:
         dist.destroy_process_group()
+
+
+def microbatch_worker(rank, world, port, cfg_over, n, M, result_q):
+    """MicroBatchedSpecMoE across processes: per-micro-batch IPC buffers."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2503_04398_b200 import synth
+        from paper_2503_04398_b200.dist import ShardGroup
+        from paper_2503_04398_b200.layer import MicroBatchedSpecMoE
+        w = synth.make_workload("toy", n=n, eps=0.3, seed=12, cfg_override=cfg_over)
+        grp = ShardGroup.from_torch_distributed()
+        layer = MicroBatchedSpecMoE(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=w.cfg["k"],
+                                    max_tokens=n, microbatches=M, group=grp)
+        L, b0 = layer.shard_count, layer.shard_begin
+        mine = torch.from_numpy(w.partials[b0:b0 + L])
+        outs = []
+        for _ in range(2):
+            outs.append(layer.forward(mine, w.tokens, w.hist).float().cpu().numpy())
+        hist = layer.next_history(n).cpu().numpy()
+        result_q.put((rank, outs, hist))
+        dist.barrier()
+        grp.close()
+    finally:
+        dist.destroy_process_group()

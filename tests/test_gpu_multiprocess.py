@@ -120,3 +120,35 @@ def test_two_process_graph_capture():
                                  base.hist).float().numpy()
         for r in range(world):
             assert np.array_equal(res[r][i], want), (r, i)
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("M", [2, 3])
+def test_two_process_microbatched_matches_single_process(M):
+    """Micro-batches on their own streams with their own IPC buffers and
+    barrier epochs, across processes: bit-identical outputs and histories."""
+    world, over, n = 2, {"G": 4, "N": 16}, 301
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=mp_worker.microbatch_worker, args=(r, world, port, over, n, M, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, outs, hist = q.get(timeout=540)
+        res[r] = (outs, hist)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    w = synth.make_workload("toy", n=n, eps=0.3, seed=12, cfg_override=over)
+    ref_layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=w.cfg["k"], max_tokens=n)
+    want = ref_layer.forward(torch.from_numpy(w.partials).to(torch.bfloat16), w.tokens,
+                             w.hist).float().numpy()
+    want_hist = ref_layer.next_history(n).cpu().numpy()
+    for r in range(world):
+        outs, hist = res[r]
+        for o in outs:
+            assert np.array_equal(o, want)
+        assert np.array_equal(hist, want_hist)
