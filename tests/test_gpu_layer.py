@@ -361,3 +361,20 @@ def test_batch_invariance_across_cuts():
         assert torch.equal(layer.next_history(size), full_hist[lo:hi])
         lo = hi
     assert lo == n
+
+
+def test_microbatched_forward_api_single_process():
+    """MicroBatchedSpecMoE.forward (host partials in, device output out) equals
+    the plain layer, and its histories are the plain layer's."""
+    from paper_2503_04398_b200.layer import MicroBatchedSpecMoE
+    over = {"G": 4, "N": 16}
+    n = 450
+    w = synth.make_workload("toy", n=n, eps=0.25, seed=61, cfg_override=over)
+    parts = torch.from_numpy(w.partials).to(torch.bfloat16)
+    ref_layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=n)
+    want = ref_layer.forward(parts, w.tokens, w.hist)
+    mb = MicroBatchedSpecMoE(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=n,
+                             microbatches=3)
+    got = mb.forward(parts, w.tokens, w.hist)
+    assert torch.equal(got.cpu(), want.cpu())
+    assert torch.equal(mb.next_history(n), ref_layer.next_history(n))
