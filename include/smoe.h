@@ -218,6 +218,8 @@ enum {
   SMOE_STAT_REMOTE_PAIRS,      /* pairs crossing shards (the A2A events, comm.py:214-216)   */
   SMOE_STAT_SRS_ROWS,          /* rows reduced by SRS (real rows, no pads)                 */
   SMOE_STAT_GROUP,             /* max group (scheduler.py:135)                              */
+  SMOE_STAT_REMOTE_ROWS,       /* distinct (token, other shard) pairs: rows a dispatch that */
+                               /* deduplicates per destination shard would send             */
   SMOE_STAT__COUNT = 16
 };
 

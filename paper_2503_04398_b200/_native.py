@@ -80,7 +80,7 @@ OPT_GEMM_PAIR_MIN_ROWS = 3
  BUF_TOPK_IDS, BUF_TOPK_W, BUF_PAIR_RANK, BUF_HMID, BUF_FORWARD, BUF_INVERSE, BUF_DEV,
  BUF_PLAN_COUNTS, BUF_GROUP, BUF_STATS, BUF_ERR, BUF_WORKSPACE, BUF_PROBLEMS,
  BUF_EPOCH, BUF_HIST_OUT) = range(23)
-STAT_LOCAL_PAIRS, STAT_REMOTE_PAIRS, STAT_SRS_ROWS, STAT_GROUP = range(4)
+STAT_LOCAL_PAIRS, STAT_REMOTE_PAIRS, STAT_SRS_ROWS, STAT_GROUP, STAT_REMOTE_ROWS = range(5)
 STAT_COUNT = 16
 (STAGE_PLAN, STAGE_SRS, STAGE_GATE, STAGE_ROUTE, STAGE_DISPATCH, STAGE_EXPERT_UP,
  STAGE_EXPERT_DOWN, STAGE_COMBINE_SAG) = range(8)

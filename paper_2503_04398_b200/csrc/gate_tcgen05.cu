@@ -190,7 +190,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
     const int ew = warp - 4;
     const int N = a.n_experts, K = a.k;
     uint32_t acc = 0, acc_phase = 0;
-    unsigned long long my_local = 0, my_remote = 0;
+    unsigned long long my_local = 0, my_remote = 0, my_rrows = 0;
     for (int32_t t = blockIdx.x; t < total; t += gridDim.x) {
       int32_t gl, blk;
       decode(t, gl, blk);
@@ -253,7 +253,17 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
         if (s < K) {
           ids[s] = sel_e[s];
           wts[s] = sel_p[s] * scale;
-          if (s_owner[sel_e[s]] == g) ++my_local; else ++my_remote;
+          const int32_t o = s_owner[sel_e[s]];
+          if (o == g) {
+            ++my_local;
+          } else {
+            ++my_remote;
+            bool seen = false;                           // first pair to this shard?
+#pragma unroll
+            for (int s2 = 0; s2 < kGtMaxK; ++s2)
+              if (s2 < s) seen |= s_owner[sel_e[s2]] == o;
+            if (!seen) ++my_rrows;
+          }
         }
       }
     }
@@ -261,11 +271,13 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
     for (int o = 16; o; o >>= 1) {
       my_local += __shfl_xor_sync(0xffffffffu, my_local, o);
       my_remote += __shfl_xor_sync(0xffffffffu, my_remote, o);
+      my_rrows += __shfl_xor_sync(0xffffffffu, my_rrows, o);
     }
     if (lane == 0 && a.stats && (my_local | my_remote)) {
       atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + SMOE_STAT_LOCAL_PAIRS), my_local);
       atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + SMOE_STAT_REMOTE_PAIRS),
                 my_remote);
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + SMOE_STAT_REMOTE_ROWS), my_rrows);
     }
   }
   tc_fence_before();

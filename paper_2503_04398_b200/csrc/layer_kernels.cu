@@ -202,7 +202,7 @@ gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ 
   __shared__ float s_logit[kGateRows * (kGateMaxN + 1)];
   __shared__ int32_t s_gl[kGateRows];
   __shared__ int64_t s_j[kGateRows];
-  __shared__ unsigned long long s_local, s_remote;
+  __shared__ unsigned long long s_local, s_remote, s_rrows;
   load_rowmap(rm, lr);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t words = d / 2;
@@ -214,7 +214,7 @@ gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ 
       s_gl[tid] = gl;
       s_j[tid] = j;
     }
-    if (tid == 0) { s_local = 0; s_remote = 0; }
+    if (tid == 0) { s_local = 0; s_remote = 0; s_rrows = 0; }
     float acc[kGateMaxN * kGateRows / 256];
 #pragma unroll
     for (int i = 0; i < kGateMaxN * kGateRows / 256; ++i) acc[i] = 0.f;
@@ -262,7 +262,7 @@ gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ 
     }
     __syncthreads();
     // top-k + softmax, one warp per row
-    unsigned long long my_local = 0, my_remote = 0;
+    unsigned long long my_local = 0, my_remote = 0, my_rrows = 0;
     for (int r = warp; r < kGateRows; r += 8) {
       const int32_t gl = s_gl[r];
       if (gl < 0) continue;
@@ -304,18 +304,25 @@ gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ 
         for (int s = 0; s < k; ++s) {
           ids[s] = sel_e[s];
           wts[s] = sel_p[s] * scale;
-          if (slot_owner[sel_e[s]] == g) ++my_local; else ++my_remote;
+          const int32_t o = slot_owner[sel_e[s]];
+          if (o == g) { ++my_local; continue; }
+          ++my_remote;
+          bool seen = false;                             // first pair to this shard?
+          for (int s2 = 0; s2 < s; ++s2) seen |= slot_owner[sel_e[s2]] == o;
+          if (!seen) ++my_rrows;
         }
       }
     }
     if (lane == 0 && (my_local | my_remote)) {
       atomicAdd(&s_local, my_local);
       atomicAdd(&s_remote, my_remote);
+      atomicAdd(&s_rrows, my_rrows);
     }
     __syncthreads();
     if (tid == 0 && stats) {
       atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_LOCAL_PAIRS), s_local);
       atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_REMOTE_PAIRS), s_remote);
+      atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_REMOTE_ROWS), s_rrows);
     }
     __syncthreads();
   }
@@ -379,7 +386,7 @@ gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ 
   __shared__ const char* s_row[kMmaRows];
   __shared__ int32_t s_gl[kMmaRows];
   __shared__ int64_t s_j[kMmaRows];
-  __shared__ unsigned long long s_local, s_remote;
+  __shared__ unsigned long long s_local, s_remote, s_rrows;
   load_rowmap(rm, lr);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(gsm));
@@ -394,7 +401,7 @@ gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ 
       s_j[tid] = j;
       s_row[tid] = gl >= 0 ? s_hs[gl] + j * d * 2 : nullptr;
     }
-    if (tid == 0) { s_local = 0; s_remote = 0; }
+    if (tid == 0) { s_local = 0; s_remote = 0; s_rrows = 0; }
     __syncthreads();
     auto load_stage = [&](int kc, int stage) {
       for (int e = tid; e < S * (kMmaRows + N) * 8; e += kMmaThreads) {
@@ -476,7 +483,7 @@ gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ 
       lgs[r * (N + 1) + e] = v;      // split 0's slot: each element read then written by one thread
     }
     __syncthreads();
-    unsigned long long my_local = 0, my_remote = 0;
+    unsigned long long my_local = 0, my_remote = 0, my_rrows = 0;
     for (int r = warp; r < kMmaRows; r += kMmaThreads / 32) {
       const int32_t gl = s_gl[r];
       if (gl < 0) continue;
@@ -517,22 +524,35 @@ gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ 
         const int64_t g = lr.shard_begin + gl;
         reinterpret_cast<int32_t*>(s_ids[gl])[s_j[r] * k + lane] = e;
         reinterpret_cast<float*>(s_wts[gl])[s_j[r] * k + lane] = renorm ? p / psum : p;
-        if (slot_owner[e] == g) ++my_local; else ++my_remote;
+        const int32_t o = slot_owner[e];
+        if (o == g) {
+          ++my_local;
+        } else {
+          ++my_remote;
+          bool seen = false;                             // first pair to this shard?
+#pragma unroll
+          for (int s2 = 0; s2 < kGateMaxK; ++s2)
+            if (s2 < lane) seen |= slot_owner[sel_e[s2]] == o;
+          if (!seen) ++my_rrows;
+        }
       }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       my_local += __shfl_xor_sync(0xffffffffu, my_local, o);
       my_remote += __shfl_xor_sync(0xffffffffu, my_remote, o);
+      my_rrows += __shfl_xor_sync(0xffffffffu, my_rrows, o);
     }
     if (lane == 0 && (my_local | my_remote)) {
       atomicAdd(&s_local, my_local);
       atomicAdd(&s_remote, my_remote);
+      atomicAdd(&s_rrows, my_rrows);
     }
     __syncthreads();
     if (tid == 0 && stats) {
       atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_LOCAL_PAIRS), s_local);
       atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_REMOTE_PAIRS), s_remote);
+      atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_REMOTE_ROWS), s_rrows);
     }
     __syncthreads();
   }

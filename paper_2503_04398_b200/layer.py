@@ -498,6 +498,7 @@ class SpecMoELayer:
         srs_bytes = int(counts.sum()) * (G - 1) * row      # rows pulled from other shards
         sag_bytes = int(counts.sum()) * (G - 1) * row      # rows pushed to other shards
         a2a = remote * row
+        rrows = int(s[N.STAT_REMOTE_ROWS])
         return {
             "local_tokens": local, "remote_tokens": remote,
             "measured_alpha": local / max(local + remote, 1),
@@ -506,7 +507,11 @@ class SpecMoELayer:
             "bytes": {"srs": srs_bytes, "a2a_dispatch": a2a, "a2a_combine": a2a,
                       "sag": sag_bytes,
                       "srs_padded_model": G * group * (G - 1) * row,
-                      "reference_model_a2a": a2a},
+                      "reference_model_a2a": a2a,
+                      # one row per (token, destination shard) instead of one
+                      # per (token, expert): a deduplicating dispatch (not built)
+                      "a2a_dispatch_dedup_model": rrows * row},
+            "remote_rows": rrows,
         }
 
 

@@ -74,6 +74,10 @@ def test_layer_matches_oracle(name, n, eps, over, gate_kernel):
     assert np.allclose(r["weights"], ref["weights"], rtol=1e-4, atol=1e-6)
     st = layer.stats()
     assert st["local_tokens"] == ref["local"] and st["remote_tokens"] == ref["remote"]
+    # rows a per-destination-shard deduplicating dispatch would send
+    owners = np.asarray(w.expert_labels)[ref["experts"]]
+    want_rows = sum(len(set(owners[i].tolist()) - {int(ref["devices"][i])}) for i in range(n))
+    assert st["remote_rows"] == want_rows
     err = np.linalg.norm(out - ref["out"]) / np.linalg.norm(ref["out"])
     assert err <= TOL, err
     # every shard's SAG copy is identical
