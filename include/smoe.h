@@ -58,6 +58,9 @@ const char* smoe_version(void);
                                         /* 0 = mma.sync / CUDA-core kernels          */
 #define SMOE_OPT_GEMM_PAIR_MIN_ROWS  3  /* layer down GEMM: one SM per tile while    */
                                         /* n*k <= this * n_experts (default 64)      */
+#define SMOE_OPT_PDL                 4  /* layer kernels: 1 = programmatic dependent */
+                                        /* launch (default; env SMOE_PDL=0 to start  */
+                                        /* with 0), 0 = plain stream order           */
 int smoe_set_option(int32_t key, int32_t value);
 int smoe_get_option(int32_t key);
 const char* smoe_status_string(int status);

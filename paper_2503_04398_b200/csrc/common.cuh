@@ -26,6 +26,42 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // Number of SMs on the current device (cached per process).
 int num_sms();
 
+// ---- programmatic dependent launch (PDL) --------------------------------
+// Layer-path kernels are launched with programmatic stream serialisation:
+// the next kernel on the stream may start while this one still runs.  Every
+// such kernel calls pdl_enter() (or, after a prologue that touches only
+// constant data — weights, tensor maps, shared memory, TMEM — pdl_trigger()
+// then pdl_wait()) before its first global read or write of data another
+// kernel produces or consumes: griddepcontrol.wait returns once the
+// preceding grid has completed and its writes are visible.  Without the
+// launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_enter() { pdl_trigger(); pdl_wait(); }
+
+int pdl_enabled();                      // SMOE_OPT_PDL (default 1; env SMOE_PDL=0)
+void set_pdl_enabled(int on);
+void set_pdl_stage(int stage);           // layer stage being launched (-1: none)
+
+// <<<grid, block, smem, st>>> with the PDL attribute when enabled.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 __device__ __forceinline__ void set_err(int32_t* err, int32_t bit) {
   if (err) atomicOr(err, bit);
 }

@@ -76,21 +76,6 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
   __shared__ int32_t s_owner[NP];        // cluster of each expert slot (locality count)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    int32_t acc = 0;
-    for (int i = 0; i < a.shard_count; ++i) {
-      const int32_t c = a.counts ? a.counts[a.shard_begin + i] : (i == 0 ? (int32_t)a.single_rows : 0);
-      s_cnt[i] = c;
-      s_prefix[i] = acc;
-      acc += (c + kGtRows - 1) / kGtRows;
-    }
-    s_prefix[a.shard_count] = acc;
-#pragma unroll
-    for (int i = 0; i < SMOE_MAX_SHARDS; ++i) {
-      s_ids[i] = a.topk_ids.p[i];
-      s_wts[i] = a.topk_w.p[i];
-    }
-  }
   if (threadIdx.x < NP) {
     s_bias[threadIdx.x] = (a.b_gate && threadIdx.x < a.n_experts) ? a.b_gate[threadIdx.x] : 0.f;
     // staged once: the epilogue's k owner lookups per row would otherwise be
@@ -116,6 +101,25 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                  :: "r"(smem_addr(&tmem_holder)), "r"(S::kTmemCols) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  // everything above reads constant data only (weights, tensor maps); the
+  // shard row counts come from the plan stage
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    int32_t acc = 0;
+    for (int i = 0; i < a.shard_count; ++i) {
+      const int32_t c = a.counts ? a.counts[a.shard_begin + i] : (i == 0 ? (int32_t)a.single_rows : 0);
+      s_cnt[i] = c;
+      s_prefix[i] = acc;
+      acc += (c + kGtRows - 1) / kGtRows;
+    }
+    s_prefix[a.shard_count] = acc;
+#pragma unroll
+    for (int i = 0; i < SMOE_MAX_SHARDS; ++i) {
+      s_ids[i] = a.topk_ids.p[i];
+      s_wts[i] = a.topk_w.p[i];
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -301,7 +305,7 @@ static int launch_cfg(const CUtensorMap& mh, const CUtensorMap& mw, const GateTc
   }
   const int64_t tiles = ceil_div(n_rows_bound, kGtRows) + a.shard_count;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms()));
-  gate_tc_kernel<NP, SUB, ST><<<grid, kGtThreads, S::kSmem, st>>>(mh, mw, a);
+  SMOE_CUDA_TRY(launch_pdl(gate_tc_kernel<NP, SUB, ST>, grid, kGtThreads, S::kSmem, st, mh, mw, a));
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }

@@ -127,26 +127,13 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t np = args.num_problems;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;     // CTA rank inside the SM pair
+  // CTA -> tile assignment follows blockIdx: the launch order places
+  // consecutive CTAs on the two SMs of a TPC, then round-robin over GPCs, so
+  // the CTAs sharing a weight tile are spread over the chip.  Mapping by
+  // %smid instead (or launching this kernel early via PDL, which scrambles
+  // the placement) costs 5-10% (profiles/r1_pdl/).
   const int32_t unit = blockIdx.x / CG, n_units = gridDim.x / CG;
 
-  // ---- problem table -> shared, tile prefix
-  for (int p = threadIdx.x; p < np; p += kThreads) {
-    const int64_t* q = args.problems + 4 * p;
-    sp.a_off[p] = q[0];
-    sp.m[p] = (int32_t)q[1];
-    sp.b_idx[p] = (int32_t)q[2];
-    sp.c_off[p] = q[3];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t acc = 0;
-    for (int p = 0; p < np; ++p) {
-      sp.tile_prefix[p] = acc;
-      const int32_t m = sp.m[p] > 0 ? sp.m[p] : 0;
-      acc += ((m + kTileM - 1) / kTileM) * args.n_tiles_n;
-    }
-    sp.tile_prefix[np] = acc;
-  }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(smem_addr(&bars[s]), 1);
@@ -172,6 +159,28 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                    :: "r"(smem_addr(tmem_holder)), "r"(kTmemCols) : "memory");
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
     }
+  }
+  // everything above touches constant data only (weights, tensor maps, smem,
+  // TMEM); the problem table is written by the dispatch stage
+  pdl_trigger();
+  pdl_wait();
+  // ---- problem table -> shared, tile prefix
+  for (int p = threadIdx.x; p < np; p += kThreads) {
+    const int64_t* q = args.problems + 4 * p;
+    sp.a_off[p] = q[0];
+    sp.m[p] = (int32_t)q[1];
+    sp.b_idx[p] = (int32_t)q[2];
+    sp.c_off[p] = q[3];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t acc = 0;
+    for (int p = 0; p < np; ++p) {
+      sp.tile_prefix[p] = acc;
+      const int32_t m = sp.m[p] > 0 ? sp.m[p] : 0;
+      acc += ((m + kTileM - 1) / kTileM) * args.n_tiles_n;
+    }
+    sp.tile_prefix[np] = acc;
   }
   tc_fence_before();
   if (CG == 2) cluster_sync(); else __syncthreads();
@@ -416,20 +425,22 @@ static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
   }
   const int grid = (num_sms() / CG) * CG;
   if (CG == 1) {
-    grouped_gemm_kernel<EPI, 1><<<grid, kThreads, S::kSmem, st>>>(a, b, g);
+    SMOE_CUDA_TRY(launch_pdl(grouped_gemm_kernel<EPI, 1>, grid, kThreads, S::kSmem, st, a, b, g));
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = S::kSmem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     SMOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<EPI, 2>, a, b, g));
   }
   SMOE_LAUNCH_CHECK();

@@ -280,8 +280,19 @@ extern "C" int smoe_layer_barrier(smoe_layer* L, void* stream) {
                         static_cast<uint32_t*>(L->buf[SMOE_BUF_EPOCH][0]), as_stream(stream));
 }
 
+static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
+                       const int64_t* hist, int64_t n, void* stream);
+
 extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
                                 const int64_t* hist, int64_t n, void* stream) {
+  set_pdl_stage(stage);
+  const int rc = layer_stage(L, stage, tokens, hist, n, stream);
+  set_pdl_stage(-1);
+  return rc;
+}
+
+static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
+                       const int64_t* hist, int64_t n, void* stream) {
   if (!L || n < 0 || n > L->cfg.max_tokens) return SMOE_ERR_INVALID_ARG;
   int rc = ensure_maps(L);
   if (rc) return rc;
@@ -472,6 +483,10 @@ extern "C" int smoe_set_option(int32_t key, int32_t value) {
       if (value < 0) return SMOE_ERR_INVALID_ARG;
       set_gemm_pair_min_rows(value);
       return SMOE_OK;
+    case SMOE_OPT_PDL:
+      if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
+      set_pdl_enabled(value);
+      return SMOE_OK;
     default:
       return SMOE_ERR_INVALID_ARG;
   }
@@ -482,6 +497,7 @@ extern "C" int smoe_get_option(int32_t key) {
   if (key == SMOE_OPT_GEMM_CTA_GROUP_DOWN) return gemm_cta_group(1);
   if (key == SMOE_OPT_GATE_TENSOR) return gate_tc_enabled();
   if (key == SMOE_OPT_GEMM_PAIR_MIN_ROWS) return gemm_pair_min_rows();
+  if (key == SMOE_OPT_PDL) return pdl_enabled();
   return -1;
 }
 

@@ -125,6 +125,7 @@ __device__ __forceinline__ void srs_span(const char* const (&src_base)[G], int64
 template <int G>
 __global__ void __launch_bounds__(256)
 srs_kernel(LocalRows lr, ShardPtrs partials, int64_t d, ShardPtrs hs, int32_t whole_rows) {
+  pdl_enter();
   __shared__ RowMap rm;
   __shared__ char* s_hs[SMOE_MAX_SHARDS];
   stage_ptrs(s_hs, hs);
@@ -165,7 +166,7 @@ int launch_srs(const LocalRows& lr, const ShardPtrs& partials, int64_t d, const 
   const int32_t wr = whole_rows_from();
   switch (lr.n_shards) {
 #define SMOE_SRS_CASE(G_) \
-    case G_: srs_kernel<G_><<<grid, 256, 0, st>>>(lr, partials, d, hs, wr); break;
+    case G_: SMOE_CUDA_TRY(launch_pdl(srs_kernel<G_>, grid, 256, 0, st, lr, partials, d, hs, wr)); break;
     SMOE_SRS_CASE(1) SMOE_SRS_CASE(2) SMOE_SRS_CASE(3) SMOE_SRS_CASE(4) SMOE_SRS_CASE(5)
     SMOE_SRS_CASE(6) SMOE_SRS_CASE(7) SMOE_SRS_CASE(8) SMOE_SRS_CASE(9) SMOE_SRS_CASE(10)
     SMOE_SRS_CASE(11) SMOE_SRS_CASE(12) SMOE_SRS_CASE(13) SMOE_SRS_CASE(14) SMOE_SRS_CASE(15)
@@ -190,6 +191,7 @@ gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ 
             const float* __restrict__ b_gate, int32_t N, int32_t k, int32_t renorm,
             const int32_t* __restrict__ slot_owner, ShardPtrs topk_ids, ShardPtrs topk_w,
             int64_t* stats) {
+  pdl_enter();
   __shared__ RowMap rm;
   __shared__ char* s_hs[SMOE_MAX_SHARDS];
   __shared__ char* s_ids[SMOE_MAX_SHARDS];
@@ -368,6 +370,7 @@ gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ 
                 const float* __restrict__ b_gate, int32_t k, int32_t renorm,
                 const int32_t* __restrict__ slot_owner, ShardPtrs topk_ids, ShardPtrs topk_w,
                 int64_t* stats) {
+  pdl_enter();
   constexpr int N = NT * 8;
   constexpr int S = mma_splits(NT);
   constexpr int kMmaRows = kMmaRowsCTA;
@@ -572,8 +575,8 @@ static int launch_gate_mma(const LocalRows& lr, const ShardPtrs& hs, int64_t d, 
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  gate_mma_kernel<NT><<<grid_cap(ceil_div(n_rows_bound, rows), 4), 128 * S, smem, st>>>(
-      lr, hs, d, static_cast<const char*>(w), b, k, renorm, owner, ids, wts, stats);
+  SMOE_CUDA_TRY(launch_pdl(gate_mma_kernel<NT>, grid_cap(ceil_div(n_rows_bound, rows), 4), 128 * S, smem, st,
+      lr, hs, d, static_cast<const char*>(w), b, k, renorm, owner, ids, wts, stats));
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }
@@ -593,9 +596,9 @@ int launch_gate(const LocalRows& lr, const ShardPtrs& hs, int64_t d, const void*
       default: break;
     }
   }
-  gate_kernel<<<grid_cap(ceil_div(n_rows_bound, kGateRows), 4), 256, 0, st>>>(
+  SMOE_CUDA_TRY(launch_pdl(gate_kernel, grid_cap(ceil_div(n_rows_bound, kGateRows), 4), 256, 0, st,
       lr, hs, d, static_cast<const uint32_t*>(w_gate), b_gate, N, k, renorm, slot_owner,
-      topk_ids, topk_w, stats);
+      topk_ids, topk_w, stats));
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }
@@ -612,6 +615,7 @@ constexpr int kRouteThreads = 1024;
 __global__ void __launch_bounds__(kRouteThreads)
 route_count_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids,
                    int32_t* __restrict__ chunk_counts, int32_t max_chunks) {
+  pdl_enter();
   __shared__ int32_t s_cnt[kGateMaxN];
   __shared__ char* s_ids[SMOE_MAX_SHARDS];
   stage_ptrs(s_ids, topk_ids);
@@ -637,6 +641,7 @@ __global__ void __launch_bounds__(kRouteThreads)
 route_rank_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids, ShardPtrs pair_rank,
                   const int32_t* __restrict__ chunk_counts, int32_t max_chunks,
                   ShardPtrs count_bufs, int32_t n_count_bufs) {
+  pdl_enter();
   __shared__ int32_t s_pre[kGateMaxN];
   __shared__ int32_t s_w[32 * kGateMaxN];
   __shared__ char* s_ids[SMOE_MAX_SHARDS];
@@ -697,11 +702,11 @@ int launch_route(const LocalRows& lr, int32_t N, int32_t k, const ShardPtrs& top
   const int32_t per_shard = (int32_t)std::max<int64_t>(
       1, std::min<int64_t>(max_chunks, ceil_div(2 * num_sms(), lr.shard_count)));
   const dim3 grid(per_shard, lr.shard_count);
-  route_count_kernel<<<grid, kRouteThreads, 0, st>>>(lr, N, k, topk_ids, chunk_counts,
-                                                      max_chunks);
+  SMOE_CUDA_TRY(launch_pdl(route_count_kernel, grid, kRouteThreads, 0, st, lr, N, k, topk_ids, chunk_counts,
+                                                      max_chunks));
   SMOE_LAUNCH_CHECK();
-  route_rank_kernel<<<grid, kRouteThreads, 0, st>>>(lr, N, k, topk_ids, pair_rank, chunk_counts,
-                                                     max_chunks, count_bufs, n_count_bufs);
+  SMOE_CUDA_TRY(launch_pdl(route_rank_kernel, grid, kRouteThreads, 0, st, lr, N, k, topk_ids, pair_rank, chunk_counts,
+                                                     max_chunks, count_bufs, n_count_bufs));
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }
@@ -715,6 +720,7 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
                 const int32_t* __restrict__ slot_owner, const int32_t* __restrict__ slot_first,
                 ShardPtrs hs, ShardPtrs topk_ids, ShardPtrs pair_rank, ShardPtrs xin,
                 ShardPtrs xmeta, int64_t expert_rows, int64_t* problems, int32_t* err) {
+  pdl_enter();
   __shared__ RowMap rm;
   __shared__ int32_t s_M[kGateMaxN];
   __shared__ int32_t s_seg[kGateMaxN];
@@ -805,9 +811,9 @@ int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
                     cudaStream_t st) {
   if (N > kGateMaxN || d % 8) return SMOE_ERR_UNSUPPORTED;
   const int64_t blocks = std::max<int64_t>(1, ceil_div(n_rows_bound, 8));
-  dispatch_kernel<<<grid_cap(blocks, 16), 256, 0, st>>>(lr, N, k, d, counts_mat, slot_owner,
+  SMOE_CUDA_TRY(launch_pdl(dispatch_kernel, grid_cap(blocks, 16), 256, 0, st, lr, N, k, d, counts_mat, slot_owner,
                                                         slot_first, hs, topk_ids, pair_rank, xin,
-                                                        xmeta, expert_rows, problems, err);
+                                                        xmeta, expert_rows, problems, err));
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }
@@ -846,6 +852,7 @@ template <int G>
 __global__ void __launch_bounds__(256)
 combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtrs topk_w,
                    ShardPtrs outs, HistUpdate hu, int32_t whole_rows) {
+  pdl_enter();
   __shared__ RowMap rm;
   __shared__ char* s_y[SMOE_MAX_SHARDS];
   __shared__ char* s_wts[SMOE_MAX_SHARDS];
@@ -905,7 +912,7 @@ int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtr
   const int32_t wr = whole_rows_from();
   switch (lr.n_shards) {
 #define SMOE_CMB_CASE(G_) \
-    case G_: combine_sag_kernel<G_><<<grid, 256, 0, st>>>(lr, k, d, ypair, topk_w, outs, hu, wr); break;
+    case G_: SMOE_CUDA_TRY(launch_pdl(combine_sag_kernel<G_>, grid, 256, 0, st, lr, k, d, ypair, topk_w, outs, hu, wr)); break;
     SMOE_CMB_CASE(1) SMOE_CMB_CASE(2) SMOE_CMB_CASE(3) SMOE_CMB_CASE(4) SMOE_CMB_CASE(5)
     SMOE_CMB_CASE(6) SMOE_CMB_CASE(7) SMOE_CMB_CASE(8) SMOE_CMB_CASE(9) SMOE_CMB_CASE(10)
     SMOE_CMB_CASE(11) SMOE_CMB_CASE(12) SMOE_CMB_CASE(13) SMOE_CMB_CASE(14) SMOE_CMB_CASE(15)
@@ -923,6 +930,7 @@ int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtr
 __global__ void __launch_bounds__(256)
 sag_kernel(LocalRows lr, int64_t d, ShardPtrs blocks, ShardPtrs outs, int32_t n_outs,
            int32_t whole_rows) {
+  pdl_enter();
   __shared__ RowMap rm;
   __shared__ char* s_in[SMOE_MAX_SHARDS];
   __shared__ char* s_out[SMOE_MAX_SHARDS];
@@ -956,8 +964,8 @@ int launch_sag(const LocalRows& lr, int64_t d, const ShardPtrs& blocks, const Sh
                int32_t n_outs, int64_t n_rows_bound, cudaStream_t st) {
   if (d % 8) return SMOE_ERR_UNSUPPORTED;
   if (n_rows_bound <= 0) return SMOE_OK;
-  sag_kernel<<<grid_items(n_rows_bound, d), 256, 0, st>>>(lr, d, blocks, outs, n_outs,
-                                                           whole_rows_from());
+  SMOE_CUDA_TRY(launch_pdl(sag_kernel, grid_items(n_rows_bound, d), 256, 0, st, lr, d, blocks, outs, n_outs,
+                                                           whole_rows_from()));
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }
@@ -1072,6 +1080,7 @@ int launch_combine_rows(const void* y, const int32_t* pair_pos, const float* top
 // ------------------------------------------------------------------ barrier
 __global__ void barrier_kernel(ShardPtrs signals, int32_t world, int32_t rank,
                                uint32_t* my_signal, uint32_t* epoch) {
+  pdl_enter();
   __shared__ uint32_t s_e;
   if (threadIdx.x == 0) {
     s_e = *epoch + 1;
@@ -1095,7 +1104,7 @@ __global__ void barrier_kernel(ShardPtrs signals, int32_t world, int32_t rank,
 int launch_barrier(const ShardPtrs& signals, int32_t world, int32_t rank, uint32_t* my_signal,
                    uint32_t* epoch, cudaStream_t st) {
   if (world <= 1) return SMOE_OK;
-  barrier_kernel<<<1, 32, 0, st>>>(signals, world, rank, my_signal, epoch);
+  SMOE_CUDA_TRY(launch_pdl(barrier_kernel, 1, 32, 0, st, signals, world, rank, my_signal, epoch));
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }

@@ -69,6 +69,7 @@ plan_count_kernel(LookupTables t, int use_lookup, const int64_t* __restrict__ to
                   const int64_t* __restrict__ devices, int64_t n, int32_t G,
                   int32_t* __restrict__ dev_ws, int64_t* __restrict__ dev_out,
                   int32_t* __restrict__ block_counts, int32_t* err) {
+  pdl_enter();
   extern __shared__ int32_t s_cnt[];                 // [G]
   for (int d = threadIdx.x; d < G; d += blockDim.x) s_cnt[d] = 0;
   __syncthreads();
@@ -99,6 +100,7 @@ plan_scatter_kernel(const int32_t* __restrict__ dev_ws, int64_t n, int32_t G,
                     int32_t n_blocks, const int32_t* __restrict__ block_counts,
                     int64_t* __restrict__ forward, int64_t* __restrict__ inverse,
                     int32_t* __restrict__ counts_out, int64_t* __restrict__ group_out) {
+  pdl_enter();
   extern __shared__ int32_t smem[];
   int32_t* s_base = smem;                 // [G] exclusive prefix over earlier tiles + running
   int32_t* s_total = smem + G;            // [G] global count per device
@@ -180,15 +182,15 @@ static int plan_impl(const LookupTables& t, int use_lookup, const int64_t* token
   char* w = static_cast<char*>(ws);
   int32_t* dev_ws = reinterpret_cast<int32_t*>(w);
   int32_t* block_counts = reinterpret_cast<int32_t*>(w + align256(sizeof(int32_t) * n));
-  plan_count_kernel<<<n_blocks, kPlanThreads, sizeof(int32_t) * G, st>>>(
-      t, use_lookup, tokens, devices, n, G, dev_ws, dev_out, block_counts, err);
+  SMOE_CUDA_TRY(launch_pdl(plan_count_kernel, n_blocks, kPlanThreads, sizeof(int32_t) * G, st,
+      t, use_lookup, tokens, devices, n, G, dev_ws, dev_out, block_counts, err));
   SMOE_LAUNCH_CHECK();
   const size_t smem2 = sizeof(int32_t) * (size_t)G * 10;
   if (smem2 > 48 * 1024)
     SMOE_CUDA_TRY(cudaFuncSetAttribute(plan_scatter_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-  plan_scatter_kernel<<<n_blocks, kPlanThreads, smem2, st>>>(
-      dev_ws, n, G, n_blocks, block_counts, forward, inverse, counts, group);
+  SMOE_CUDA_TRY(launch_pdl(plan_scatter_kernel, n_blocks, kPlanThreads, smem2, st,
+      dev_ws, n, G, n_blocks, block_counts, forward, inverse, counts, group));
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }

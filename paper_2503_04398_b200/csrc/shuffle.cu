@@ -9,6 +9,7 @@
 //   smoe_count_local       simulate_layer event count, comm.py:214
 #include "common.cuh"
 #include <algorithm>
+#include <cstdlib>
 
 namespace smoe {
 
@@ -22,6 +23,25 @@ int num_sms() {
   }
   return cached;
 }
+
+static int g_pdl = -1;
+// Layer stages whose kernels may launch early (SMOE_PDL_STAGES bit mask over
+// SMOE_STAGE_*).  Not the up GEMM: its persistent CTAs take tiles by blockIdx
+// and the launch order's CTA placement is worth 5-10% there; an early launch
+// lands the CTAs wherever the dispatch kernel leaves room (profiles/r1_pdl/).
+static int g_pdl_stage_mask = ~(1 << SMOE_STAGE_EXPERT_UP);
+static thread_local int g_pdl_stage = -1;
+int pdl_enabled() {
+  if (g_pdl < 0) {
+    const char* e = getenv("SMOE_PDL");
+    g_pdl = (e && e[0] == '0') ? 0 : 1;
+    const char* m = getenv("SMOE_PDL_STAGES");
+    if (m) g_pdl_stage_mask = (int)strtol(m, nullptr, 0);
+  }
+  return g_pdl && (g_pdl_stage < 0 || ((g_pdl_stage_mask >> g_pdl_stage) & 1));
+}
+void set_pdl_stage(int stage) { g_pdl_stage = stage; }
+void set_pdl_enabled(int on) { g_pdl = on ? 1 : 0; }
 
 static int grid_for(int64_t work, int threads, int waves = 8) {
   int64_t b = ceil_div(work, threads);

@@ -90,7 +90,8 @@ def test_new_entry_points_validate_before_device_work(lib):
     assert h.smoe_tile_weights(None, 256, 64, fake, None) == N.ERR_INVALID_ARG
     # options: known keys round-trip, unknown keys / values are rejected
     for key, vals in ((N.OPT_GEMM_CTA_GROUP_UP, (1, 2)), (N.OPT_GEMM_CTA_GROUP_DOWN, (1, 2)),
-                      (N.OPT_GATE_TENSOR, (0, 1)), (N.OPT_GEMM_PAIR_MIN_ROWS, (0, 64, 1000))):
+                      (N.OPT_GATE_TENSOR, (0, 1)), (N.OPT_GEMM_PAIR_MIN_ROWS, (0, 64, 1000)),
+                      (N.OPT_PDL, (0, 1))):
         old = h.smoe_get_option(key)
         for v in vals:
             assert h.smoe_set_option(key, v) == N.OK and h.smoe_get_option(key) == v

@@ -51,8 +51,13 @@ def main():
         torch.cuda.synchronize()
         same = bool(torch.equal(layer.out_view(n), ref))
         graph = timed(g.replay)
+        import hashlib
+        import os
+        sha = hashlib.sha1(layer.out_view(n).view(torch.int16).cpu().numpy().tobytes()).hexdigest()
         print(json.dumps({"config": a.config, "tokens": n, "eager_us": eager, "graph_us": graph,
-                          "graph_output_identical": same}), flush=True)
+                          "graph_output_identical": same, "out_sha1": sha[:16],
+                          "env": {k: v for k, v in os.environ.items() if k.startswith("SMOE_")}}),
+              flush=True)
         del layer, w, g
         torch.cuda.empty_cache()
 
