@@ -61,6 +61,9 @@ const char* smoe_version(void);
 #define SMOE_OPT_PDL                 4  /* layer kernels: 1 = programmatic dependent */
                                         /* launch (default; env SMOE_PDL=0 to start  */
                                         /* with 0), 0 = plain stream order           */
+#define SMOE_OPT_PDL_STAGES          5  /* bit mask over SMOE_STAGE_*: stages whose  */
+                                        /* kernels launch early (default: all but    */
+                                        /* EXPERT_UP; env SMOE_PDL_STAGES)           */
 int smoe_set_option(int32_t key, int32_t value);
 int smoe_get_option(int32_t key);
 const char* smoe_status_string(int status);

@@ -44,6 +44,8 @@ __device__ __forceinline__ void pdl_enter() { pdl_trigger(); pdl_wait(); }
 int pdl_enabled();                      // SMOE_OPT_PDL (default 1; env SMOE_PDL=0)
 void set_pdl_enabled(int on);
 void set_pdl_stage(int stage);           // layer stage being launched (-1: none)
+int pdl_stage_mask();                    // SMOE_OPT_PDL_STAGES
+void set_pdl_stage_mask(int mask);
 
 // <<<grid, block, smem, st>>> with the PDL attribute when enabled.
 template <typename... KArgs, typename... Args>

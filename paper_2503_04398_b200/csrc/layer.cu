@@ -487,6 +487,10 @@ extern "C" int smoe_set_option(int32_t key, int32_t value) {
       if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
       set_pdl_enabled(value);
       return SMOE_OK;
+    case SMOE_OPT_PDL_STAGES:
+      if (value < 0 || value > 0xff) return SMOE_ERR_INVALID_ARG;
+      set_pdl_stage_mask(value);
+      return SMOE_OK;
     default:
       return SMOE_ERR_INVALID_ARG;
   }
@@ -498,6 +502,7 @@ extern "C" int smoe_get_option(int32_t key) {
   if (key == SMOE_OPT_GATE_TENSOR) return gate_tc_enabled();
   if (key == SMOE_OPT_GEMM_PAIR_MIN_ROWS) return gemm_pair_min_rows();
   if (key == SMOE_OPT_PDL) return pdl_enabled();
+  if (key == SMOE_OPT_PDL_STAGES) return pdl_stage_mask();
   return -1;
 }
 

@@ -41,6 +41,8 @@ int pdl_enabled() {
   return g_pdl && (g_pdl_stage < 0 || ((g_pdl_stage_mask >> g_pdl_stage) & 1));
 }
 void set_pdl_stage(int stage) { g_pdl_stage = stage; }
+int pdl_stage_mask() { pdl_enabled(); return g_pdl_stage_mask & 0xff; }
+void set_pdl_stage_mask(int mask) { pdl_enabled(); g_pdl_stage_mask = mask & 0xff; }
 void set_pdl_enabled(int on) { g_pdl = on ? 1 : 0; }
 
 static int grid_for(int64_t work, int threads, int waves = 8) {

@@ -382,3 +382,41 @@ def test_microbatched_forward_api_single_process():
     got = mb.forward(parts, w.tokens, w.hist)
     assert torch.equal(got.cpu(), want.cpu())
     assert torch.equal(mb.next_history(n), ref_layer.next_history(n))
+
+
+@pytest.mark.parametrize("stages", [0x00, 0xff])
+def test_programmatic_dependent_launch_is_bit_identical(stages):
+    """Programmatic dependent launch changes only when kernels start: the
+    layer with every stage launched early (0xff, including the up GEMM the
+    default keeps on a plain launch) and with none (0x00, SMOE_OPT_PDL = 0),
+    eager and graph-replayed, matches the default bit for bit."""
+    from paper_2503_04398_b200 import _native as N
+    lib = N.lib()
+    over = {"G": 8, "N": 64, "k": 6, "d": 512, "f": 256}
+    n = 900
+    w = synth.make_workload("toy", n=n, eps=0.3, seed=17, cfg_override=over, device=True)
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=6, max_tokens=n)
+    layer.partial_views(n).copy_(w.partials)
+    tok = torch.as_tensor(w.tokens, device="cuda")
+    hist = torch.as_tensor(w.hist, device="cuda")
+    layer.run_device(tok, hist)
+    torch.cuda.synchronize()
+    want, want_hist = layer.out_view(n).clone(), layer.next_history(n).clone()
+    old = lib.smoe_get_option(N.OPT_PDL), lib.smoe_get_option(N.OPT_PDL_STAGES)
+    try:
+        N.check(lib.smoe_set_option(N.OPT_PDL, int(stages != 0)), "opt")
+        N.check(lib.smoe_set_option(N.OPT_PDL_STAGES, stages), "opt")
+        for _ in range(2):
+            layer.out_view(n).zero_()
+            layer.run_device(tok, hist)
+            torch.cuda.synchronize()
+            assert torch.equal(layer.out_view(n), want)
+            assert torch.equal(layer.next_history(n), want_hist)
+        g = layer.capture(tok, hist)
+        layer.out_view(n).zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(layer.out_view(n), want)
+    finally:
+        N.check(lib.smoe_set_option(N.OPT_PDL, old[0]), "opt")
+        N.check(lib.smoe_set_option(N.OPT_PDL_STAGES, old[1]), "opt")
