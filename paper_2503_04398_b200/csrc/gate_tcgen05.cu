@@ -106,19 +106,30 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
   // shard row counts come from the plan stage
   pdl_trigger();
   pdl_wait();
-  if (threadIdx.x == 0) {
-    int32_t acc = 0;
-    for (int i = 0; i < a.shard_count; ++i) {
-      const int32_t c = a.counts ? a.counts[a.shard_begin + i] : (i == 0 ? (int32_t)a.single_rows : 0);
-      s_cnt[i] = c;
-      s_prefix[i] = acc;
-      acc += (c + kGtRows - 1) / kGtRows;
-    }
-    s_prefix[a.shard_count] = acc;
+  if (threadIdx.x < 32) {
+    // one lane per shard: the count loads are in flight together
+    const int i = threadIdx.x;
+    int32_t c = 0;
+    if (i < a.shard_count)
+      c = a.counts ? a.counts[a.shard_begin + i] : (i == 0 ? (int32_t)a.single_rows : 0);
+    const int32_t tiles = (c + kGtRows - 1) / kGtRows;
+    int32_t incl = tiles;                  // inclusive prefix of the tile counts
 #pragma unroll
-    for (int i = 0; i < SMOE_MAX_SHARDS; ++i) {
-      s_ids[i] = a.topk_ids.p[i];
-      s_wts[i] = a.topk_w.p[i];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (i >= o) incl += v;
+    }
+    if (i < a.shard_count) {
+      s_cnt[i] = c;
+      s_prefix[i] = incl - tiles;
+    }
+    if (i == a.shard_count - 1) s_prefix[a.shard_count] = incl;
+    if (i == 0) {
+#pragma unroll
+      for (int j = 0; j < SMOE_MAX_SHARDS; ++j) {
+        s_ids[j] = a.topk_ids.p[j];
+        s_wts[j] = a.topk_w.p[j];
+      }
     }
   }
   tc_fence_before();

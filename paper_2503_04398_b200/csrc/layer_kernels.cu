@@ -38,18 +38,31 @@ struct RowMap {
 };
 
 __device__ __forceinline__ void load_rowmap(RowMap& rm, const LocalRows& lr) {
-  if (threadIdx.x == 0 && lr.counts == nullptr) {
-    rm.cnt[0] = (int32_t)lr.single_rows;
-    rm.total = (int32_t)lr.single_rows;
-    rm.group = 0;
-  } else if (threadIdx.x == 0) {
-    int32_t t = 0;
-    for (int i = 0; i < lr.shard_count; ++i) {
-      rm.cnt[i] = lr.counts[lr.shard_begin + i];
-      t += rm.cnt[i];
+  // warp 0: one lane per resident shard, so the count loads (written by the
+  // plan stage) are in flight together -- a serial loop paid one L2 round
+  // trip per shard, several microseconds of a decode-sized kernel
+  if (threadIdx.x < 32) {
+    const int i = threadIdx.x;
+    if (lr.counts == nullptr) {
+      if (i == 0) {
+        rm.cnt[0] = (int32_t)lr.single_rows;
+        rm.total = (int32_t)lr.single_rows;
+        rm.group = 0;
+      }
+    } else {
+      const int64_t grp = i == 0 ? *lr.group : 0;
+      int32_t c = 0;
+      if (i < lr.shard_count) {
+        c = lr.counts[lr.shard_begin + i];
+        rm.cnt[i] = c;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (i == 0) {
+        rm.total = c;
+        rm.group = grp;
+      }
     }
-    rm.total = t;
-    rm.group = *lr.group;
   }
   __syncthreads();
 }
@@ -737,18 +750,22 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
   stage_ptrs(s_xmeta, xmeta);
   const int G = lr.n_shards;
   const int tid = threadIdx.x, lane = tid & 31;
+  // the [G, N] count matrix -> shared memory in one round of loads (it was
+  // read column-serially: G dependent L2 round trips per thread, twice)
+  for (int i = tid; i < G * N; i += blockDim.x) s_off[i] = C[i];
+  load_rowmap(rm, lr);    // contains __syncthreads
   for (int e = tid; e < N; e += blockDim.x) {
     int32_t m = 0;
-    for (int s = 0; s < G; ++s) m += C[s * N + e];
+    for (int s = 0; s < G; ++s) m += s_off[s * N + e];
     s_M[e] = m;
   }
-  load_rowmap(rm, lr);    // contains __syncthreads
+  __syncthreads();
   for (int e = tid; e < N; e += blockDim.x) {
     int32_t seg = 0;
     for (int e2 = slot_first[slot_owner[e]]; e2 < e; ++e2) seg += s_M[e2];
     s_seg[e] = seg;
-    int32_t run = seg;
-    for (int s = 0; s < G; ++s) { s_off[s * N + e] = run; run += C[s * N + e]; }
+    int32_t run = seg;                     // column e: counts -> running offsets, in place
+    for (int s = 0; s < G; ++s) { const int32_t c = s_off[s * N + e]; s_off[s * N + e] = run; run += c; }
   }
   __syncthreads();
   if (blockIdx.x == 0) {
