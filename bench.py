@@ -342,7 +342,8 @@ def main():
         "gate": n_loc * row + pairs_loc * 8,
         "route": 16.0 * pairs_loc,
         "dispatch": n_loc * row + pairs_loc * (row + 8),
-        "combine_sag": pairs_loc * row + G * n_loc * row + 8 * n_loc,
+        # one output copy per process (co-resident shards share it)
+        "combine_sag": pairs_loc * row + world * n_loc * row + 8 * n_loc,
     }
     stages_rf = []
     for nm in N.STAGE_NAMES:

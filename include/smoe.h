@@ -191,7 +191,9 @@ enum {
   SMOE_BUF_XIN,           /* bf16 [expert_rows, d]: expert input rows (dispatch dst) */
   SMOE_BUF_XMETA,         /* int64 [expert_rows]: (src shard << 40) | pair slot      */
   SMOE_BUF_YPAIR,         /* bf16 [max_tokens*k, d]: expert outputs per (token,slot) */
-  SMOE_BUF_OUT,           /* bf16 [max_tokens, d]: layer output, original order      */
+  SMOE_BUF_OUT,           /* bf16 [max_tokens, d]: layer output, original order;     */
+                          /* shards of one process may share one buffer (the SAG   */
+                          /* writes each row once per distinct buffer)             */
   SMOE_BUF_COUNTS,        /* int32 [G, N]: pair counts source shard x expert slot    */
   SMOE_BUF_SIGNAL,        /* uint32 [64]: cross-process barrier pad (per process)    */
   /* local, per resident shard */

@@ -406,9 +406,12 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       hu.n_hist_outs = 0;
       if (L->buf[SMOE_BUF_HIST_OUT][0] && hu.hist_len > 0 && hu.hist_len <= 32)
         hu.hist_outs = distinct_ptrs(L, SMOE_BUF_HIST_OUT, &hu.n_hist_outs);
+      // SAG: each token's row goes once to every distinct output buffer (one
+      // per process: co-resident shards share their process's output)
+      int32_t n_outs = 0;
+      const ShardPtrs outs = distinct_ptrs(L, SMOE_BUF_OUT, &n_outs);
       rc = launch_combine_sag(lr, c.top_k, c.hidden, resident_ptrs(L, SMOE_BUF_YPAIR),
-                              local_ptrs(L, SMOE_BUF_TOPK_W), peer_ptrs(L, SMOE_BUF_OUT), hu, n,
-                              st);
+                              local_ptrs(L, SMOE_BUF_TOPK_W), outs, n_outs, hu, n, st);
       if (rc) return rc;
       return smoe_layer_barrier(L, stream);
     }

@@ -837,7 +837,8 @@ int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
 
 // ------------------------------------------------------------------ K8 combine + SAG
 // Weighted sum of the k expert outputs of one row for vectors [v0, v1), stored
-// to the token's original position in every shard's output (the SAG).
+// to the token's original position in each of the G distinct output buffers
+// (the SAG: one per process).
 template <int G>
 __device__ __forceinline__ void combine_span(char* const (&dst_base)[G], const char* y,
                                              const float (&wk)[kGateMaxK], int32_t k, int64_t d,
@@ -921,13 +922,13 @@ combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtr
 }
 
 int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtrs& ypair,
-                       const ShardPtrs& topk_w, const ShardPtrs& outs, const HistUpdate& hu,
-                       int64_t n_rows_bound, cudaStream_t st) {
+                       const ShardPtrs& topk_w, const ShardPtrs& outs, int32_t n_outs,
+                       const HistUpdate& hu, int64_t n_rows_bound, cudaStream_t st) {
   if (k > kGateMaxK || d % 8) return SMOE_ERR_UNSUPPORTED;
   if (n_rows_bound <= 0) return SMOE_OK;
   const int grid = grid_items(n_rows_bound, d);
   const int32_t wr = whole_rows_from();
-  switch (lr.n_shards) {
+  switch (n_outs) {
 #define SMOE_CMB_CASE(G_) \
     case G_: SMOE_CUDA_TRY(launch_pdl(combine_sag_kernel<G_>, grid, 256, 0, st, lr, k, d, ypair, topk_w, outs, hu, wr)); break;
     SMOE_CMB_CASE(1) SMOE_CMB_CASE(2) SMOE_CMB_CASE(3) SMOE_CMB_CASE(4) SMOE_CMB_CASE(5)

@@ -70,8 +70,8 @@ struct HistUpdate {
 };
 
 int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtrs& ypair,
-                       const ShardPtrs& topk_w, const ShardPtrs& outs, const HistUpdate& hu,
-                       int64_t n_rows_bound, cudaStream_t st);
+                       const ShardPtrs& topk_w, const ShardPtrs& outs, int32_t n_outs,
+                       const HistUpdate& hu, int64_t n_rows_bound, cudaStream_t st);
 
 // Standalone shuffled all-gather (smoe_sag): row j of blocks[g] -> every
 // outs[o] at forward[g*group + j].

@@ -98,9 +98,12 @@ class ShardGroup:
         # two partial-input buffers: forward_async fills one while the peers'
         # SRS reads the other
         per_shard = {"partial": n * d * 2, "partial_b": n * d * 2, "xin": R * d * 2,
-                     "xmeta": R * 8, "ypair": n * k * d * 2, "out": n * d * 2}
+                     "xmeta": R * 8, "ypair": n * k * d * 2}
         h = max(int(layer.tables.ngram_n), 1)
-        peer, local = self.peer_tables(G, layer.N, per_shard, {"hist": n * h * 8})
+        # one output (and next-layer history) per process: the SAG delivers
+        # every token's row to each process once, whichever of its shards
+        peer, local = self.peer_tables(G, layer.N, per_shard,
+                                       {"hist": n * h * 8, "out": n * d * 2})
 
         def tensor(ptr, shape, typestr):
             return torch.as_tensor(_CudaArray(ptr, shape, typestr), device=device)
@@ -109,7 +112,7 @@ class ShardGroup:
         peer["partial_local"] = tensor(local["partial"], (L, n, d), "<i2").view(torch.bfloat16)
         peer["partial_b_local"] = tensor(local["partial_b"], (L, n, d),
                                          "<i2").view(torch.bfloat16)
-        peer["out_local"] = tensor(local["out"], (L, n, d), "<i2").view(torch.bfloat16)
+        peer["out_local"] = tensor(local["out"], (n, d), "<i2").view(torch.bfloat16)
         peer["counts_local"] = tensor(local["counts"], (G, layer.N), "<i4")
         peer["hist_local"] = tensor(local["hist"], (n, h), "<i8")
         tensor(local["signal"], (64,), "<i4").zero_()

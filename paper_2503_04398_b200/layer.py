@@ -131,24 +131,27 @@ class SpecMoELayer:
             self.xin = t.empty((G, R, d), dtype=bf, device=dev)
             self.xmeta = t.empty((G, R), dtype=t.int64, device=dev)
             self.ypair = t.empty((G, n * k, d), dtype=bf, device=dev)
-            self.out = t.empty((G, n, d), dtype=bf, device=dev)
+            self.out_buf = t.empty((n, d), dtype=bf, device=dev)
             self.counts_mat = t.zeros((G, self.N), dtype=t.int32, device=dev)
             self.hist_next = t.zeros((n, max(self.tables.ngram_n, 1)), dtype=t.int64, device=dev)
             peer = {"partial": [self.partial[g] for g in range(G)],
                     "xin": [self.xin[g] for g in range(G)],
                     "xmeta": [self.xmeta[g] for g in range(G)],
                     "ypair": [self.ypair[g] for g in range(G)],
-                    "out": [self.out[g] for g in range(G)],
+                    "out": [self.out_buf] * G,         # one copy per process (SAG)
                     "counts": [self.counts_mat] * G,
                     "hist": [self.hist_next] * G,
                     "signal": [None] * G}
         else:
             peer = self.group.alloc_layer_buffers(self, dev)
             self.partial = peer["partial_local"]
-            self.out = peer["out_local"]
+            self.out_buf = peer["out_local"]
             self.counts_mat = peer["counts_local"]
             self.hist_next = peer["hist_local"]
         self._peer = peer
+        # every resident shard's output is the process's single output buffer
+        # (indexable per shard for the reference-style per-rank view)
+        self.out = self.out_buf.unsqueeze(0).expand(G if self.group is None else L, n, d)
         self.hs = t.empty((L, n, d), dtype=bf, device=dev)
         self.topk_ids = t.empty((L, n, k), dtype=t.int32, device=dev)
         self.topk_w = t.empty((L, n, k), dtype=t.float32, device=dev)
@@ -572,7 +575,8 @@ class MicroBatchedSpecMoE:
         if self.group is not None:
             return                       # every micro-batch layer keeps its own IPC buffers
         self.partial = t.zeros((G, self.max_tokens, d), dtype=t.bfloat16, device=dev)
-        self.out = t.empty((G, self.max_tokens, d), dtype=t.bfloat16, device=dev)
+        self.out_buf = t.empty((self.max_tokens, d), dtype=t.bfloat16, device=dev)
+        self.out = self.out_buf.unsqueeze(0).expand(G, self.max_tokens, d)
         h = max(first.tables.ngram_n, 1)
         self.hist_next = t.zeros((self.max_tokens, h), dtype=t.int64, device=dev)
         for c, L in enumerate(self.layers):
@@ -581,9 +585,11 @@ class MicroBatchedSpecMoE:
             P = self.partial[:, lo:hi]
             L._bind_partial(P)
             L.partial, L.out = P, self.out[:, lo:hi]       # drop the layer's own copies
+            L.out_buf = self.out_buf[lo:hi]
             L._bound_partial = P
             for g in range(G):
-                N.check(L.lib.smoe_layer_bind(L._h, N.BUF_OUT, g, N.ptr(self.out[g, lo:])), "bind")
+                N.check(L.lib.smoe_layer_bind(L._h, N.BUF_OUT, g, N.ptr(self.out_buf[lo:])),
+                        "bind")
                 N.check(L.lib.smoe_layer_bind(L._h, N.BUF_HIST_OUT, g,
                                               N.ptr(self.hist_next[lo:])), "bind")
 
