@@ -116,7 +116,9 @@ class DSMoELayer:
             N.check(self.lib.smoe_srs(C.cast(pa, C.c_void_p), self.G, 0, 1, N.ptr(fwd),
                                       N.ptr(counts), N.ptr(grp), n, self.d,
                                       C.cast(po, C.c_void_p), N.stream_ptr()), "all_reduce")
-        return {r: h.clone() for r in self.local_ranks}        # every rank holds the sum
+        # every rank holds the sum: co-resident ranks share one copy (as the
+        # s-MoE layer's co-resident shards share one SAG output)
+        return {r: h for r in self.local_ranks}
 
     def _gather_counts(self):
         t = _dev.torch()
