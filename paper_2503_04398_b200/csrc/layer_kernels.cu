@@ -839,29 +839,49 @@ int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
 // Weighted sum of the k expert outputs of one row for vectors [v0, v1), stored
 // to the token's original position in each of the G distinct output buffers
 // (the SAG: one per process).
+// U vectors per lane per iteration (U * k 16-B loads in flight); every
+// output vector is the same fused multiply-add chain over s = 0..k-1
+// whichever U computes it, so whole-row and chunked work items agree bit
+// for bit (batch invariance).
+template <int G, int U, int KM>
+__device__ __forceinline__ int64_t combine_span_u(char* const (&dst_base)[G], const char* y,
+                                                  const float (&wk)[kGateMaxK], int32_t k,
+                                                  int64_t d, int64_t i, int64_t v, int64_t v1) {
+  for (; v + 32 * (U - 1) < v1; v += 32 * U) {
+    uint4 yv[U][KM];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int s = 0; s < KM; ++s)
+        if (s < k) yv[u][s] = ld_nc_v4(y + ((int64_t)s * d + (v + 32 * u) * 8) * 2);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int s = 0; s < KM; ++s) {
+        if (s < k) {
+          float t[8];
+          set_bf16x8(t, yv[u][s]);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) a[c] = __fmaf_rn(wk[s], t[c], a[c]);
+        }
+      }
+      const uint4 o = pack_bf16x8(a);
+#pragma unroll
+      for (int r = 0; r < G; ++r) st_cs_v4(dst_base[r] + (i * d + (v + 32 * u) * 8) * 2, o);
+    }
+  }
+  return v;
+}
+
 template <int G>
 __device__ __forceinline__ void combine_span(char* const (&dst_base)[G], const char* y,
                                              const float (&wk)[kGateMaxK], int32_t k, int64_t d,
                                              int64_t i, int64_t v0, int64_t v1, int lane) {
-  for (int64_t v = v0 + lane; v < v1; v += 32) {
-    uint4 yv[kGateMaxK];
-#pragma unroll
-    for (int s = 0; s < kGateMaxK; ++s)
-      if (s < k) yv[s] = ld_nc_v4(y + ((int64_t)s * d + v * 8) * 2);
-    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int s = 0; s < kGateMaxK; ++s) {
-      if (s < k) {
-        float t[8];
-        set_bf16x8(t, yv[s]);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) a[c] += wk[s] * t[c];
-      }
-    }
-    const uint4 o = pack_bf16x8(a);
-#pragma unroll
-    for (int r = 0; r < G; ++r) st_cs_v4(dst_base[r] + (i * d + v * 8) * 2, o);
-  }
+  int64_t v = v0 + lane;
+  if (k <= 2) v = combine_span_u<G, 4, 2>(dst_base, y, wk, k, d, i, v, v1);
+  else if (k <= 4) v = combine_span_u<G, 2, 4>(dst_base, y, wk, k, d, i, v, v1);
+  combine_span_u<G, 1, kGateMaxK>(dst_base, y, wk, k, d, i, v, v1);
 }
 
 // Work items: whole rows, or 1 KiB column chunks for small batches (as in the
