@@ -16,6 +16,7 @@ enum GemmEpilogue : int32_t {
 constexpr int kGemmBM = 128;
 constexpr int kGemmBN = 256;
 constexpr int kGemmBK = 64;
+constexpr int kGemmNarrowM = 32;      // m-block rows of the narrow (decode) variant
 constexpr int kGemmMaxProblems = 512;
 constexpr int64_t kMetaSlotMask = (int64_t(1) << 40) - 1;
 
@@ -51,6 +52,13 @@ void set_gemm_cta_group(int which, int cg);
 // Rows of B staged per CTA per k-block: the box height of B's tensor map.
 int gemm_b_box_rows(int cg);
 
+// Narrow m-blocks (cg = 0 in launch_grouped_gemm) while the batch has at most
+// this many routed rows per expert on average (SMOE_OPT_GEMM_NARROW_MAX_ROWS).
+int gemm_narrow_max_rows();
+void set_gemm_narrow_max_rows(int rows);
+
+// cg: 1 = one SM per 128x256 tile, 2 = SM pair per 256x256 tile, 0 = one SM
+// per 32x256 tile (narrow; tmap_a must have kGemmNarrowM-row boxes).
 int launch_grouped_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap_b,
                         const GemmArgs& args, int32_t epilogue, int cg, cudaStream_t stream);
 

@@ -35,18 +35,25 @@
 namespace smoe {
 
 constexpr int kThreads = 256;
-constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2;    // 16 KiB: 128 A rows x 64 K per CTA
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kStagingBytes = 4 * 32 * 64;        // 4 epilogue warps x 32 rows x 64 B
 
 // Per cta_group: CG = 1 (one SM, tile 128 x 256) or CG = 2 (an SM pair, tile
 // 256 x 256: each CTA stages 128 A rows and half of the 256 B rows, the
 // leader issues tcgen05.mma.cta_group::2 over both CTAs' shared memory).
-template <int CG> struct GemmShape {
+// NARROW (CG = 1 only, decode-sized batches): m-blocks of kGemmNarrowM rows.
+// A stages shrink to 4 KiB, which buys a fifth stage — 160 instead of 128 KiB
+// of weight tiles in flight per SM, the lever when the GEMM streams weights.
+// The MMA stays M = 128: its A operand reads 16 KiB from the stage's address,
+// i.e. the next stages' A rows (or the first B stage) as rows 32..127 — in
+// bounds, and those accumulator rows are never stored (an MMA row of D only
+// depends on the same row of A).
+template <int CG, int NARROW = 0> struct GemmShape {
+  static constexpr uint32_t kABytes = (NARROW ? kGemmNarrowM : kGemmBM) * kGemmBK * 2;
   static constexpr uint32_t kBBytes = (kGemmBN / CG) * kGemmBK * 2;   // B rows staged per CTA
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = CG == 1 ? 4 : SMOE_CG2_STAGES;
-  static constexpr int kTileM = kGemmBM * CG;
+  static constexpr int kStages = NARROW ? 5 : (CG == 1 ? 4 : SMOE_CG2_STAGES);
+  static constexpr int kTileM = NARROW ? kGemmNarrowM : kGemmBM * CG;
   static constexpr size_t kSmem = 1024 + kStages * kStageBytes + kStagingBytes + 1024 +
                                   kGemmMaxProblems * 32 + 4 * (kGemmMaxProblems + 1);
   // instruction descriptor: D f32, A/B bf16, K-major both, N = 256, M = 128 * CG
@@ -105,12 +112,14 @@ __device__ __forceinline__ TileCoord decode_tile(const SmemProblems& sp, int32_t
   return c;
 }
 
-template <int EPI, int CG>
+template <int EPI, int CG, int NARROW>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                     const __grid_constant__ CUtensorMap tmap_b, const GemmArgs args) {
-  using S = GemmShape<CG>;
+  static_assert(!NARROW || CG == 1, "narrow m-blocks are a one-SM variant");
+  using S = GemmShape<CG, NARROW>;
   constexpr int kStages = S::kStages;
+  constexpr uint32_t kABytes = S::kABytes;
   constexpr uint32_t kBBytes = S::kBBytes;
   constexpr int kTileM = S::kTileM;
   extern __shared__ uint8_t smem_raw[];
@@ -270,6 +279,17 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       const TileCoord tc = decode_tile<kTileM>(sp, np, args.n_tiles_n, args.group_m, t, cursor);
       const int32_t m = sp.m[tc.p];
       const int32_t row0 = tc.m_blk * kTileM + rank * kGemmBM + ew * 32;   // first row of warp
+      // narrow tiles: only the first warp's TMEM lanes hold rows of this tile
+      if (NARROW && ew * 32 >= kTileM) {
+        mbar_wait(tfull0 + 8 * acc, acc_phase);
+        tc_fence_after();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        continue;
+      }
       // per-lane destination row pointer (lane l <-> row row0 + l)
       char* my_row = nullptr;
       {
@@ -398,13 +418,13 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t col
   return r == CUDA_SUCCESS ? SMOE_OK : SMOE_ERR_CUDA;
 }
 
-template <int EPI, int CG>
+template <int EPI, int CG, int NARROW = 0>
 static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args,
                        cudaStream_t st) {
-  using S = GemmShape<CG>;
+  using S = GemmShape<CG, NARROW>;
   static bool attr_set = false;
   if (!attr_set) {
-    SMOE_CUDA_TRY(cudaFuncSetAttribute(grouped_gemm_kernel<EPI, CG>,
+    SMOE_CUDA_TRY(cudaFuncSetAttribute(grouped_gemm_kernel<EPI, CG, NARROW>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)S::kSmem));
     attr_set = true;
@@ -425,7 +445,8 @@ static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
   }
   const int grid = (num_sms() / CG) * CG;
   if (CG == 1) {
-    SMOE_CUDA_TRY(launch_pdl(grouped_gemm_kernel<EPI, 1>, grid, kThreads, S::kSmem, st, a, b, g));
+    SMOE_CUDA_TRY(
+        launch_pdl(grouped_gemm_kernel<EPI, 1, NARROW>, grid, kThreads, S::kSmem, st, a, b, g));
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -441,7 +462,7 @@ static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    SMOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<EPI, 2>, a, b, g));
+    SMOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<EPI, 2, 0>, a, b, g));
   }
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
@@ -460,11 +481,29 @@ void set_gemm_pair_min_rows(int rows) { g_pair_min_rows = rows; }
 void set_gemm_cta_group(int which, int cg) { g_cta_group[which ? 1 : 0] = (cg == 2) ? 2 : 1; }
 int gemm_b_box_rows(int cg) { return kGemmBN / cg; }
 
+static int g_narrow_max_rows = -1;   // -1: not set yet (env SMOE_GEMM_NARROW_MAX_ROWS, else 16)
+int gemm_narrow_max_rows() {
+  if (g_narrow_max_rows < 0) {
+    const char* e = getenv("SMOE_GEMM_NARROW_MAX_ROWS");
+    g_narrow_max_rows = (e && atoi(e) >= 0) ? atoi(e) : 16;
+  }
+  return g_narrow_max_rows;
+}
+void set_gemm_narrow_max_rows(int rows) { g_narrow_max_rows = rows; }
+
 int launch_grouped_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args,
                         int32_t epilogue, int cg, cudaStream_t st) {
   if (args.num_problems <= 0) return SMOE_OK;
   if (args.num_problems > kGemmMaxProblems) return SMOE_ERR_UNSUPPORTED;
   const bool pair = cg == 2;
+  if (cg == 0) {   // narrow m-blocks (tmap_a has kGemmNarrowM-row boxes)
+    switch (epilogue) {
+      case kEpiStore: return launch_impl<kEpiStore, 1, 1>(a, b, args, st);
+      case kEpiSwiGLU: return launch_impl<kEpiSwiGLU, 1, 1>(a, b, args, st);
+      case kEpiScatter: return launch_impl<kEpiScatter, 1, 1>(a, b, args, st);
+      default: return SMOE_ERR_INVALID_ARG;
+    }
+  }
   switch (epilogue) {
     case kEpiStore: return pair ? launch_impl<kEpiStore, 2>(a, b, args, st)
                                 : launch_impl<kEpiStore, 1>(a, b, args, st);

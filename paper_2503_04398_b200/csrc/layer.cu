@@ -42,6 +42,7 @@ struct smoe_layer {
   int maps_cg_up = 0, maps_cg_down = 0;
   CUtensorMap map_x, map_w13, map_h, map_w2;
   CUtensorMap map_w2_single;         // w2 with one-SM boxes (small batches, see EXPERT_DOWN)
+  CUtensorMap map_x_narrow, map_h_narrow;   // 32-row A boxes (decode-sized batches)
   // tensor-core gate: hidden rows of the resident shards (one arena) and W_g
   bool gate_tc = false;
   CUtensorMap map_hs, map_wg;
@@ -228,6 +229,12 @@ static int ensure_maps(smoe_layer* L) {
                            L->w_tiled ? kGemmBK : c.hidden, gemm_b_box_rows(gemm_cta_group(0)))))
     return rc;
   if ((rc = make_tmap_bf16(&L->map_h, L->buf[SMOE_BUF_HMID][0], rows, c.ffn, kGemmBM))) return rc;
+  if ((rc = make_tmap_bf16(&L->map_x_narrow, L->buf[SMOE_BUF_XIN][c.shard_begin], rows, c.hidden,
+                           kGemmNarrowM)))
+    return rc;
+  if ((rc = make_tmap_bf16(&L->map_h_narrow, L->buf[SMOE_BUF_HMID][0], rows, c.ffn,
+                           kGemmNarrowM)))
+    return rc;
   if ((rc = make_tmap_bf16(&L->map_w2, L->w2,
                            L->w_tiled ? w2_rows * (c.ffn / kGemmBK) : w2_rows,
                            L->w_tiled ? kGemmBK : c.ffn, gemm_b_box_rows(gemm_cta_group(1)))))
@@ -282,6 +289,13 @@ extern "C" int smoe_layer_barrier(smoe_layer* L, void* stream) {
 
 static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
                        const int64_t* hist, int64_t n, void* stream);
+
+// narrow GEMM m-blocks while the batch averages <= gemm_narrow_max_rows()
+// routed rows per expert (any routing is correct: an expert with more rows
+// takes several 32-row m-blocks)
+static bool narrow_gemm(const smoe_layer_config& c, int64_t n) {
+  return n * (int64_t)c.top_k <= (int64_t)gemm_narrow_max_rows() * c.n_experts;
+}
 
 extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
                                 const int64_t* hist, int64_t n, void* stream) {
@@ -375,6 +389,10 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       a.c = static_cast<char*>(L->buf[SMOE_BUF_HMID][0]);
       a.ldc = c.ffn;
       a.b_tiled = L->w_tiled;
+      // decode-sized batches stream the weights: narrow m-blocks keep more
+      // weight tiles in flight per SM (gemm_tcgen05.cu, GemmShape NARROW)
+      if (narrow_gemm(c, n) && L->maps_cg_up == 1)
+        return launch_grouped_gemm(L->map_x_narrow, L->map_w13, a, kEpiSwiGLU, 0, st);
       return launch_grouped_gemm(L->map_x, L->map_w13, a, kEpiSwiGLU, L->maps_cg_up, st);
     }
     case SMOE_STAGE_EXPERT_DOWN: {
@@ -392,7 +410,9 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       // average): one SM per tile streams w2 in a single wave; the SM pair's
       // second, partial wave costs 5-16% there (profiles/r1_down_cta_group_small.jsonl)
       const bool small = n * (int64_t)c.top_k <= (int64_t)gemm_pair_min_rows() * c.n_experts;
-      rc = small ? launch_grouped_gemm(L->map_h, L->map_w2_single, a, kEpiScatter, 1, st)
+      rc = narrow_gemm(c, n)
+               ? launch_grouped_gemm(L->map_h_narrow, L->map_w2_single, a, kEpiScatter, 0, st)
+           : small ? launch_grouped_gemm(L->map_h, L->map_w2_single, a, kEpiScatter, 1, st)
                  : launch_grouped_gemm(L->map_h, L->map_w2, a, kEpiScatter, L->maps_cg_down, st);
       if (rc) return rc;
       return smoe_layer_barrier(L, stream);
@@ -486,6 +506,10 @@ extern "C" int smoe_set_option(int32_t key, int32_t value) {
       if (value < 0) return SMOE_ERR_INVALID_ARG;
       set_gemm_pair_min_rows(value);
       return SMOE_OK;
+    case SMOE_OPT_GEMM_NARROW_MAX_ROWS:
+      if (value < 0) return SMOE_ERR_INVALID_ARG;
+      set_gemm_narrow_max_rows(value);
+      return SMOE_OK;
     case SMOE_OPT_PDL:
       if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
       set_pdl_enabled(value);
@@ -504,6 +528,7 @@ extern "C" int smoe_get_option(int32_t key) {
   if (key == SMOE_OPT_GEMM_CTA_GROUP_DOWN) return gemm_cta_group(1);
   if (key == SMOE_OPT_GATE_TENSOR) return gate_tc_enabled();
   if (key == SMOE_OPT_GEMM_PAIR_MIN_ROWS) return gemm_pair_min_rows();
+  if (key == SMOE_OPT_GEMM_NARROW_MAX_ROWS) return gemm_narrow_max_rows();
   if (key == SMOE_OPT_PDL) return pdl_enabled();
   if (key == SMOE_OPT_PDL_STAGES) return pdl_stage_mask();
   return -1;

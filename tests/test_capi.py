@@ -91,11 +91,13 @@ def test_new_entry_points_validate_before_device_work(lib):
     # options: known keys round-trip, unknown keys / values are rejected
     for key, vals in ((N.OPT_GEMM_CTA_GROUP_UP, (1, 2)), (N.OPT_GEMM_CTA_GROUP_DOWN, (1, 2)),
                       (N.OPT_GATE_TENSOR, (0, 1)), (N.OPT_GEMM_PAIR_MIN_ROWS, (0, 64, 1000)),
-                      (N.OPT_PDL, (0, 1)), (N.OPT_PDL_STAGES, (0, 0xff, 0xdf))):
+                      (N.OPT_PDL, (0, 1)), (N.OPT_PDL_STAGES, (0, 0xff, 0xdf)),
+                      (N.OPT_GEMM_NARROW_MAX_ROWS, (0, 16, 1000))):
         old = h.smoe_get_option(key)
         for v in vals:
             assert h.smoe_set_option(key, v) == N.OK and h.smoe_get_option(key) == v
-        bad = {N.OPT_GEMM_PAIR_MIN_ROWS: -1, N.OPT_PDL_STAGES: 256}.get(key, 7)
+        bad = {N.OPT_GEMM_PAIR_MIN_ROWS: -1, N.OPT_PDL_STAGES: 256,
+               N.OPT_GEMM_NARROW_MAX_ROWS: -1}.get(key, 7)
         assert h.smoe_set_option(key, bad) == \
             N.ERR_INVALID_ARG
         assert h.smoe_set_option(key, old) == N.OK

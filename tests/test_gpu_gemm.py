@@ -135,6 +135,31 @@ def test_small_batch_down_gemm_single_sm_matches_pair():
     assert torch.equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("n,narrow_rows", [(64, 16), (700, 10000)])
+def test_narrow_gemm_bit_identical_to_wide(n, narrow_rows):
+    """The narrow GEMM variant (32-row m-blocks, 5-stage weight ring) gives the
+    same bits as the 128-row tiles: at a decode-sized batch, and forced on a
+    700-token batch where experts span many 32-row m-blocks
+    (SMOE_OPT_GEMM_NARROW_MAX_ROWS)."""
+    from paper_2503_04398_b200 import SpecMoELayer, synth
+    lib = N.lib()
+    over = {"G": 4, "N": 16, "k": 2, "d": 512, "f": 384}
+    w = synth.make_workload("toy", n=n, eps=0.3, seed=8, cfg_override=over)
+    parts = torch.from_numpy(w.partials).to(torch.bfloat16)
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=n)
+    old = lib.smoe_get_option(N.OPT_GEMM_NARROW_MAX_ROWS)
+    outs = []
+    try:
+        for rows in (narrow_rows, 0):
+            N.check(lib.smoe_set_option(N.OPT_GEMM_NARROW_MAX_ROWS, rows), "opt")
+            assert lib.smoe_get_option(N.OPT_GEMM_NARROW_MAX_ROWS) == rows
+            outs.append(layer.forward(parts, w.tokens, w.hist).clone())
+    finally:
+        N.check(lib.smoe_set_option(N.OPT_GEMM_NARROW_MAX_ROWS, old), "opt")
+    assert torch.equal(outs[0], outs[1])
+    assert outs[0].abs().sum().item() > 0
+
+
 def test_grouped_512_problems_and_limit():
     """The problem table holds up to 512 problems (DS-MoE batches every
     emulated rank's (source, expert) segments into one launch); 513 is
