@@ -18,6 +18,7 @@ constexpr int kGemmBN = 256;
 constexpr int kGemmBK = 64;
 constexpr int kGemmNarrowM = 32;      // m-block rows of the narrow (decode) variant
 constexpr int kGemmMaxProblems = 512;
+constexpr int kGemmNarrowMaxProblems = 192;   // problem table of the narrow variant
 constexpr int64_t kMetaSlotMask = (int64_t(1) << 40) - 1;
 
 struct GemmArgs {

@@ -32,11 +32,23 @@
 #ifndef SMOE_CG2_STAGES
 #define SMOE_CG2_STAGES 6
 #endif
+#ifndef SMOE_NARROW_STAGES
+#define SMOE_NARROW_STAGES 5   // 6 measured slower (profiles/r1_narrow/narrow6_rejected_ab.jsonl)
+#endif
 namespace smoe {
 
 constexpr int kThreads = 256;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kStagingBytes = 4 * 32 * 64;        // 4 epilogue warps x 32 rows x 64 B
+
+// Problem table staged in shared memory (capacity CAP problems).
+template <int CAP> struct SmemProblemsT {
+  int64_t a_off[CAP];
+  int64_t c_off[CAP];
+  int32_t m[CAP];
+  int32_t b_idx[CAP];
+  int32_t tile_prefix[CAP + 1];
+};
 
 // Per cta_group: CG = 1 (one SM, tile 128 x 256) or CG = 2 (an SM pair, tile
 // 256 x 256: each CTA stages 128 A rows and half of the 256 B rows, the
@@ -52,10 +64,15 @@ template <int CG, int NARROW = 0> struct GemmShape {
   static constexpr uint32_t kABytes = (NARROW ? kGemmNarrowM : kGemmBM) * kGemmBK * 2;
   static constexpr uint32_t kBBytes = (kGemmBN / CG) * kGemmBK * 2;   // B rows staged per CTA
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = NARROW ? 5 : (CG == 1 ? 4 : SMOE_CG2_STAGES);
+  static constexpr int kStages = NARROW ? SMOE_NARROW_STAGES : (CG == 1 ? 4 : SMOE_CG2_STAGES);
   static constexpr int kTileM = NARROW ? kGemmNarrowM : kGemmBM * CG;
-  static constexpr size_t kSmem = 1024 + kStages * kStageBytes + kStagingBytes + 1024 +
-                                  kGemmMaxProblems * 32 + 4 * (kGemmMaxProblems + 1);
+  // narrow: only the first epilogue warp stores rows, and the problem table
+  // holds kGemmNarrowMaxProblems entries — the room pays for the extra stage
+  static constexpr uint32_t kStaging = NARROW ? 32 * 64 : kStagingBytes;
+  static constexpr int kMaxProblems = NARROW ? kGemmNarrowMaxProblems : kGemmMaxProblems;
+  using Problems = SmemProblemsT<kMaxProblems>;
+  static constexpr size_t kSmem =
+      1024 + kStages * kStageBytes + kStaging + 1024 + sizeof(Problems);
   // instruction descriptor: D f32, A/B bf16, K-major both, N = 256, M = 128 * CG
   static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) |
                                      (uint32_t(kGemmBN >> 3) << 17) |
@@ -63,13 +80,6 @@ template <int CG, int NARROW = 0> struct GemmShape {
 };
 
 // ---------------------------------------------------------------- tiles
-struct SmemProblems {
-  int64_t a_off[kGemmMaxProblems];
-  int64_t c_off[kGemmMaxProblems];
-  int32_t m[kGemmMaxProblems];
-  int32_t b_idx[kGemmMaxProblems];
-  int32_t tile_prefix[kGemmMaxProblems + 1];
-};
 
 struct TileCoord {
   int32_t p, m_blk, n_blk;
@@ -80,7 +90,7 @@ struct TileCoord {
 // and m varies fastest inside a group: the CTAs of one wave share a few weight
 // tiles (n-blocks) and sweep the group's A rows, so A is read from DRAM once
 // and B once per group.
-template <int TILE_M>
+template <int TILE_M, typename SmemProblems>
 __device__ __forceinline__ TileCoord decode_tile(const SmemProblems& sp, int32_t np,
                                                  int32_t n_tiles_n, int32_t group_m, int32_t t,
                                                  int32_t& cursor) {
@@ -128,10 +138,10 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + kStages * kABytes;
   uint8_t* staging = smem + kStages * S::kStageBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + kStagingBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + S::kStaging);
   // bars: full[kStages], empty[kStages], tfull[2], tempty[2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
-  SmemProblems& sp = *reinterpret_cast<SmemProblems*>(bars + 2 * kStages + 8);
+  typename S::Problems& sp = *reinterpret_cast<typename S::Problems*>(bars + 2 * kStages + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t np = args.num_problems;
@@ -422,6 +432,7 @@ template <int EPI, int CG, int NARROW = 0>
 static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args,
                        cudaStream_t st) {
   using S = GemmShape<CG, NARROW>;
+  static_assert(S::kSmem <= 227 * 1024, "shared memory budget of one CTA per SM");
   static bool attr_set = false;
   if (!attr_set) {
     SMOE_CUDA_TRY(cudaFuncSetAttribute(grouped_gemm_kernel<EPI, CG, NARROW>,
@@ -497,6 +508,7 @@ int launch_grouped_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmAr
   if (args.num_problems > kGemmMaxProblems) return SMOE_ERR_UNSUPPORTED;
   const bool pair = cg == 2;
   if (cg == 0) {   // narrow m-blocks (tmap_a has kGemmNarrowM-row boxes)
+    if (args.num_problems > kGemmNarrowMaxProblems) return SMOE_ERR_UNSUPPORTED;
     switch (epilogue) {
       case kEpiStore: return launch_impl<kEpiStore, 1, 1>(a, b, args, st);
       case kEpiSwiGLU: return launch_impl<kEpiSwiGLU, 1, 1>(a, b, args, st);

@@ -293,8 +293,10 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
 // narrow GEMM m-blocks while the batch averages <= gemm_narrow_max_rows()
 // routed rows per expert (any routing is correct: an expert with more rows
 // takes several 32-row m-blocks)
-static bool narrow_gemm(const smoe_layer_config& c, int64_t n) {
-  return n * (int64_t)c.top_k <= (int64_t)gemm_narrow_max_rows() * c.n_experts;
+static bool narrow_gemm(const smoe_layer* L, int64_t n) {
+  const auto& c = L->cfg;
+  return L->local_slots <= kGemmNarrowMaxProblems &&
+         n * (int64_t)c.top_k <= (int64_t)gemm_narrow_max_rows() * c.n_experts;
 }
 
 extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
@@ -391,7 +393,7 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       a.b_tiled = L->w_tiled;
       // decode-sized batches stream the weights: narrow m-blocks keep more
       // weight tiles in flight per SM (gemm_tcgen05.cu, GemmShape NARROW)
-      if (narrow_gemm(c, n) && L->maps_cg_up == 1)
+      if (narrow_gemm(L, n) && L->maps_cg_up == 1)
         return launch_grouped_gemm(L->map_x_narrow, L->map_w13, a, kEpiSwiGLU, 0, st);
       return launch_grouped_gemm(L->map_x, L->map_w13, a, kEpiSwiGLU, L->maps_cg_up, st);
     }
@@ -410,7 +412,7 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       // average): one SM per tile streams w2 in a single wave; the SM pair's
       // second, partial wave costs 5-16% there (profiles/r1_down_cta_group_small.jsonl)
       const bool small = n * (int64_t)c.top_k <= (int64_t)gemm_pair_min_rows() * c.n_experts;
-      rc = narrow_gemm(c, n)
+      rc = narrow_gemm(L, n)
                ? launch_grouped_gemm(L->map_h_narrow, L->map_w2_single, a, kEpiScatter, 0, st)
            : small ? launch_grouped_gemm(L->map_h, L->map_w2_single, a, kEpiScatter, 1, st)
                  : launch_grouped_gemm(L->map_h, L->map_w2, a, kEpiScatter, L->maps_cg_down, st);
