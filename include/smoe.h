@@ -66,7 +66,7 @@ const char* smoe_version(void);
                                         /* EXPERT_UP; env SMOE_PDL_STAGES)           */
 #define SMOE_OPT_GEMM_NARROW_MAX_ROWS 6 /* layer GEMMs: 32-row m-blocks, 5-stage     */
                                         /* weight ring while n*k <= this * n_experts */
-                                        /* (default 16; 0 = off)                     */
+                                        /* (default 0 = off)                         */
 int smoe_set_option(int32_t key, int32_t value);
 int smoe_get_option(int32_t key);
 const char* smoe_status_string(int status);
