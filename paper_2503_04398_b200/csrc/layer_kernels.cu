@@ -886,8 +886,12 @@ __device__ __forceinline__ void combine_span(char* const (&dst_base)[G], const c
 
 // Work items: whole rows, or 1 KiB column chunks for small batches (as in the
 // SRS); the first chunk of a row also writes the next layer's history window.
-template <int G>
-__global__ void __launch_bounds__(256)
+// MINB: CTAs per SM the register budget is sized for.  3 for k > 2 (DSV2-Lite
+// combine + SAG 0.105 -> 0.095 ms at 16 384 tokens); 2 for k <= 2, whose
+// 4 x k loads in flight per lane spill at 3 (Mixtral 0.084 -> 0.128 ms;
+// profiles/r1_cmb_occupancy_ab.jsonl, _rejected.jsonl).
+template <int G, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtrs topk_w,
                    ShardPtrs outs, HistUpdate hu, int32_t whole_rows) {
   pdl_enter();
@@ -950,7 +954,12 @@ int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtr
   const int32_t wr = whole_rows_from();
   switch (n_outs) {
 #define SMOE_CMB_CASE(G_) \
-    case G_: SMOE_CUDA_TRY(launch_pdl(combine_sag_kernel<G_>, grid, 256, 0, st, lr, k, d, ypair, topk_w, outs, hu, wr)); break;
+    case G_:                                                                             \
+      SMOE_CUDA_TRY(k <= 2 ? launch_pdl(combine_sag_kernel<G_, 2>, grid, 256, 0, st, lr, k, d,  \
+                                        ypair, topk_w, outs, hu, wr)                         \
+                           : launch_pdl(combine_sag_kernel<G_, 3>, grid, 256, 0, st, lr, k, d,  \
+                                        ypair, topk_w, outs, hu, wr));                       \
+      break;
     SMOE_CMB_CASE(1) SMOE_CMB_CASE(2) SMOE_CMB_CASE(3) SMOE_CMB_CASE(4) SMOE_CMB_CASE(5)
     SMOE_CMB_CASE(6) SMOE_CMB_CASE(7) SMOE_CMB_CASE(8) SMOE_CMB_CASE(9) SMOE_CMB_CASE(10)
     SMOE_CMB_CASE(11) SMOE_CMB_CASE(12) SMOE_CMB_CASE(13) SMOE_CMB_CASE(14) SMOE_CMB_CASE(15)
