@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--ep", type=int, default=0, help="EP shards (default: config's 8)")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU baseline work")
+    p.add_argument("--ref-budget", type=float, default=300.0,
+                   help="--impl reference: max seconds for the K timed steps")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-dsmoe", action="store_true", help="skip the DS-MoE baseline timing")
@@ -166,8 +168,46 @@ def emit(line: dict):
 
 
 # --------------------------------------------------------------------------- reference arm
+def host_workload(args, cfg, n):
+    """The bench workload (same generator semantics as synth.make_workload:
+    planted routing, orthonormal gate, 1/sqrt(d)-scaled SwiGLU weights) built
+    on the HOST for the CPU arms; big tensors from torch's CPU RNG, rounded
+    to bf16 values, as float32 numpy arrays."""
+    import torch
+    from paper_2503_04398_b200 import synth
+    G, N, k, d, f, vocab = cfg["G"], cfg["N"], cfg["k"], cfg["d"], cfg["f"], cfg["vocab"]
+    rng = np.random.default_rng(args.seed)
+    bundle = synth.make_bundle(G, N, vocab, rng)
+    tokens = rng.integers(0, vocab, size=n).astype(np.int64)
+    cl = np.asarray(bundle.token_table.labels, dtype=np.int64)[tokens]
+    hist = rng.integers(0, G, size=(n, 2)).astype(np.int64)
+    keep = rng.random(n) < 0.9
+    hist[keep] = cl[keep, None]
+    chosen = synth.routing_choices(bundle, tokens, k, args.eps, rng)
+    gate = synth.planted_gate(N, d, rng)
+    g = torch.Generator().manual_seed(args.seed)
+    bf = lambda x: x.to(torch.bfloat16).float().numpy()  # noqa: E731
+    coef = torch.tensor(1.0 - 0.5 * np.arange(k) / k, dtype=torch.float32)
+    gt = torch.from_numpy(gate)
+    h = 8.0 * (coef[None, :, None] * gt[torch.from_numpy(chosen)]).sum(1)
+    h += 0.05 * torch.randn((n, d), generator=g)
+    z = torch.randn((G, n, d), generator=g)
+    z -= z.mean(0, keepdim=True)
+    partials = bf(h[None] / G + 0.5 * z)
+    del h, z
+    w1 = bf(torch.randn((N, f, d), generator=g) / d ** 0.5)
+    w3 = bf(torch.randn((N, f, d), generator=g) / d ** 0.5)
+    w2 = bf(torch.randn((N, d, f), generator=g) / f ** 0.5)
+    return bundle, tokens, hist, gate, w1, w3, w2, partials
+
+
 def run_reference(args, world, rank):
-    """CPU path of the reference, restated (oracle port): bounded sample per step."""
+    """The reference's CPU path on the host cores (the reference is pure
+    Python and ships no layer: its index half and the fp32 layer are restated
+    in oracle/), on the SAME workload as the GPU arm: every
+    timed step is the whole batch (tokens_per_gpu x N tokens) unless K steps
+    of it would exceed --ref-budget seconds, in which case each step is the
+    largest leading sample that fits (config.same_config says which)."""
     if rank != 0:
         return
     import torch
@@ -176,63 +216,78 @@ def run_reference(args, world, rank):
     cfg = dict(synth.CONFIGS[args.config])
     if args.ep:
         cfg["G"] = args.ep
-    # generate a small sample of the same workload on the host (same generator)
-    steps = args.steps + args.warmup
-    per_step_budget = max(2.0, min(args.cpu_budget, 150.0 / max(steps, 1)))
-    n_host = 2048                       # host copy of the workload the samples are cut from
-    w = synth.make_workload(args.config, n=n_host, eps=args.eps, seed=args.seed, device=False,
-                            cfg_override=cfg) if cfg["d"] * cfg["f"] * cfg["N"] < 2e9 else None
-    if w is None:
-        # big configs: numpy weight generation is slow; use torch's CPU RNG for the weights
-        w = _host_workload_torch(args, cfg)
-    gw, w1, w3, w2 = w.gate_w, w.w1, w.w3, w.w2
-    ns, _ = oracle_sample(w.bundle, w.partials, w.tokens, w.hist, gw, w1, w3, w2, cfg["k"],
-                          per_step_budget, len(w.tokens))
-    from oracle import layer_ref  # noqa: F401
+    n_full = args.tokens * max(world, args.gpus)
+    bundle, tokens, hist, gate, w1, w3, w2, parts = host_workload(args, cfg, n_full)
+    # warm-up + calibration on a small leading sample (untimed)
+    n_cal = min(512, n_full)
+    t_cal = min(oracle_sample(bundle, parts, tokens, hist, gate, w1, w3, w2, cfg["k"], 0.0,
+                              n_cal, fixed=n_cal)[1] for _ in range(max(1, args.warmup)))
+    per_tok = t_cal / n_cal
+    ns = n_full
+    if args.steps * per_tok * n_full > args.ref_budget:
+        ns = int(max(n_cal, min(n_full, args.ref_budget / args.steps / per_tok)))
     times = []
-    for i in range(steps):
-        _, t = oracle_sample(w.bundle, w.partials, w.tokens, w.hist, gw, w1, w3, w2, cfg["k"],
-                             0.0, ns, fixed=ns)
-        if i >= args.warmup:
-            times.append(t)
+    for _ in range(args.steps):
+        times.append(oracle_sample(bundle, parts, tokens, hist, gate, w1, w3, w2, cfg["k"], 0.0,
+                                   ns, fixed=ns)[1])
     total = sum(times)
     value = ns * len(times) / total
     cores = cpu_threads()
+    same = ns == n_full
     emit({"impl": "reference", "metric": "MoE-layer tokens/sec", "value": value,
           "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
           "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
           "vs_baseline": None, "dtype": "f32", "data": "synthetic (planted skew, host RNG)",
-          "config": {"workload": f"{args.config} MoE layer, EP={cfg['G']} shards, top-{cfg['k']}, "
-                                 f"hidden {cfg['d']}, CPU sample {ns} tokens/step",
-                     "tokens_per_step": ns, "eps": args.eps},
+          "config": {"workload": f"{args.config} MoE layer (N={cfg['N']} experts, top-{cfg['k']}, "
+                                 f"hidden {cfg['d']}, ffn {cfg['f']}), EP={cfg['G']} shards",
+                     "tokens_per_gpu": args.tokens, "global_tokens": n_full,
+                     "tokens_per_step": ns, "same_config": same, "eps": args.eps},
           "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
-                           "sample": f"{ns} tokens of the {args.config} workload per step "
-                                     f"(oracle/layer_ref: lookup, plan, SRS over {cfg['G']} "
-                                     f"partials, fp32 gate, SwiGLU experts, combine)"},
+                           "sample": (f"the whole {n_full}-token batch per step" if same else
+                                      f"first {ns} of the {n_full}-token batch per step "
+                                      f"(--ref-budget {args.ref_budget:.0f} s)") +
+                                     f" through oracle/layer_ref (lookup, plan, SRS over "
+                                     f"{cfg['G']} partials, fp32 gate, SwiGLU experts, combine)"},
           "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                   "d2h_bytes_per_step": 0}})
 
 
-def _host_workload_torch(args, cfg):
-    import torch
-    from paper_2503_04398_b200 import synth
-    small = dict(cfg)
-    small["f"] = 128
-    w = synth.make_workload(args.config, n=2048, eps=args.eps, seed=args.seed, device=False,
-                            cfg_override=small)
-    g = torch.Generator().manual_seed(args.seed)
-    N, f, d = cfg["N"], cfg["f"], cfg["d"]
-    bf = lambda x: x.to(torch.bfloat16).float().numpy()  # noqa: E731
-    w.w1 = bf(torch.randn((N, f, d), generator=g) / d ** 0.5)
-    w.w3 = bf(torch.randn((N, f, d), generator=g) / d ** 0.5)
-    w.w2 = bf(torch.randn((N, d, f), generator=g) / f ** 0.5)
-    w.cfg = cfg
-    return w
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def ensure_world(args) -> None:
+    """`--gpus N` means N ranks, one per GPU.  Launched without torchrun
+    (no WORLD_SIZE) and N > 1, re-exec under torch.distributed.run with N
+    processes; launched by torchrun with a different world size, fail.  A
+    plain `python bench.py --gpus 8` can therefore never silently time N = 1."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None:
+        if args.gpus <= 1:
+            return
+        if args.impl == "smoe" and os.environ.get("SMOE_BENCH_SAME_GPU") != "1":
+            import torch
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                sys.exit(f"bench.py: --gpus {args.gpus} but this box has {have} CUDA device(s)")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(_free_port()), str(Path(__file__).resolve()), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    if int(env_world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}: refusing to time "
+                 "a different GPU count than requested")
 
 
 # --------------------------------------------------------------------------- smoe arm
 def main():
     args = parse()
+    ensure_world(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

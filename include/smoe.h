@@ -67,6 +67,10 @@ const char* smoe_version(void);
 #define SMOE_OPT_GEMM_NARROW_MAX_ROWS 6 /* layer GEMMs: 32-row m-blocks, 5-stage     */
                                         /* weight ring while n*k <= this * n_experts */
                                         /* (default 0 = off)                         */
+#define SMOE_OPT_GATE_SPLIT          7  /* tcgen05 gate: 1 = logits kernel + warp-per-row */
+                                        /* selection kernel (default; env            */
+                                        /* SMOE_GATE_SPLIT=0 to start with 0), 0 =   */
+                                        /* selection in the MMA kernel's epilogue    */
 int smoe_set_option(int32_t key, int32_t value);
 int smoe_get_option(int32_t key);
 const char* smoe_status_string(int status);
@@ -157,6 +161,20 @@ int smoe_count_local(const int64_t* experts, int64_t occ, int32_t k,
                      const int64_t* expert_dev, int32_t n_experts,
                      const int64_t* token_dev, int64_t* local_out,
                      int32_t* err, void* stream);
+
+/* solver.metrics (solver.py:766-800), the event half: over occ x k events,
+ * event (i, j) has expert experts[i*k+j] (experts NULL: expert j, i.e. a
+ * dense token x expert matrix with k = N) and integer weight weights[i*k+j]
+ * (NULL: 1).  local_out = sum of weights with expert_dev[e] == token_dev[i];
+ * loads_out[c] = sum of weights with expert_dev[e] == c (c < n_clusters
+ * <= SMOE_MAX_PLAN_DEVICES), the expert-side load whose max / median is the
+ * reference's imbalance.  Negative expert ids wrap like numpy; out-of-range
+ * ids set SMOE_ERRBIT_INDEX_RANGE, cluster labels outside [0, n_clusters)
+ * SMOE_ERRBIT_EXPERT_LABEL. */
+int smoe_event_metrics(const int64_t* experts, const int64_t* weights, int64_t occ,
+                       int32_t k, const int64_t* expert_dev, int32_t n_experts,
+                       const int64_t* token_dev, int32_t n_clusters,
+                       int64_t* local_out, int64_t* loads_out, int32_t* err, void* stream);
 
 /* schedule_requests_dp (scheduler.py:160-183): request r goes to the
  * highest-affinity device still open in its window of n_devices consecutive
@@ -291,8 +309,27 @@ enum {
   SMOE_STAGE__COUNT
 };
 
-/* Run one stage / the whole layer.  tokens int64[n] and hist (int64[n,
- * hist_len] or NULL) are replicated on every process, as in attention TP. */
+/* Run one stage / the whole layer (lookup_devices scheduler.py:82-98 through
+ * resume_tokens :152-157).  tokens int64[n] and hist are replicated on every
+ * process, as in attention TP.
+ *
+ * hist: int64[n, hist_width] row-major (contiguous) window of the previous
+ * layers' top-1 clusters, oldest digit first (predictor.py:149-166), or NULL
+ * for the first layer.  hist_width must equal the table depth `hist_len` of
+ * smoe_layer_set_tables (SMOE_ERR_INVALID_ARG otherwise).  Only the newest
+ * hist_depth digits are valid: the lookup uses the n-gram table only when
+ * hist_depth == hist_width (the reference passes histories=None for the
+ * first n layers, scheduler.py:84-89), while a partial window still shifts
+ * into the next one.  The next window (SMOE_BUF_HIST_OUT) is the input
+ * shifted by one digit plus this layer's top-1 cluster; its valid depth is
+ * min(hist_depth + 1, hist_width) (0-filled digits below that).          */
+int smoe_layer_stage_hist(smoe_layer* layer, int32_t stage, const int64_t* tokens,
+                          const int64_t* hist, int32_t hist_width, int32_t hist_depth,
+                          int64_t n, void* stream);
+int smoe_layer_forward_hist(smoe_layer* layer, const int64_t* tokens,
+                            const int64_t* hist, int32_t hist_width, int32_t hist_depth,
+                            int64_t n, void* stream);
+/* Same with a full-depth window (hist_width = hist_depth = hist_len) or NULL. */
 int smoe_layer_stage(smoe_layer* layer, int32_t stage, const int64_t* tokens,
                      const int64_t* hist, int64_t n, void* stream);
 int smoe_layer_forward(smoe_layer* layer, const int64_t* tokens,
@@ -303,7 +340,7 @@ int smoe_layer_barrier(smoe_layer* layer, void* stream);
 
 /* ---- single-rank building blocks (used by the DS-MoE baseline pipeline) -- */
 /* Gate over `rows` contiguous bf16 rows h[rows, hidden]: top-k expert ids
- * (lowest index on ties) and softmax weights; stats[0..1] += local / remote
+ * (lowest index on ties; -inf logits remain candidates) and softmax weights; stats[0..1] += local / remote
  * pairs where local means expert_owner[e] == my_shard (stats nullable). */
 int smoe_gate_topk(const void* h, int64_t rows, int32_t hidden, const void* w_gate,
                    const float* b_gate, int32_t n_experts, int32_t top_k,

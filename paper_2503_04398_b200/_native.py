@@ -35,6 +35,7 @@ SIGNATURES = [
     ("smoe_permute_columns", C.c_int, [P, c_i64, c_i32, c_i32, P, P, P]),
     ("smoe_remap_index", C.c_int, [P, c_i64, P, c_i64, P, P, P]),
     ("smoe_count_local", C.c_int, [P, c_i64, c_i32, P, c_i32, P, P, P, P]),
+    ("smoe_event_metrics", C.c_int, [P, P, c_i64, c_i32, P, c_i32, P, c_i32, P, P, P, P]),
     ("smoe_schedule_requests_dp", C.c_int, [P, c_i64, c_i32, P, P]),
     ("smoe_layer_workspace_bytes", c_sz, [P]),
     ("smoe_layer_create", C.c_int, [P, P]),
@@ -49,6 +50,8 @@ SIGNATURES = [
     ("smoe_pack_w13", C.c_int, [P, P, c_i32, c_i32, c_i32, P, P]),
     ("smoe_layer_stage", C.c_int, [P, c_i32, P, P, c_i64, P]),
     ("smoe_layer_forward", C.c_int, [P, P, P, c_i64, P]),
+    ("smoe_layer_stage_hist", C.c_int, [P, c_i32, P, P, c_i32, c_i32, c_i64, P]),
+    ("smoe_layer_forward_hist", C.c_int, [P, P, P, c_i32, c_i32, c_i64, P]),
     ("smoe_layer_barrier", C.c_int, [P, P]),
     ("smoe_gate_topk", C.c_int,
      [P, c_i64, c_i32, P, P, c_i32, c_i32, c_i32, P, c_i32, P, P, P, P]),
@@ -78,6 +81,7 @@ OPT_GEMM_PAIR_MIN_ROWS = 3
 OPT_PDL = 4
 OPT_PDL_STAGES = 5
 OPT_GEMM_NARROW_MAX_ROWS = 6
+OPT_GATE_SPLIT = 7
 
 (BUF_PARTIAL, BUF_XIN, BUF_XMETA, BUF_YPAIR, BUF_OUT, BUF_COUNTS, BUF_SIGNAL, BUF_HS,
  BUF_TOPK_IDS, BUF_TOPK_W, BUF_PAIR_RANK, BUF_HMID, BUF_FORWARD, BUF_INVERSE, BUF_DEV,

@@ -91,10 +91,26 @@ class DSMoELayer:
         self.last = {}
 
     # ------------------------------------------------------------ collectives
+    def _staged(self) -> bool:
+        """gloo process groups (tests: several ranks sharing one GPU, where
+        NCCL refuses to run) carry the same collectives through host memory;
+        NCCL groups run them on the device."""
+        import torch.distributed as dist
+        return dist.get_backend(self.pg) == "gloo"
+
     def _all_reduce(self, partials):
         t = _dev.torch()
         if self.distributed:
             import torch.distributed as dist
+            if self._staged():
+                # fp32 sum in rank order, as the single-process emulation
+                h32 = partials[0].float().cpu()
+                parts = [t.empty_like(h32) for _ in range(self.G)]
+                dist.all_gather(parts, h32, group=self.pg)
+                acc = parts[0].clone()
+                for p in parts[1:]:
+                    acc += p
+                return {self.rank: acc.to(t.bfloat16).to(partials[0].device)}
             h = partials[0].clone()
             dist.all_reduce(h, group=self.pg)
             return {self.rank: h}
@@ -124,6 +140,10 @@ class DSMoELayer:
         t = _dev.torch()
         if self.distributed:
             import torch.distributed as dist
+            if self._staged():
+                parts = [t.empty(self.N, dtype=t.int32) for _ in range(self.G)]
+                dist.all_gather(parts, self.buf[self.rank]["cnt"].cpu(), group=self.pg)
+                return t.stack(parts).numpy().astype(np.int64)
             out = t.empty((self.G, self.N), dtype=t.int32, device=self.w_gate.device)
             dist.all_gather_into_tensor(out, self.buf[self.rank]["cnt"], group=self.pg)
             return out.cpu().numpy().astype(np.int64)
@@ -132,9 +152,19 @@ class DSMoELayer:
     def _all_to_all(self, name_in, name_out, send_splits, recv_splits):
         """send_splits[r][o] rows go from rank r to rank o; received rows are
         source-major in name_out."""
+        t = _dev.torch()
         if self.distributed:
             import torch.distributed as dist
             r = self.rank
+            if self._staged():
+                src = self.buf[r][name_in][: int(sum(send_splits[r]))].view(t.int16).cpu()
+                dst = t.empty((int(sum(recv_splits[r])), self.d), dtype=t.int16)
+                dist.all_to_all_single(dst, src,
+                                       output_split_sizes=[int(x) for x in recv_splits[r]],
+                                       input_split_sizes=[int(x) for x in send_splits[r]],
+                                       group=self.pg)
+                self.buf[r][name_out][: dst.shape[0]].view(t.int16).copy_(dst)
+                return
             dist.all_to_all_single(self.buf[r][name_out][: int(sum(recv_splits[r]))],
                                    self.buf[r][name_in][: int(sum(send_splits[r]))],
                                    output_split_sizes=[int(x) for x in recv_splits[r]],
@@ -155,6 +185,11 @@ class DSMoELayer:
         t = _dev.torch()
         if self.distributed:
             import torch.distributed as dist
+            if self._staged():
+                mine = self.buf[self.rank]["out"][:group].view(t.int16).cpu()
+                parts = [t.empty_like(mine) for _ in range(self.G)]
+                dist.all_gather(parts, mine, group=self.pg)
+                return t.cat(parts).to(self.w_gate.device).view(t.bfloat16)
             full = t.empty((self.G * group, self.d), dtype=t.bfloat16, device=self.w_gate.device)
             dist.all_gather_into_tensor(full, self.buf[self.rank]["out"][:group], group=self.pg)
             return full

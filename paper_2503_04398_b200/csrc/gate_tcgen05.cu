@@ -16,7 +16,7 @@
 //   warp 2         TMEM allocator
 //   warps 4..7     epilogue, ONE THREAD PER ROW: tcgen05.ld 32x32b gives the
 //                  thread its row's N' logits in registers; bias, max, softmax
-//                  sum, top-k (larger logit first, lowest expert on ties) and
+//                  sum, top-k (larger logit first, lowest s-EG slot on ties) and
 //                  the locality count need no shuffles or shared memory.
 //
 // N' = N rounded up to 16 (the MMA's N granularity at M = 128); W rows past
@@ -54,7 +54,7 @@ template <int NP, int SUB, int ST> struct GtShape {
                                      (uint32_t(NP >> 3) << 17) | (uint32_t(kGtRows >> 4) << 24);
 };
 
-template <int NP, int SUB, int ST>
+template <int NP, int SUB, int ST, bool LOGITS>
 __global__ void __launch_bounds__(kGtThreads, 1)
 gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
                const __grid_constant__ CUtensorMap tmap_w, const GateTcArgs a) {
@@ -224,11 +224,34 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
 
       const int64_t j = (int64_t)blk * kGtRows + ew * 32 + lane;
       if (j >= s_cnt[gl]) continue;
+      // NaN marks "not a candidate" (slots past N, experts already taken):
+      // every comparison with it is false, so -inf logits stay ordinary
+      // candidates and fewer than k finite logits still yield k distinct
+      // slots, as the stable argsort of the reference idiom does
+      if constexpr (LOGITS) {
+        // split gate: biased logits out, selection in gate_select_kernel
+        float* dst = a.logits + ((int64_t)gl * a.rows_per_shard + j) * N;
+        if ((N & 3) == 0) {
+#pragma unroll
+          for (int e = 0; e < NP; e += 4)
+            if (e < N)
+              *reinterpret_cast<float4*>(dst + e) =
+                  make_float4(__uint_as_float(v[e]) + s_bias[e],
+                              __uint_as_float(v[e + 1]) + s_bias[e + 1],
+                              __uint_as_float(v[e + 2]) + s_bias[e + 2],
+                              __uint_as_float(v[e + 3]) + s_bias[e + 3]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < NP; ++e)
+            if (e < N) dst[e] = __uint_as_float(v[e]) + s_bias[e];
+        }
+        continue;
+      }
       float lg[NP];
       float mx = -INFINITY;
 #pragma unroll
       for (int e = 0; e < NP; ++e) {
-        lg[e] = e < N ? __uint_as_float(v[e]) + s_bias[e] : -INFINITY;
+        lg[e] = e < N ? __uint_as_float(v[e]) + s_bias[e] : __int_as_float(0x7fffffff);
         mx = fmaxf(mx, lg[e]);
       }
       float ex = 0.f;
@@ -246,14 +269,16 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
         sel_e[s] = 0;
         sel_p[s] = 0.f;
         if (s < K) {
+          // descending scan with >=: the largest logit, lowest slot on exact
+          // ties (ties broken in s-EG slot space, test_acceptance.py:179-193)
           float bv = -INFINITY;
           int bi = 0;
 #pragma unroll
-          for (int e = 0; e < NP; ++e)
-            if (lg[e] > bv) { bv = lg[e]; bi = e; }      // strict: lowest expert on ties
+          for (int e = NP - 1; e >= 0; --e)
+            if (lg[e] >= bv) { bv = lg[e]; bi = e; }
 #pragma unroll
           for (int e = 0; e < NP; ++e)
-            if (e == bi) lg[e] = -INFINITY;
+            if (e == bi) lg[e] = __int_as_float(0x7fffffff);
           sel_e[s] = bi;
           sel_p[s] = __expf(bv - mx) * inv;
           psum += sel_p[s];
@@ -304,21 +329,29 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
   }
 }
 
-template <int NP, int SUB, int ST>
-static int launch_cfg(const CUtensorMap& mh, const CUtensorMap& mw, const GateTcArgs& a,
-                      int64_t n_rows_bound, cudaStream_t st) {
+template <int NP, int SUB, int ST, bool LOGITS>
+static int launch_cfg_l(const CUtensorMap& mh, const CUtensorMap& mw, const GateTcArgs& a,
+                        int64_t n_rows_bound, cudaStream_t st) {
   using S = GtShape<NP, SUB, ST>;
   static bool attr = false;
   if (!attr) {
-    SMOE_CUDA_TRY(cudaFuncSetAttribute(gate_tc_kernel<NP, SUB, ST>,
+    SMOE_CUDA_TRY(cudaFuncSetAttribute(gate_tc_kernel<NP, SUB, ST, LOGITS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::kSmem));
     attr = true;
   }
   const int64_t tiles = ceil_div(n_rows_bound, kGtRows) + a.shard_count;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms()));
-  SMOE_CUDA_TRY(launch_pdl(gate_tc_kernel<NP, SUB, ST>, grid, kGtThreads, S::kSmem, st, mh, mw, a));
+  SMOE_CUDA_TRY(launch_pdl(gate_tc_kernel<NP, SUB, ST, LOGITS>, grid, kGtThreads, S::kSmem, st,
+                           mh, mw, a));
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
+}
+
+template <int NP, int SUB, int ST>
+static int launch_cfg(const CUtensorMap& mh, const CUtensorMap& mw, const GateTcArgs& a,
+                      int64_t n_rows_bound, cudaStream_t st) {
+  return a.logits ? launch_cfg_l<NP, SUB, ST, true>(mh, mw, a, n_rows_bound, st)
+                  : launch_cfg_l<NP, SUB, ST, false>(mh, mw, a, n_rows_bound, st);
 }
 
 // Ring shape (SMOE_GATE_RING=<k-blocks per stage>x<stages>, tuning only):

@@ -60,10 +60,18 @@ static size_t plan_ws_aligned(const smoe_layer_config* cfg) {
   return (smoe_plan_workspace_bytes(cfg->max_tokens, cfg->n_shards) + 255) & ~size_t(255);
 }
 
+// split gate logits [shard_count * max_tokens, N] fp32 after the plan and
+// route scratch
+static size_t gate_ws_offset(const smoe_layer_config* cfg) {
+  return (plan_ws_aligned(cfg) +
+          route_workspace_bytes(cfg->max_tokens, cfg->top_k, cfg->n_experts, cfg->shard_count) +
+          255) & ~size_t(255);
+}
+
 extern "C" size_t smoe_layer_workspace_bytes(const smoe_layer_config* cfg) {
   if (!cfg) return 0;
-  return plan_ws_aligned(cfg) +
-         route_workspace_bytes(cfg->max_tokens, cfg->top_k, cfg->n_experts, cfg->shard_count);
+  return gate_ws_offset(cfg) +
+         sizeof(float) * (size_t)cfg->shard_count * cfg->max_tokens * cfg->n_experts;
 }
 
 extern "C" int smoe_layer_create(const smoe_layer_config* cfg, smoe_layer** out) {
@@ -288,7 +296,7 @@ extern "C" int smoe_layer_barrier(smoe_layer* L, void* stream) {
 }
 
 static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
-                       const int64_t* hist, int64_t n, void* stream);
+                       const int64_t* hist, int32_t hist_depth, int64_t n, void* stream);
 
 // narrow GEMM m-blocks while the batch averages <= gemm_narrow_max_rows()
 // routed rows per expert (any routing is correct: an expert with more rows
@@ -299,16 +307,37 @@ static bool narrow_gemm(const smoe_layer* L, int64_t n) {
          n * (int64_t)c.top_k <= (int64_t)gemm_narrow_max_rows() * c.n_experts;
 }
 
-extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
-                                const int64_t* hist, int64_t n, void* stream) {
+// hist: [n, hist_width] window of the previous layers' top-1 clusters (oldest
+// digit first), of which the newest hist_depth digits are valid.  The lookup
+// uses the n-gram table only for a full window (depth == width; the
+// reference passes histories=None for the first n layers, scheduler.py:84-89);
+// a partial window still feeds the next window's shift (COMBINE_SAG).
+extern "C" int smoe_layer_stage_hist(smoe_layer* L, int32_t stage, const int64_t* tokens,
+                                     const int64_t* hist, int32_t hist_width,
+                                     int32_t hist_depth, int64_t n, void* stream) {
+  if (!L) return SMOE_ERR_INVALID_ARG;
+  if (hist) {
+    // the kernels index the window as [n, hist_len]: any other width would
+    // be misread (or read past the buffer)
+    if (hist_width != L->hist_len || hist_depth < 0 || hist_depth > hist_width)
+      return SMOE_ERR_INVALID_ARG;
+  } else {
+    hist_depth = 0;
+  }
   set_pdl_stage(stage);
-  const int rc = layer_stage(L, stage, tokens, hist, n, stream);
+  const int rc = layer_stage(L, stage, tokens, hist, hist_depth, n, stream);
   set_pdl_stage(-1);
   return rc;
 }
 
+extern "C" int smoe_layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
+                                const int64_t* hist, int64_t n, void* stream) {
+  if (!L) return SMOE_ERR_INVALID_ARG;
+  return smoe_layer_stage_hist(L, stage, tokens, hist, L->hist_len, L->hist_len, n, stream);
+}
+
 static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
-                       const int64_t* hist, int64_t n, void* stream) {
+                       const int64_t* hist, int32_t hist_depth, int64_t n, void* stream) {
   if (!L || n < 0 || n > L->cfg.max_tokens) return SMOE_ERR_INVALID_ARG;
   int rc = ensure_maps(L);
   if (rc) return rc;
@@ -322,7 +351,8 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       if (n > 0 && !tokens) return SMOE_ERR_INVALID_ARG;
       SMOE_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(int64_t) * SMOE_STAT__COUNT, st));
       SMOE_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
-      return smoe_lookup_plan(tokens, n, hist, L->hist_len, L->t_labels, L->t_conf, L->vocab,
+      const int64_t* lookup_hist = (hist && hist_depth >= L->hist_len) ? hist : nullptr;
+      return smoe_lookup_plan(tokens, n, lookup_hist, L->hist_len, L->t_labels, L->t_conf, L->vocab,
                               L->a_best, L->a_conf, L->a_rows, c.n_shards,
                               static_cast<int64_t*>(L->buf[SMOE_BUF_DEV][0]),
                               static_cast<int64_t*>(L->buf[SMOE_BUF_FORWARD][0]),
@@ -354,6 +384,17 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
         g.topk_ids = local_ptrs(L, SMOE_BUF_TOPK_IDS);
         g.topk_w = local_ptrs(L, SMOE_BUF_TOPK_W);
         g.stats = stats;
+        if (gate_split_enabled()) {
+          // logits (tensor cores, HBM-bound) then selection (warp per row)
+          g.logits = reinterpret_cast<float*>(static_cast<char*>(L->buf[SMOE_BUF_WORKSPACE][0]) +
+                                              gate_ws_offset(&c));
+          rc = launch_gate_tc(L->map_hs, L->map_wg, g, n, st);
+          if (rc) return rc;
+          return launch_gate_select(lr, g.logits, c.max_tokens, c.n_experts, c.top_k,
+                                    c.renormalize, L->slot_owner_d,
+                                    local_ptrs(L, SMOE_BUF_TOPK_IDS),
+                                    local_ptrs(L, SMOE_BUF_TOPK_W), stats, n, st);
+        }
         return launch_gate_tc(L->map_hs, L->map_wg, g, n, st);
       }
       return launch_gate(lr, local_ptrs(L, SMOE_BUF_HS), c.hidden, L->w_gate, L->b_gate,
@@ -442,13 +483,20 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
   }
 }
 
-extern "C" int smoe_layer_forward(smoe_layer* L, const int64_t* tokens, const int64_t* hist,
-                                  int64_t n, void* stream) {
+extern "C" int smoe_layer_forward_hist(smoe_layer* L, const int64_t* tokens,
+                                       const int64_t* hist, int32_t hist_width,
+                                       int32_t hist_depth, int64_t n, void* stream) {
   for (int s = 0; s < SMOE_STAGE__COUNT; ++s) {
-    int rc = smoe_layer_stage(L, s, tokens, hist, n, stream);
+    int rc = smoe_layer_stage_hist(L, s, tokens, hist, hist_width, hist_depth, n, stream);
     if (rc) return rc;
   }
   return SMOE_OK;
+}
+
+extern "C" int smoe_layer_forward(smoe_layer* L, const int64_t* tokens, const int64_t* hist,
+                                  int64_t n, void* stream) {
+  if (!L) return SMOE_ERR_INVALID_ARG;
+  return smoe_layer_forward_hist(L, tokens, hist, L->hist_len, L->hist_len, n, stream);
 }
 
 // ---------------------------------------------------------------- single-rank C-ABI
@@ -512,6 +560,10 @@ extern "C" int smoe_set_option(int32_t key, int32_t value) {
       if (value < 0) return SMOE_ERR_INVALID_ARG;
       set_gemm_narrow_max_rows(value);
       return SMOE_OK;
+    case SMOE_OPT_GATE_SPLIT:
+      if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
+      set_gate_split_enabled(value);
+      return SMOE_OK;
     case SMOE_OPT_PDL:
       if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
       set_pdl_enabled(value);
@@ -532,6 +584,7 @@ extern "C" int smoe_get_option(int32_t key) {
   if (key == SMOE_OPT_GEMM_PAIR_MIN_ROWS) return gemm_pair_min_rows();
   if (key == SMOE_OPT_GEMM_NARROW_MAX_ROWS) return gemm_narrow_max_rows();
   if (key == SMOE_OPT_PDL) return pdl_enabled();
+  if (key == SMOE_OPT_GATE_SPLIT) return gate_split_enabled();
   if (key == SMOE_OPT_PDL_STAGES) return pdl_stage_mask();
   return -1;
 }

@@ -199,6 +199,158 @@ constexpr int kGatePad = kGateWords + 1;     // conflict-free row stride (words)
 constexpr int kGateMaxN = 64;
 constexpr int kGateMaxK = 8;
 
+// Softmax + ordered top-k of one row with a warp: lane holds the logits of
+// slots `lane` (v0) and `lane + 32` (v1), NaN for slots >= N.  Larger logit
+// first, lowest slot on exact ties (the stable argsort of -logits over the
+// s-EG slot order, test_acceptance.py:179-193); NaN marks "not a candidate"
+// (slots >= N, slots already taken), so -inf logits stay candidates and fewer
+// than k finite logits still give k distinct slots.  Every lane returns the
+// same selection.
+__device__ __forceinline__ void warp_topk(float v0, float v1, int32_t N, int32_t k,
+                                          int lane, int (&sel_e)[kGateMaxK],
+                                          float (&sel_p)[kGateMaxK], float& psum) {
+  float mx = fmaxf(v0, v1);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float ex = (lane < N ? __expf(v0 - mx) : 0.f) + (lane + 32 < N ? __expf(v1 - mx) : 0.f);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ex += __shfl_xor_sync(0xffffffffu, ex, o);
+  const float inv = 1.0f / ex;
+  psum = 0.f;
+#pragma unroll
+  for (int s = 0; s < kGateMaxK; ++s) {
+    sel_e[s] = 0;
+    sel_p[s] = 0.f;
+    if (s < k) {
+      float bv; int bi;
+      if (v1 == v1 && !(v0 >= v1)) { bv = v1; bi = lane + 32; }
+      else if (v0 == v0) { bv = v0; bi = lane; }
+      else { bv = -INFINITY; bi = 1 << 20; }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      sel_e[s] = bi;
+      sel_p[s] = __expf(bv - mx) * inv;
+      psum += sel_p[s];
+      if (bi == lane) v0 = __int_as_float(0x7fffffff);
+      if (bi == lane + 32) v1 = __int_as_float(0x7fffffff);
+    }
+  }
+}
+
+// Lane s < k of the warp stores selection s of row j of local shard gl and
+// counts its pair as local / remote (and whether it is the first pair of
+// the row to that remote shard).
+__device__ __forceinline__ void warp_store_topk(int lane, int32_t k, int32_t renorm,
+                                                const int (&sel_e)[kGateMaxK],
+                                                const float (&sel_p)[kGateMaxK], float psum,
+                                                int32_t* ids, float* wts, int64_t g,
+                                                const int32_t* slot_owner,
+                                                unsigned long long& my_local,
+                                                unsigned long long& my_remote,
+                                                unsigned long long& my_rrows) {
+  if (lane >= k) return;
+  float p = 0.f; int e = 0;
+#pragma unroll
+  for (int s = 0; s < kGateMaxK; ++s) if (s == lane) { p = sel_p[s]; e = sel_e[s]; }
+  ids[lane] = e;
+  wts[lane] = renorm ? p / psum : p;
+  const int32_t o = slot_owner[e];
+  if (o == g) {
+    ++my_local;
+  } else {
+    ++my_remote;
+    bool seen = false;                               // first pair to this shard?
+#pragma unroll
+    for (int s2 = 0; s2 < kGateMaxK; ++s2)
+      if (s2 < lane) seen |= slot_owner[sel_e[s2]] == o;
+    if (!seen) ++my_rrows;
+  }
+}
+
+__device__ __forceinline__ void flush_pair_stats(unsigned long long my_local,
+                                                 unsigned long long my_remote,
+                                                 unsigned long long my_rrows, int64_t* stats) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    my_local += __shfl_xor_sync(0xffffffffu, my_local, o);
+    my_remote += __shfl_xor_sync(0xffffffffu, my_remote, o);
+    my_rrows += __shfl_xor_sync(0xffffffffu, my_rrows, o);
+  }
+  if ((threadIdx.x & 31) == 0 && stats && (my_local | my_remote)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_LOCAL_PAIRS), my_local);
+    atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_REMOTE_PAIRS), my_remote);
+    atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_REMOTE_ROWS), my_rrows);
+  }
+}
+
+// Second half of the split tensor-core gate: the tcgen05 kernel streams the
+// hidden rows through the MMA and stores the biased logits (fp32, N per row,
+// ~4-32 MB for 16K tokens -- a few % of the bytes it read); here a warp per
+// row does softmax, top-k and the locality count.  Selection is a chain of k
+// dependent passes: one thread per row (the fused epilogue) left only 4 warps
+// per SM to hide it, 12 us of a 27 us DeepSeek-V2-Lite gate at 16K tokens.
+__global__ void __launch_bounds__(256)
+gate_select_kernel(LocalRows lr, const float* __restrict__ logits, int64_t rows_per_shard,
+                   int32_t N, int32_t k, int32_t renorm, const int32_t* __restrict__ slot_owner,
+                   ShardPtrs topk_ids, ShardPtrs topk_w, int64_t* stats) {
+  pdl_enter();
+  __shared__ RowMap rm;
+  __shared__ char* s_ids[SMOE_MAX_SHARDS];
+  __shared__ char* s_wts[SMOE_MAX_SHARDS];
+  __shared__ int32_t s_owner[kGateMaxN];
+  stage_ptrs(s_ids, topk_ids);
+  stage_ptrs(s_wts, topk_w);
+  if (threadIdx.x < kGateMaxN) s_owner[threadIdx.x] = threadIdx.x < N ? slot_owner[threadIdx.x] : -1;
+  load_rowmap(rm, lr);
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t w0 = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  unsigned long long my_local = 0, my_remote = 0, my_rrows = 0;
+  for (int64_t q = w0; q < rm.total; q += nwarps) {
+    int32_t gl; int64_t j;
+    decode_row(rm, lr.shard_count, q, gl, j);
+    const float* lg = logits + (gl * rows_per_shard + j) * N;
+    const float v0 = lane < N ? __ldg(lg + lane) : __int_as_float(0x7fffffff);
+    const float v1 = lane + 32 < N ? __ldg(lg + lane + 32) : __int_as_float(0x7fffffff);
+    int sel_e[kGateMaxK];
+    float sel_p[kGateMaxK];
+    float psum;
+    warp_topk(v0, v1, N, k, lane, sel_e, sel_p, psum);
+    warp_store_topk(lane, k, renorm, sel_e, sel_p, psum,
+                    reinterpret_cast<int32_t*>(s_ids[gl]) + j * k,
+                    reinterpret_cast<float*>(s_wts[gl]) + j * k, lr.shard_begin + gl, s_owner,
+                    my_local, my_remote, my_rrows);
+  }
+  flush_pair_stats(my_local, my_remote, my_rrows, stats);
+}
+
+int launch_gate_select(const LocalRows& lr, const float* logits, int64_t rows_per_shard,
+                       int32_t N, int32_t k, int32_t renorm, const int32_t* slot_owner,
+                       const ShardPtrs& topk_ids, const ShardPtrs& topk_w, int64_t* stats,
+                       int64_t n_rows_bound, cudaStream_t st) {
+  if (N > kGateMaxN || k > kGateMaxK || k > N) return SMOE_ERR_UNSUPPORTED;
+  if (n_rows_bound <= 0) return SMOE_OK;
+  const int grid = grid_cap(ceil_div(n_rows_bound, 8), 16);
+  SMOE_CUDA_TRY(launch_pdl(gate_select_kernel, grid, 256, 0, st, lr, logits, rows_per_shard, N,
+                           k, renorm, slot_owner, topk_ids, topk_w, stats));
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
+static int g_gate_split = -1;
+int gate_split_enabled() {
+  if (g_gate_split < 0) {
+    const char* e = getenv("SMOE_GATE_SPLIT");
+    g_gate_split = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_gate_split;
+}
+void set_gate_split_enabled(int on) { g_gate_split = on ? 1 : 0; }
+
 __global__ void __launch_bounds__(256)
 gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ w_gate,
             const float* __restrict__ b_gate, int32_t N, int32_t k, int32_t renorm,
@@ -282,51 +434,22 @@ gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ 
       const int32_t gl = s_gl[r];
       if (gl < 0) continue;
       const float* lg = s_logit + r * (kGateMaxN + 1);
-      float v0 = lane < N ? lg[lane] : -INFINITY;
-      float v1 = lane + 32 < N ? lg[lane + 32] : -INFINITY;
-      float mx = fmaxf(v0, v1);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      float ex = (lane < N ? __expf(v0 - mx) : 0.f) + (lane + 32 < N ? __expf(v1 - mx) : 0.f);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) ex += __shfl_xor_sync(0xffffffffu, ex, o);
-      const float inv = 1.0f / ex;
+      const float v0 = lane < N ? lg[lane] : __int_as_float(0x7fffffff);
+      const float v1 = lane + 32 < N ? lg[lane + 32] : __int_as_float(0x7fffffff);
       int sel_e[kGateMaxK];
       float sel_p[kGateMaxK];
-      float psum = 0.f;
-      for (int s = 0; s < k; ++s) {
-        // candidate: larger value wins, ties -> lower index (stable argsort of -logits)
-        float bv; int bi;
-        if (v1 > v0) { bv = v1; bi = lane + 32; } else { bv = v0; bi = lane; }
-        if (bv == -INFINITY) bi = 1 << 20;
+      float psum;
+      warp_topk(v0, v1, N, k, lane, sel_e, sel_p, psum);
+      warp_store_topk(lane, k, renorm, sel_e, sel_p, psum,
+                      reinterpret_cast<int32_t*>(s_ids[gl]) + s_j[r] * k,
+                      reinterpret_cast<float*>(s_wts[gl]) + s_j[r] * k, lr.shard_begin + gl,
+                      slot_owner, my_local, my_remote, my_rrows);
+    }
 #pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-        }
-        sel_e[s] = bi;
-        sel_p[s] = __expf(bv - mx) * inv;
-        psum += sel_p[s];
-        if (bi == lane) v0 = -INFINITY;
-        if (bi == lane + 32) v1 = -INFINITY;
-      }
-      if (lane == 0) {
-        const int64_t g = lr.shard_begin + gl;
-        int32_t* ids = reinterpret_cast<int32_t*>(s_ids[gl]) + s_j[r] * k;
-        float* wts = reinterpret_cast<float*>(s_wts[gl]) + s_j[r] * k;
-        const float scale = renorm ? 1.0f / psum : 1.0f;
-        for (int s = 0; s < k; ++s) {
-          ids[s] = sel_e[s];
-          wts[s] = sel_p[s] * scale;
-          const int32_t o = slot_owner[sel_e[s]];
-          if (o == g) { ++my_local; continue; }
-          ++my_remote;
-          bool seen = false;                             // first pair to this shard?
-          for (int s2 = 0; s2 < s; ++s2) seen |= slot_owner[sel_e[s2]] == o;
-          if (!seen) ++my_rrows;
-        }
-      }
+    for (int o = 16; o; o >>= 1) {
+      my_local += __shfl_xor_sync(0xffffffffu, my_local, o);
+      my_remote += __shfl_xor_sync(0xffffffffu, my_remote, o);
+      my_rrows += __shfl_xor_sync(0xffffffffu, my_rrows, o);
     }
     if (lane == 0 && (my_local | my_remote)) {
       atomicAdd(&s_local, my_local);
@@ -504,54 +627,16 @@ gate_mma_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const char* __restrict__ 
       const int32_t gl = s_gl[r];
       if (gl < 0) continue;
       const float* lg = lgs + r * (N + 1);
-      float v0 = lane < N ? lg[lane] : -INFINITY;
-      float v1 = lane + 32 < N ? lg[lane + 32] : -INFINITY;
-      float mx = fmaxf(v0, v1);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      float ex = (lane < N ? __expf(v0 - mx) : 0.f) + (lane + 32 < N ? __expf(v1 - mx) : 0.f);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) ex += __shfl_xor_sync(0xffffffffu, ex, o);
-      const float inv = 1.0f / ex;
+      const float v0 = lane < N ? lg[lane] : __int_as_float(0x7fffffff);
+      const float v1 = lane + 32 < N ? lg[lane + 32] : __int_as_float(0x7fffffff);
       int sel_e[kGateMaxK];
       float sel_p[kGateMaxK];
-      float psum = 0.f;
-      for (int s = 0; s < k; ++s) {
-        float bv; int bi;
-        if (v1 > v0) { bv = v1; bi = lane + 32; } else { bv = v0; bi = lane; }
-        if (bv == -INFINITY) bi = 1 << 20;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-        }
-        sel_e[s] = bi;
-        sel_p[s] = __expf(bv - mx) * inv;
-        psum += sel_p[s];
-        if (bi == lane) v0 = -INFINITY;
-        if (bi == lane + 32) v1 = -INFINITY;
-      }
-      if (lane < k) {
-        // lane s writes slot s (all lanes hold the same selection)
-        float p = 0.f; int e = 0;
-#pragma unroll
-        for (int s = 0; s < kGateMaxK; ++s) if (s == lane) { p = sel_p[s]; e = sel_e[s]; }
-        const int64_t g = lr.shard_begin + gl;
-        reinterpret_cast<int32_t*>(s_ids[gl])[s_j[r] * k + lane] = e;
-        reinterpret_cast<float*>(s_wts[gl])[s_j[r] * k + lane] = renorm ? p / psum : p;
-        const int32_t o = slot_owner[e];
-        if (o == g) {
-          ++my_local;
-        } else {
-          ++my_remote;
-          bool seen = false;                             // first pair to this shard?
-#pragma unroll
-          for (int s2 = 0; s2 < kGateMaxK; ++s2)
-            if (s2 < lane) seen |= slot_owner[sel_e[s2]] == o;
-          if (!seen) ++my_rrows;
-        }
-      }
+      float psum;
+      warp_topk(v0, v1, N, k, lane, sel_e, sel_p, psum);
+      warp_store_topk(lane, k, renorm, sel_e, sel_p, psum,
+                      reinterpret_cast<int32_t*>(s_ids[gl]) + s_j[r] * k,
+                      reinterpret_cast<float*>(s_wts[gl]) + s_j[r] * k, lr.shard_begin + gl,
+                      slot_owner, my_local, my_remote, my_rrows);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -931,7 +1016,9 @@ combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtr
         const int32_t top1 = reinterpret_cast<const int32_t*>(s_ids[gl])[j * k];
         v = hu.slot_owner[top1];
       } else {
-        v = hu.hist_in ? hu.hist_in[i * L + lane + 1] : g;   // no history yet: this shard
+        // older digits shift in from the input window; with no input
+        // window they are not valid (the caller tracks the valid depth)
+        v = hu.hist_in ? hu.hist_in[i * L + lane + 1] : 0;
       }
       for (int b = 0; b < hu.n_hist_outs; ++b)
         reinterpret_cast<int64_t*>(s_hist[b])[i * L + lane] = v;

@@ -40,6 +40,10 @@ struct GateTcArgs {
   const int32_t* slot_owner;
   ShardPtrs topk_ids, topk_w;
   int64_t* stats;
+  // non-null: the kernel only writes the biased logits, fp32 [i * rows_per_shard
+  // + j, N] for resident shard i, row j, and launch_gate_select does the
+  // softmax / top-k / locality with a warp per row
+  float* logits;
 };
 bool gate_tc_supported(int32_t n_experts, int32_t top_k, int64_t d);
 int gate_tc_enabled();                 // SMOE_OPT_GATE_TENSOR
@@ -47,6 +51,14 @@ void set_gate_tc_enabled(int on);
 int gate_tc_rows(int32_t n_experts);   // W box rows (N rounded up to 16)
 int launch_gate_tc(const CUtensorMap& map_h, const CUtensorMap& map_w, const GateTcArgs& a,
                    int64_t n_rows_bound, cudaStream_t st);
+
+int gate_split_enabled();              // SMOE_OPT_GATE_SPLIT
+void set_gate_split_enabled(int on);
+// softmax + top-k + locality over logits written by the tcgen05 gate (warp per row)
+int launch_gate_select(const LocalRows& lr, const float* logits, int64_t rows_per_shard,
+                       int32_t N, int32_t k, int32_t renorm, const int32_t* slot_owner,
+                       const ShardPtrs& topk_ids, const ShardPtrs& topk_w, int64_t* stats,
+                       int64_t n_rows_bound, cudaStream_t st);
 
 size_t route_workspace_bytes(int64_t max_tokens, int32_t k, int32_t N, int32_t shard_count);
 int launch_route(const LocalRows& lr, int32_t N, int32_t k, const ShardPtrs& topk_ids,

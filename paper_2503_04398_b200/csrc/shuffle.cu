@@ -7,6 +7,7 @@
 //   smoe_permute_columns   apply_expert_shuffle, scheduler.py:213-219
 //   smoe_remap_index       remap_topk, scheduler.py:222-224
 //   smoe_count_local       simulate_layer event count, comm.py:214
+//   smoe_event_metrics     solver.metrics LAR + per-cluster loads, solver.py:766-800
 #include "common.cuh"
 #include <algorithm>
 #include <cstdlib>
@@ -174,6 +175,41 @@ count_local_kernel(const int64_t* __restrict__ experts, int64_t occ, int32_t k,
   if ((threadIdx.x & 31) == 0 && mine) atomicAdd(local_out, mine);
 }
 
+// solver.metrics (solver.py:766-800): local events and the expert-side load
+// of every cluster.  Event (i, j) has expert experts[i*k + j] (or j when
+// experts is NULL: a dense token x expert count matrix) and weight
+// weights[i*k + j] (or 1).  Per-CTA shared histogram, one atomic per cluster
+// per CTA; all sums are exact integers (order-independent).
+__global__ void __launch_bounds__(256)
+event_metrics_kernel(const int64_t* __restrict__ experts, const int64_t* __restrict__ weights,
+                     int64_t occ, int32_t k, const int64_t* __restrict__ expert_dev, int32_t N,
+                     const int64_t* __restrict__ token_dev, int32_t n_clusters,
+                     unsigned long long* local_out, unsigned long long* loads, int32_t* err) {
+  extern __shared__ unsigned long long s_loads[];
+  for (int c = threadIdx.x; c < n_clusters; c += blockDim.x) s_loads[c] = 0;
+  __syncthreads();
+  unsigned long long mine = 0;
+  const int64_t total = occ * k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t x = experts ? __ldg(experts + e) : e % k;
+    if (x < 0) x += N;                                   // numpy wrap, as C[routed]
+    if (x < 0 || x >= N) { set_err(err, SMOE_ERRBIT_INDEX_RANGE); continue; }
+    const unsigned long long w = weights ? (unsigned long long)__ldg(weights + e) : 1ull;
+    if (w == 0) continue;
+    const int64_t c = __ldg(expert_dev + x);
+    if (c < 0 || c >= n_clusters) { set_err(err, SMOE_ERRBIT_EXPERT_LABEL); continue; }
+    if (c == __ldg(token_dev + e / k)) mine += w;
+    atomicAdd(&s_loads[c], w);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(local_out, mine);
+  __syncthreads();
+  for (int c = threadIdx.x; c < n_clusters; c += blockDim.x)
+    if (s_loads[c]) atomicAdd(&loads[c], s_loads[c]);
+}
+
 // schedule_requests_dp (scheduler.py:160-183): the open-device mask resets
 // every n_devices requests, so windows are independent -> one thread per
 // window runs the reference's greedy argmax (first maximum wins; numpy's
@@ -294,6 +330,27 @@ extern "C" int smoe_remap_index(const int64_t* idx, int64_t count, const int64_t
   if (!idx || !dst || !table) return SMOE_ERR_INVALID_ARG;
   remap_index_kernel<<<grid_for(count, 256), 256, 0, as_stream(stream)>>>(idx, count, table,
                                                                         table_len, dst, err);
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
+extern "C" int smoe_event_metrics(const int64_t* experts, const int64_t* weights, int64_t occ,
+                                  int32_t k, const int64_t* expert_dev, int32_t n_experts,
+                                  const int64_t* token_dev, int32_t n_clusters,
+                                  int64_t* local_out, int64_t* loads_out, int32_t* err,
+                                  void* stream) {
+  if (occ < 0 || k < 0 || n_clusters < 1 || n_clusters > SMOE_MAX_PLAN_DEVICES || !local_out ||
+      !loads_out)
+    return SMOE_ERR_INVALID_ARG;
+  cudaStream_t st = as_stream(stream);
+  SMOE_CUDA_TRY(cudaMemsetAsync(local_out, 0, sizeof(int64_t), st));
+  SMOE_CUDA_TRY(cudaMemsetAsync(loads_out, 0, sizeof(int64_t) * n_clusters, st));
+  if (occ == 0 || k == 0) return SMOE_OK;
+  if (!expert_dev || !token_dev || n_experts < 1) return SMOE_ERR_INVALID_ARG;
+  event_metrics_kernel<<<grid_for(occ * k, 256, 2), 256, sizeof(int64_t) * n_clusters, st>>>(
+      experts, weights, occ, k, expert_dev, n_experts, token_dev, n_clusters,
+      reinterpret_cast<unsigned long long*>(local_out),
+      reinterpret_cast<unsigned long long*>(loads_out), err);
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }

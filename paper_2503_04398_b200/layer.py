@@ -243,26 +243,63 @@ class SpecMoELayer:
             N.check(self.lib.smoe_layer_bind(self._h, N.BUF_PARTIAL, g, ptr), "bind")
         self._bound_partial = P
 
-    def run_device(self, tokens_t, hist_t=None, stream=None, stages=None):
-        """Run the layer on device-resident inputs already in the partial
-        buffers; no host synchronisation (graph-capturable)."""
-        n = int(tokens_t.shape[0])
+    @property
+    def history_width(self) -> int:
+        """Digits of the n-gram window (the bundle's n, predictor.py:57-82)."""
+        return int(self.tables.ngram_n)
+
+    def _device_inputs(self, tokens_t, hist_t, hist_depth):
+        """Validated, contiguous int64 device views of the token ids and the
+        history window, and the window's valid depth.  The kernels index the
+        window as [n, history_width] with a fixed stride, so any other shape
+        is rejected (IndexError, as numpy raises for rows outside the n-gram
+        table) instead of being misread."""
+        t = _dev.torch()
+        dev = self.w_gate.device
+        tok = tokens_t.reshape(-1).to(device=dev, dtype=t.int64).contiguous()
+        n = int(tok.shape[0])
         if n > self.max_tokens:
             raise SchedulerError(f"{n} tokens exceed max_tokens={self.max_tokens}")
-        # like the vectorised reference, any history width is accepted (a row
-        # code outside the n-gram table raises IndexError via the error flag)
+        if hist_t is None:
+            return tok, None, 0
+        h = self.history_width
+        if hist_t.dim() != 2 or tuple(hist_t.shape) != (n, h):
+            raise IndexError(f"histories must be [{n}, {h}] (tokens x n-gram depth), "
+                             f"got {tuple(hist_t.shape)}")
+        depth = h if hist_depth is None else int(hist_depth)
+        if not 0 <= depth <= h:
+            raise ValueError(f"history_depth must be in [0, {h}]")
+        hist = hist_t.to(device=dev, dtype=t.int64).contiguous()
+        return tok, hist, depth
+
+    def run_device(self, tokens_t, hist_t=None, stream=None, stages=None, hist_depth=None):
+        """Run the layer on device-resident inputs already in the partial
+        buffers; no host synchronisation (graph-capturable).
+
+        hist_t: [n, history_width] window of the previous layers' top-1
+        clusters or None (first layer); hist_depth: how many of its newest
+        digits are valid (default: all).  The n-gram lookup is used only for
+        a full window, as the reference passes histories=None for the first
+        n layers (scheduler.py:84-89)."""
+        tok, hist, depth = self._device_inputs(tokens_t, hist_t, hist_depth)
+        n = int(tok.shape[0])
+        self._inputs = (tok, hist)                 # alive until the kernels ran
         sp = N.stream_ptr(stream)
-        hp = N.ptr(hist_t)
+        hp = N.ptr(hist)
+        w = self.history_width
         if stages is None:
-            N.check(self.lib.smoe_layer_forward(self._h, N.ptr(tokens_t), hp, n, sp),
+            N.check(self.lib.smoe_layer_forward_hist(self._h, N.ptr(tok), hp, w, depth, n, sp),
                     "layer_forward")
         else:
             for s in stages:
-                N.check(self.lib.smoe_layer_stage(self._h, s, N.ptr(tokens_t), hp, n, sp),
+                N.check(self.lib.smoe_layer_stage_hist(self._h, s, N.ptr(tok), hp, w, depth,
+                                                       n, sp),
                         f"layer stage {N.STAGE_NAMES[s]}")
+        if stages is None or N.STAGE_COMBINE_SAG in stages:
+            self._hist_depth_out = min(depth + 1, w)
         return self.out_view(n)
 
-    def capture(self, tokens_t, hist_t=None):
+    def capture(self, tokens_t, hist_t=None, hist_depth=None):
         """Record one forward over these device tensors as a CUDA graph.
 
         Replaying the returned `torch.cuda.CUDAGraph` re-runs the whole layer
@@ -273,14 +310,19 @@ class SpecMoELayer:
         every process captures and replays in lockstep: the signal-pad barriers
         count epochs in device memory, so replays stay ordered across processes."""
         t = _dev.torch()
+        # the graph reads these exact buffers at replay: they must already be
+        # contiguous int64 device tensors (no hidden copy inside the capture)
+        for x in (tokens_t, hist_t):
+            if x is not None and not (x.is_cuda and x.dtype == t.int64 and x.is_contiguous()):
+                raise ValueError("capture() needs contiguous int64 CUDA token ids / histories")
         s = t.cuda.Stream()
         s.wait_stream(t.cuda.current_stream())
         with t.cuda.stream(s):                  # warm-up off the capture (lazy attributes)
-            self.run_device(tokens_t, hist_t, stream=s)
+            self.run_device(tokens_t, hist_t, stream=s, hist_depth=hist_depth)
         t.cuda.current_stream().wait_stream(s)
         g = t.cuda.CUDAGraph()
         with t.cuda.graph(g):
-            self.run_device(tokens_t, hist_t)
+            self.run_device(tokens_t, hist_t, hist_depth=hist_depth)
         return g
 
     def out_view(self, n: int, shard: int | None = None):
@@ -291,16 +333,29 @@ class SpecMoELayer:
 
     def next_history(self, n: int):
         """[n, h] device view of the n-gram window for the NEXT MoE layer,
-        written by the last forward: this window shifted by one layer plus the
-        cluster of each token's top-1 expert (predictor.py:165-166).  Without
-        an input history the older digits are the token's shard this layer."""
-        return self.hist_next[:n]
+        written by the last forward: the input window shifted by one layer
+        plus the cluster of each token's top-1 expert (predictor.py:165-166),
+        or None while fewer than h layers of routing have been observed --
+        the reference's contract is histories=None for the first n layers
+        (scheduler.py:84-89).  `history_window` returns the partial window."""
+        win, depth = self.history_window(n)
+        return win if depth >= self.history_width and depth > 0 else None
 
-    def forward(self, hidden_partials, token_ids, histories=None, out=None):
+    def history_window(self, n: int):
+        """(window [n, h] device view, valid depth): the next layer's n-gram
+        window and how many of its newest digits are real top-1 clusters.
+        Chain layers with `forward(..., histories=win, history_depth=depth)`;
+        the lookup switches to the n-gram table once depth == h."""
+        return self.hist_next[:n], int(getattr(self, "_hist_depth_out", 0))
+
+    def forward(self, hidden_partials, token_ids, histories=None, out=None,
+                history_depth=None):
         """Full layer from user tensors (host or device).
 
         hidden_partials: [L, n, d] (one partial per resident shard) or [n, d]
-        when there is a single shard; token_ids int [n]; histories int [n, h].
+        when there is a single shard; token_ids int [n]; histories int [n, h]
+        (h = the bundle's n-gram depth) or None; history_depth: valid newest
+        digits of `histories` (default h, see `history_window`).
         Returns the layer output [n, d] (bf16) in the original token order:
         a device view for CUDA inputs, else a host tensor (`out` if given —
         pass pinned host tensors for asynchronous copies).
@@ -310,13 +365,16 @@ class SpecMoELayer:
 
         def dev_i64(x):
             if isinstance(x, t.Tensor):
-                return x.to(device=self.w_gate.device, dtype=t.int64, non_blocking=True)
-            return _dev.to_device(x, t.int64)
+                return x.to(device=self.w_gate.device, dtype=t.int64,
+                            non_blocking=True).contiguous()
+            return _dev.to_device(np.ascontiguousarray(x), t.int64)
 
         tok = dev_i64(token_ids).reshape(-1)
         n = int(tok.numel())
         if n > self.max_tokens:
             raise SchedulerError(f"{n} tokens exceed max_tokens={self.max_tokens}")
+        hist = None if histories is None else dev_i64(histories)
+        self._device_inputs(tok, hist, history_depth)      # validate before any copy
         hp = hidden_partials if isinstance(hidden_partials, t.Tensor) else t.as_tensor(
             np.asarray(hidden_partials))
         if hp.dim() == 2:
@@ -328,8 +386,7 @@ class SpecMoELayer:
             dst.copy_(hp, non_blocking=True)
         else:
             dst.copy_(hp.to(device=dst.device, non_blocking=True).to(t.bfloat16))
-        hist = None if histories is None else dev_i64(histories)
-        res = self.run_device(tok, hist)
+        res = self.run_device(tok, hist, hist_depth=history_depth)
         if not host:
             self.check_errors()
             return res
@@ -340,7 +397,8 @@ class SpecMoELayer:
         return out
 
     # ------------------------------------------------------------ pipelined serving
-    def forward_async(self, hidden_partials, token_ids, histories=None, out=None):
+    def forward_async(self, hidden_partials, token_ids, histories=None, out=None,
+                      history_depth=None):
         """Pipelined `forward` for a stream of batches from HOST memory.
 
         Returns a handle whose `.result()` yields the host output.  Inputs
@@ -356,16 +414,23 @@ class SpecMoELayer:
         of the next batch is already queued behind the running one).
         """
         t = _dev.torch()
-        st = self._pipeline()
-        i = st["count"]
-        st["count"] += 1
-        slot = i % 2
         n = int(token_ids.shape[0])
         if n > self.max_tokens:
             raise SchedulerError(f"{n} tokens exceed max_tokens={self.max_tokens}")
         hp = hidden_partials if hidden_partials.dim() == 3 else hidden_partials.unsqueeze(0)
         if tuple(hp.shape) != (self.shard_count, n, self.d) or hp.dtype != t.bfloat16:
             raise SchedulerError(f"partials must be bf16 [{self.shard_count}, {n}, {self.d}]")
+        if histories is not None and tuple(histories.shape) != (n, self.history_width):
+            raise IndexError(f"histories must be [{n}, {self.history_width}]")
+        if token_ids.dim() != 1:
+            raise SchedulerError("token_ids must be 1-D")
+        # every input is validated before the pipeline state moves: a rejected
+        # batch must not flip the slot parity (peers in a ShardGroup follow
+        # the same batch sequence and barrier epochs)
+        st = self._pipeline()
+        i = st["count"]
+        st["count"] += 1
+        slot = i % 2
         P, tok, hist = st["P"][slot], st["tok"][slot], st["hist"][slot]
         # ---- H2D on the copy stream, once the slot's previous batch has passed its SRS
         with t.cuda.stream(st["h2d"]):
@@ -383,24 +448,26 @@ class SpecMoELayer:
             cs.wait_event(st["in"][slot])
             hp_t = hist[:n] if histories is not None else None
             if self.group is None:
-                self.run_device(tok[:n], hp_t, stream=cs, stages=[N.STAGE_PLAN, N.STAGE_SRS])
+                self.run_device(tok[:n], hp_t, stream=cs, hist_depth=history_depth,
+                                stages=[N.STAGE_PLAN, N.STAGE_SRS])
                 st["free_p"][slot].record(cs)
-                self.run_device(tok[:n], hp_t, stream=cs,
+                self.run_device(tok[:n], hp_t, stream=cs, hist_depth=history_depth,
                                 stages=range(N.STAGE_GATE, N.STAGE_COMBINE_SAG))
                 cs.wait_event(st["d2h_done"])      # previous output fully read out
-                self.run_device(tok[:n], hp_t, stream=cs, stages=[N.STAGE_COMBINE_SAG])
+                self.run_device(tok[:n], hp_t, stream=cs, hist_depth=history_depth,
+                                stages=[N.STAGE_COMBINE_SAG])
             else:
                 # peers read this process's partial slot in their SRS and write
                 # its output buffer in their SAG: the slot is free once every
                 # process passed this batch's ROUTE barrier, and the previous
                 # D2H must end before the barrier that closes EXPERT_DOWN
-                self.run_device(tok[:n], hp_t, stream=cs,
+                self.run_device(tok[:n], hp_t, stream=cs, hist_depth=history_depth,
                                 stages=range(N.STAGE_PLAN, N.STAGE_DISPATCH))
                 st["free_p"][slot].record(cs)
-                self.run_device(tok[:n], hp_t, stream=cs,
+                self.run_device(tok[:n], hp_t, stream=cs, hist_depth=history_depth,
                                 stages=[N.STAGE_DISPATCH, N.STAGE_EXPERT_UP])
                 cs.wait_event(st["d2h_done"])
-                self.run_device(tok[:n], hp_t, stream=cs,
+                self.run_device(tok[:n], hp_t, stream=cs, hist_depth=history_depth,
                                 stages=[N.STAGE_EXPERT_DOWN, N.STAGE_COMBINE_SAG])
             # this batch's error flag, read out before the next batch's plan
             # resets it (stream order); the host reads it in .result()
@@ -621,12 +688,18 @@ class MicroBatchedSpecMoE:
         return self.out[shard, :n]
 
     def next_history(self, n: int):
+        """As SpecMoELayer.next_history: None until the window is full."""
+        win, depth = self.history_window(n)
+        return win if depth >= self.layers[0].history_width and depth > 0 else None
+
+    def history_window(self, n: int):
+        depth = int(getattr(self.layers[0], "_hist_depth_out", 0))
         if self.group is not None:
             t = _dev.torch()
-            return t.cat([L.next_history(hi - lo) for c, L, lo, hi in self._pieces(n)])
-        return self.hist_next[:n]
+            return t.cat([L.history_window(hi - lo)[0] for c, L, lo, hi in self._pieces(n)]), depth
+        return self.hist_next[:n], depth
 
-    def forward(self, hidden_partials, token_ids, histories=None):
+    def forward(self, hidden_partials, token_ids, histories=None, history_depth=None):
         """[L, n, d] partials (device or host), token ids [n], histories
         [n, h]: the layer output [n, d] on the device."""
         t = _dev.torch()
@@ -634,18 +707,19 @@ class MicroBatchedSpecMoE:
         hp = t.as_tensor(hidden_partials)
         if hp.dim() == 2:
             hp = hp.unsqueeze(0)
-        tok = t.as_tensor(token_ids).to(device=dev, dtype=t.int64)
-        hist = None if histories is None else t.as_tensor(histories).to(device=dev,
-                                                                         dtype=t.int64)
+        tok = t.as_tensor(token_ids).to(device=dev, dtype=t.int64).reshape(-1).contiguous()
+        hist = None if histories is None else t.as_tensor(histories).to(
+            device=dev, dtype=t.int64).contiguous()
+        self.layers[0]._device_inputs(tok, hist, history_depth)   # validate the whole batch
         if self.group is None:
             self.partial_views(int(tok.numel())).copy_(hp)
         else:
             self.load_partials(hp.to(device=dev, dtype=t.bfloat16))
-        out = self.run_device(tok, hist)
+        out = self.run_device(tok, hist, history_depth)
         self.check_errors()
         return out
 
-    def run_device(self, tokens_t, hist_t=None):
+    def run_device(self, tokens_t, hist_t=None, hist_depth=None):
         """All micro-batches of one forward; returns the output view.  The
         GEMMs run in micro-batch order (each waits for the previous one's
         down projection), the movers of neighbouring micro-batches overlap
@@ -661,7 +735,8 @@ class MicroBatchedSpecMoE:
         parts = self._pieces(n)
         for c, L, lo, hi in parts:                    # movers of every micro-batch first
             h = None if hist_t is None else hist_t[lo:hi]
-            L.run_device(tokens_t[lo:hi], h, stream=self.streams[c], stages=pre)
+            L.run_device(tokens_t[lo:hi], h, stream=self.streams[c], stages=pre,
+                         hist_depth=hist_depth)
         prev = None
         for c, L, lo, hi in parts:                    # GEMMs in order, combine overlaps next
             s = self.streams[c]
@@ -669,10 +744,11 @@ class MicroBatchedSpecMoE:
             if prev is not None:
                 s.wait_event(prev)
             L.run_device(tokens_t[lo:hi], h, stream=s,
-                         stages=[N.STAGE_EXPERT_UP, N.STAGE_EXPERT_DOWN])
+                         stages=[N.STAGE_EXPERT_UP, N.STAGE_EXPERT_DOWN], hist_depth=hist_depth)
             self.events[c].record(s)
             prev = self.events[c]
-            L.run_device(tokens_t[lo:hi], h, stream=s, stages=[N.STAGE_COMBINE_SAG])
+            L.run_device(tokens_t[lo:hi], h, stream=s, stages=[N.STAGE_COMBINE_SAG],
+                         hist_depth=hist_depth)
         for s in self.streams[1:]:
             main.wait_stream(s)
         return self.out_view(n)

@@ -109,6 +109,27 @@ def routing_choices(bundle, tokens: np.ndarray, k: int, eps: float, rng) -> np.n
     return out
 
 
+def planted_gate(N: int, d: int, rng) -> np.ndarray:
+    """Orthonormal gate rows (bf16-valued float32 [N, d])."""
+    q, _ = np.linalg.qr(rng.standard_normal((d, N)))
+    return bf16_round(q.T.astype(np.float32))
+
+
+def planted_partials(gate_w: np.ndarray, chosen: np.ndarray, G: int, rng,
+                     alpha: float = 8.0) -> np.ndarray:
+    """bf16-valued [G, n, d] attention-TP partials whose reduced rows route,
+    through an orthonormal gate, to exactly `chosen` (ordered top-k, original
+    expert ids) with logit gaps >= alpha / (2k)."""
+    k = chosen.shape[1]
+    n, d = chosen.shape[0], gate_w.shape[1]
+    coef = (1.0 - 0.5 * np.arange(k) / k).astype(np.float32)
+    h = np.float32(alpha) * np.einsum("s,nsd->nd", coef, gate_w[chosen]).astype(np.float32)
+    h += 0.05 * rng.standard_normal((n, d)).astype(np.float32)
+    z = rng.standard_normal((G, n, d)).astype(np.float32)
+    z -= z.mean(0, keepdims=True)
+    return bf16_round(h[None] / G + 0.5 * z)
+
+
 def make_workload(name: str = "toy", n: int = 256, eps: float = 0.1, seed: int = 0,
                   device: bool = False, cfg_override: dict | None = None,
                   hist_consistency: float = 0.9) -> Workload:

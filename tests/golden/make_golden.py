@@ -176,11 +176,91 @@ def toy_bundle():
     np.savez_compressed(OUT / "toy.npz", **out)
 
 
+def toy_chain():
+    """configs[0] through the whole layer: the toy bundles of toy_bundle()
+    driving a 3-layer chain.  Per layer the reference's own functions give the
+    lookup (histories=None for the first n = 2 layers, scheduler.py:84-89;
+    then the top-1 clusters of the previous two layers, predictor.py:157-166),
+    the rebatch plan (rebatch_tokens) and -- through solver.metrics on a
+    one-layer trace with those devices as token labels -- the local events."""
+    out = {}
+    toy = np.load(OUT / "toy.npz")
+    for ci in range(3):
+        b = tables.read_bundle(OUT / f"toy_eps{[0, 2, 5][ci]}.bin")
+        tokens = toy[f"c{ci}_tokens"]
+        routed = toy[f"c{ci}_routed"]
+        C = np.asarray(b.expert_labels, dtype=np.int64)
+        n = 2
+        for layer in range(routed.shape[1]):
+            hist = None if layer < n else C[routed[:, layer - n:layer, 0]]
+            dev = scheduler.lookup_devices(b, tokens, hist)
+            sh, ix = scheduler.rebatch_tokens(tokens, dev, 2)
+            # metrics over this layer with the looked-up devices as the
+            # "token labels" of each occurrence (occurrence i -> token id i)
+            occ = np.arange(len(tokens))
+            tr = profiles.RequestTrace(requests=((0, occ),), routed=(routed[:, layer:layer + 1],))
+            m = solver.metrics(solver.Assignment(token_labels=dev, expert_labels=C), tr)
+            pre = f"c{ci}_l{layer}_"
+            out[pre + "dev"] = dev
+            out[pre + "forward"] = ix.forward
+            out[pre + "inverse"] = ix.inverse
+            out[pre + "group"] = np.int64(ix.group_size)
+            out[pre + "shuffled"] = sh
+            out[pre + "local"] = np.int64(m["local_events"])
+            out[pre + "imbalance"] = np.float64(m["imbalance"])
+            if hist is not None:
+                out[pre + "hist"] = hist
+    out["n_cases"] = np.int64(3)
+    np.savez_compressed(OUT / "toy_chain.npz", **out)
+
+
+def metrics_cases():
+    """solver.metrics (solver.py:766-800) on the reference's own planted
+    fixtures (tests/conftest.py:7-24): truth assignment (test_solver.py:
+    342-351: LAR 1.0, imbalance 1.0), a round-robin assignment and a solved
+    one, each on the trace and on the aggregated count matrix."""
+    out = {}
+    ci = 0
+    for noise, seed in ((0.0, 0), (0.2, 1)):
+        topo = profiles.Topology(devices=4, clusters=4, experts=16, top_k=2, layers=3,
+                                 vocab=1024)
+        mats, trace, truth = profiles.synthesize_planted_profile(
+            topo, noise=noise, tokens_per_cluster=50, seed=seed, reps=8)
+        agg = aggregate(mats)
+        R = truth["token_labels"].copy()
+        R[R < 0] = 0
+        assigns = [solver.Assignment(token_labels=R, expert_labels=truth["expert_labels"]),
+                   solver.baseline_round_robin(topo)]
+        cfg = solver.SolverConfig(n_steps=20, n_samples=32, eta=0.5, seed=seed)
+        assigns.append(solver.solve_ceo(agg, cfg, topo)[0])
+        for a in assigns:
+            for kind, ev in (("trace", trace), ("matrix", agg)):
+                m = solver.metrics(a, ev)
+                pre = f"c{ci}_"
+                out[pre + "kind"] = np.int64(kind == "trace")
+                out[pre + "token_labels"] = np.asarray(a.token_labels, dtype=np.int64)
+                out[pre + "expert_labels"] = np.asarray(a.expert_labels, dtype=np.int64)
+                out[pre + "lar"] = np.float64(m["lar"])
+                out[pre + "imbalance"] = np.float64(m["imbalance"])
+                out[pre + "events"] = np.int64(m["events"])
+                out[pre + "local_events"] = np.int64(m["local_events"])
+                if kind == "trace":
+                    out[pre + "tokens"] = trace.all_tokens()
+                    out[pre + "routed"] = trace.all_routed()
+                else:
+                    out[pre + "counts"] = agg.counts.astype(np.int64)
+                ci += 1
+    out["n_cases"] = np.int64(ci)
+    np.savez_compressed(OUT / "metrics.npz", **out)
+
+
 if __name__ == "__main__":
     lookup_cases()
     rebatch_cases()
     gate_cases()
     simulate_cases()
     toy_bundle()
+    toy_chain()
+    metrics_cases()
     for p in sorted(OUT.glob("*.npz")) + sorted(OUT.glob("*.bin")):
         print(p.name, p.stat().st_size)

@@ -5,11 +5,21 @@ import os
 import numpy as np
 
 
+def bind_device(rank, world):
+    """Rank r on cuda:r when the box has a GPU per rank (then the IPC peer
+    buffers, peer stores and signal-pad barriers really cross NVLink);
+    otherwise every rank on cuda:0 (IPC within one GPU)."""
+    import torch
+    dev = rank if torch.cuda.device_count() >= world else 0
+    torch.cuda.set_device(dev)
+    return dev
+
+
 def layer_worker(rank, world, port, cfg_over, n, result_q):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(0)                      # every rank on one GPU (IPC still applies)
+    bind_device(rank, world)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2503_04398_b200 import SpecMoELayer, synth
@@ -39,7 +49,7 @@ def async_worker(rank, world, port, cfg_over, sizes, result_q):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(0)
+    bind_device(rank, world)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2503_04398_b200 import SpecMoELayer, synth
@@ -70,7 +80,7 @@ def capture_worker(rank, world, port, cfg_over, seeds, n, result_q):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(0)
+    bind_device(rank, world)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2503_04398_b200 import SpecMoELayer, synth
@@ -104,7 +114,7 @@ def microbatch_worker(rank, world, port, cfg_over, n, M, result_q):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(0)
+    bind_device(rank, world)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2503_04398_b200 import synth
@@ -123,5 +133,33 @@ def microbatch_worker(rank, world, port, cfg_over, n, M, result_q):
         result_q.put((rank, outs, hist))
         dist.barrier()
         grp.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def dsmoe_worker(rank, world, port, cfg_over, n, backend, result_q):
+    """DSMoELayer(distributed=True): one DS-MoE rank per process.  NCCL when
+    every rank has its own GPU; gloo (collectives staged through host
+    memory) when the ranks share one GPU."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = bind_device(rank, world)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2503_04398_b200 import synth
+        from paper_2503_04398_b200.baseline import DSMoELayer
+        w = synth.make_workload("toy", n=n, eps=0.3, seed=5, cfg_override=cfg_over)
+        layer = DSMoELayer(w.gate_w, w.w1, w.w3, w.w2, n_ranks=world, top_k=w.cfg["k"],
+                           max_tokens=n, distributed=True)
+        mine = torch.from_numpy(w.partials[rank]).to(torch.bfloat16).cuda()
+        outs = [layer.forward([mine], n).float().cpu().numpy() for _ in range(2)]
+        st = layer.stats()
+        result_q.put((rank, outs, (st["local_tokens"], st["remote_tokens"])))
+        dist.barrier()
     finally:
         dist.destroy_process_group()

@@ -97,3 +97,80 @@ def test_layer_oracle_identities():
     assert np.array_equal(ref["experts"], w.chosen)
     assert np.allclose(ref["h"], w.partials.sum(0), atol=0.05)
     assert ref["local"] + ref["remote"] == 200 * 2
+
+
+# ---------------------------------------------------------------- round 2 pins
+@pytest.mark.parametrize("c", cases("metrics"), ids=lambda c: "trace" if int(c["kind"]) else "matrix")
+def test_metrics_golden(c):
+    """solver.metrics (solver.py:766-800) restated; golden values from the
+    reference on its planted fixtures (truth / round-robin / solved)."""
+    if int(c["kind"]):
+        m = layer_ref.metrics(c["token_labels"], c["expert_labels"], tokens=c["tokens"],
+                              routed=c["routed"])
+    else:
+        m = layer_ref.metrics(c["token_labels"], c["expert_labels"], counts=c["counts"])
+    assert m["lar"] == float(c["lar"]) and m["imbalance"] == float(c["imbalance"])
+    assert m["events"] == int(c["events"]) and m["local_events"] == int(c["local_events"])
+
+
+def test_metrics_known_answer_truth():
+    # test_solver.py:342-351: truth assignment -> LAR 1.0, imbalance 1.0,
+    # events = k * L * occurrences
+    c = cases("metrics")[0]
+    m = layer_ref.metrics(c["token_labels"], c["expert_labels"], tokens=c["tokens"],
+                          routed=c["routed"])
+    assert m["lar"] == 1.0 and m["imbalance"] == 1.0
+    assert m["events"] == 2 * 3 * len(c["tokens"])
+
+
+def _chain(ci):
+    from golden_util import toy_bundle_path
+    from paper_2503_04398_b200 import tables
+    b = tables.read_bundle(toy_bundle_path(ci))
+    return b, cases("toy")[ci], cases("toy_chain")[ci]
+
+
+@pytest.mark.parametrize("ci", range(3))
+def test_toy_chain_oracle(ci):
+    """configs[0] three-layer chain: the oracle's lookup with the history
+    window it builds itself (next_window, depth-tracked: T-only until two
+    layers were observed) equals the reference's per-layer lookup / plan /
+    local events (tests/golden/toy_chain.npz)."""
+    b, toy, ch = _chain(ci)
+    tokens, routed = toy["tokens"], toy["routed"]
+    C = np.asarray(b.expert_labels, dtype=np.int64)
+    best, conf = R.ngram_best_conf(b.ngram_table.probs)
+    win, depth = None, 0
+    for layer in range(3):
+        lookup_hist = win if (win is not None and depth >= 2) else None
+        dev = R.lookup_devices(b.token_table.labels, b.token_table.confidence, best, conf, 2,
+                               tokens, lookup_hist)
+        pre = f"l{layer}_"
+        assert np.array_equal(dev, ch[pre + "dev"])
+        if lookup_hist is not None:
+            assert np.array_equal(lookup_hist, ch[pre + "hist"])
+        sh, fwd, inv, group = R.rebatch_tokens(tokens, dev, 2)
+        assert np.array_equal(fwd, ch[pre + "forward"]) and group == int(ch[pre + "group"])
+        assert R.count_local(routed[:, layer], C, dev) == int(ch[pre + "local"])
+        win, depth = layer_ref.next_window(win, depth, C[routed[:, layer, 0]], 2)
+
+
+def test_gate_topk_slot_space_ties():
+    """Ties are broken in s-EG slot space (test_acceptance.py:179-193): the
+    first k of a stable argsort of the SHUFFLED logits, remapped; -inf logits
+    remain candidates, so fewer than k finite logits still yield k experts."""
+    labels = np.array([1, 0, 1, 0])             # slot order: experts 1, 3, 0, 2
+    n2o, _ = R.gate_permutation(labels, 2)
+    assert n2o.tolist() == [1, 3, 0, 2]
+    logits = np.array([[1.0, 1.0, 0.0, 0.0],    # 0 and 1 tie: expert 1 (slot 0) before 0 (slot 2)
+                       [0.0, 2.0, 0.0, 2.0],    # 1 and 3 tie: expert 1 (slot 0) first
+                       [-np.inf, -np.inf, 5.0, -np.inf],
+                       [-np.inf] * 4])
+    ids, w, _ = layer_ref.gate_topk(None, None, 2, True, new_to_old=n2o, logits=logits)
+    assert ids[0].tolist() == [1, 0] and ids[1].tolist() == [1, 3]
+    assert ids[2].tolist() == [2, 1]            # finite first, then the lowest -inf SLOT
+    assert ids[3].tolist() == [1, 3]
+    assert w[2].tolist() == [1.0, 0.0]
+    # identity slot order = the reference's argsort over original ids
+    ids, _, _ = layer_ref.gate_topk(None, None, 2, True, logits=logits)
+    assert ids[0].tolist() == [0, 1] and ids[2].tolist() == [2, 0]
