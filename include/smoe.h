@@ -67,10 +67,6 @@ const char* smoe_version(void);
 #define SMOE_OPT_GEMM_NARROW_MAX_ROWS 6 /* layer GEMMs: 32-row m-blocks, 5-stage     */
                                         /* weight ring while n*k <= this * n_experts */
                                         /* (default 0 = off)                         */
-#define SMOE_OPT_GATE_SPLIT          7  /* tcgen05 gate: 1 = logits kernel + warp-per-row */
-                                        /* selection kernel (default; env            */
-                                        /* SMOE_GATE_SPLIT=0 to start with 0), 0 =   */
-                                        /* selection in the MMA kernel's epilogue    */
 int smoe_set_option(int32_t key, int32_t value);
 int smoe_get_option(int32_t key);
 const char* smoe_status_string(int status);
@@ -238,6 +234,10 @@ enum {
                           /* next layer's n-gram window = this window shifted by one  */
                           /* plus the cluster of each token's top-1 expert            */
                           /* (predictor.py:165-166)                                   */
+  SMOE_BUF_AR,            /* bf16 [max_tokens, d], per process (bind for every shard; */
+                          /* co-resident shards share): DS-MoE all-reduce output     */
+  SMOE_BUF_AG,            /* bf16 [ag_rows, d], per process: DS-MoE all-gather of the */
+                          /* combined token groups (row g * group + j)               */
   SMOE_BUF__COUNT
 };
 
@@ -258,6 +258,19 @@ int smoe_layer_create(const smoe_layer_config* cfg, smoe_layer** out);
 void smoe_layer_destroy(smoe_layer* layer);
 /* Bind a device buffer (see SMOE_BUF_*). */
 int smoe_layer_bind(smoe_layer* layer, int32_t slot, int32_t index, void* ptr);
+
+/* Pipeline structure.  SMOE_PIPELINE_SMOE (default): the speculative
+ * pipeline SRS -> A2A -> A2A -> SAG.  SMOE_PIPELINE_DSMOE:
+ * the DS-MoE baseline structure AR -> A2A -> A2A -> AG (comm.py:99-108) on
+ * the same kernels -- the SRS stage becomes a two-shot all-reduce into
+ * SMOE_BUF_AR plus each rank's slice of it, and COMBINE_SAG combines into
+ * the SMOE_BUF_AG all-gather blocks (G * group <= ag_rows, else
+ * SMOE_ERRBIT_CAPACITY) followed by a local resume gather into SMOE_BUF_OUT.
+ * Paired with position-sharding tables (token i -> shard i % G, comm.py:202)
+ * and contiguous expert blocks (comm.py:201).  Bind AR / AG first. */
+#define SMOE_PIPELINE_SMOE  0
+#define SMOE_PIPELINE_DSMOE 1
+int smoe_layer_set_pipeline(smoe_layer* layer, int32_t pipeline, int64_t ag_rows);
 
 /* Lookup tables (predictor.py:39-82) and the s-EG expert placement
  * (scheduler.py:200-224).  slot_owner[N]: cluster (= shard) that owns expert

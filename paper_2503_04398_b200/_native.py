@@ -43,6 +43,7 @@ SIGNATURES = [
     ("smoe_layer_bind", C.c_int, [P, c_i32, c_i32, P]),
     ("smoe_layer_set_tables", C.c_int, [P, P, P, c_i64, P, P, c_i64, c_i32, P]),
     ("smoe_layer_set_weights", C.c_int, [P, P, P, P, P]),
+    ("smoe_layer_set_pipeline", C.c_int, [P, c_i32, c_i64]),
     ("smoe_layer_set_weights_tiled", C.c_int, [P, P, P, P, P]),
     ("smoe_tile_weights", C.c_int, [P, c_i64, c_i64, P, P]),
     ("smoe_srs", C.c_int, [P, c_i32, c_i32, c_i32, P, P, P, c_i64, c_i32, P, P]),
@@ -81,12 +82,12 @@ OPT_GEMM_PAIR_MIN_ROWS = 3
 OPT_PDL = 4
 OPT_PDL_STAGES = 5
 OPT_GEMM_NARROW_MAX_ROWS = 6
-OPT_GATE_SPLIT = 7
 
 (BUF_PARTIAL, BUF_XIN, BUF_XMETA, BUF_YPAIR, BUF_OUT, BUF_COUNTS, BUF_SIGNAL, BUF_HS,
  BUF_TOPK_IDS, BUF_TOPK_W, BUF_PAIR_RANK, BUF_HMID, BUF_FORWARD, BUF_INVERSE, BUF_DEV,
  BUF_PLAN_COUNTS, BUF_GROUP, BUF_STATS, BUF_ERR, BUF_WORKSPACE, BUF_PROBLEMS,
- BUF_EPOCH, BUF_HIST_OUT) = range(23)
+ BUF_EPOCH, BUF_HIST_OUT, BUF_AR, BUF_AG) = range(25)
+PIPELINE_SMOE, PIPELINE_DSMOE = 0, 1
 STAT_LOCAL_PAIRS, STAT_REMOTE_PAIRS, STAT_SRS_ROWS, STAT_GROUP, STAT_REMOTE_ROWS = range(5)
 STAT_COUNT = 16
 (STAGE_PLAN, STAGE_SRS, STAGE_GATE, STAGE_ROUTE, STAGE_DISPATCH, STAGE_EXPERT_UP,

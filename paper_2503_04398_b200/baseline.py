@@ -157,13 +157,14 @@ class DSMoELayer:
             import torch.distributed as dist
             r = self.rank
             if self._staged():
-                src = self.buf[r][name_in][: int(sum(send_splits[r]))].view(t.int16).cpu()
-                dst = t.empty((int(sum(recv_splits[r])), self.d), dtype=t.int16)
+                # gloo moves no 16-bit types: ship the bf16 rows as bytes
+                src = self.buf[r][name_in][: int(sum(send_splits[r]))].view(t.uint8).cpu()
+                dst = t.empty((int(sum(recv_splits[r])), 2 * self.d), dtype=t.uint8)
                 dist.all_to_all_single(dst, src,
                                        output_split_sizes=[int(x) for x in recv_splits[r]],
                                        input_split_sizes=[int(x) for x in send_splits[r]],
                                        group=self.pg)
-                self.buf[r][name_out][: dst.shape[0]].view(t.int16).copy_(dst)
+                self.buf[r][name_out][: dst.shape[0]].view(t.uint8).copy_(dst)
                 return
             dist.all_to_all_single(self.buf[r][name_out][: int(sum(recv_splits[r]))],
                                    self.buf[r][name_in][: int(sum(send_splits[r]))],
@@ -186,7 +187,7 @@ class DSMoELayer:
         if self.distributed:
             import torch.distributed as dist
             if self._staged():
-                mine = self.buf[self.rank]["out"][:group].view(t.int16).cpu()
+                mine = self.buf[self.rank]["out"][:group].view(t.uint8).cpu()
                 parts = [t.empty_like(mine) for _ in range(self.G)]
                 dist.all_gather(parts, mine, group=self.pg)
                 return t.cat(parts).to(self.w_gate.device).view(t.bfloat16)

@@ -17,7 +17,12 @@
 //   warps 4..7     epilogue, ONE THREAD PER ROW: tcgen05.ld 32x32b gives the
 //                  thread its row's N' logits in registers; bias, max, softmax
 //                  sum, top-k (larger logit first, lowest s-EG slot on ties) and
-//                  the locality count need no shuffles or shared memory.
+//                  the locality count need no shuffles or shared memory.  Each
+//                  of the k selections is a max-TREE over the N' logits (depth
+//                  log2 N', independent compares) instead of a linear scan:
+//                  the scan was a 64-long dependent chain per pass and one
+//                  warp per SMSP could not hide it (12 us of a 24 us decode
+//                  gate at N = 64, k = 6).
 //
 // N' = N rounded up to 16 (the MMA's N granularity at M = 128); W rows past
 // N are TMA out-of-bounds fills (zeros) and are masked to -inf.  Rows past a
@@ -54,7 +59,7 @@ template <int NP, int SUB, int ST> struct GtShape {
                                      (uint32_t(NP >> 3) << 17) | (uint32_t(kGtRows >> 4) << 24);
 };
 
-template <int NP, int SUB, int ST, bool LOGITS>
+template <int NP, int SUB, int ST>
 __global__ void __launch_bounds__(kGtThreads, 1)
 gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
                const __grid_constant__ CUtensorMap tmap_w, const GateTcArgs a) {
@@ -224,65 +229,65 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
 
       const int64_t j = (int64_t)blk * kGtRows + ew * 32 + lane;
       if (j >= s_cnt[gl]) continue;
-      // NaN marks "not a candidate" (slots past N, experts already taken):
-      // every comparison with it is false, so -inf logits stay ordinary
-      // candidates and fewer than k finite logits still yield k distinct
+      // order-preserving int keys (+0 and -0 merged, -inf an ordinary
+      // candidate); INT_MIN marks "not a candidate" (slots >= N, slots
+      // already taken), so fewer than k finite logits still give k distinct
       // slots, as the stable argsort of the reference idiom does
-      if constexpr (LOGITS) {
-        // split gate: biased logits out, selection in gate_select_kernel
-        float* dst = a.logits + ((int64_t)gl * a.rows_per_shard + j) * N;
-        if ((N & 3) == 0) {
+      constexpr int NT = NP <= 16 ? 16 : (NP <= 32 ? 32 : 64);   // tree leaves (power of 2)
+      int32_t key[NT];
 #pragma unroll
-          for (int e = 0; e < NP; e += 4)
-            if (e < N)
-              *reinterpret_cast<float4*>(dst + e) =
-                  make_float4(__uint_as_float(v[e]) + s_bias[e],
-                              __uint_as_float(v[e + 1]) + s_bias[e + 1],
-                              __uint_as_float(v[e + 2]) + s_bias[e + 2],
-                              __uint_as_float(v[e + 3]) + s_bias[e + 3]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < NP; ++e)
-            if (e < N) dst[e] = __uint_as_float(v[e]) + s_bias[e];
-        }
-        continue;
+      for (int e = 0; e < NT; ++e) {
+        const int32_t b = e < NP ? __float_as_int(__uint_as_float(v[e]) + s_bias[e] + 0.0f) : 0;
+        key[e] = e < N ? (b >= 0 ? b : b ^ 0x7fffffff) : INT_MIN;
       }
-      float lg[NP];
-      float mx = -INFINITY;
-#pragma unroll
-      for (int e = 0; e < NP; ++e) {
-        lg[e] = e < N ? __uint_as_float(v[e]) + s_bias[e] : __int_as_float(0x7fffffff);
-        mx = fmaxf(mx, lg[e]);
-      }
-      float ex = 0.f;
-#pragma unroll
-      for (int e = 0; e < NP; ++e) ex += e < N ? __expf(lg[e] - mx) : 0.f;
-      const float inv = 1.0f / ex;
       int sel_e[kGtMaxK];
-      float sel_p[kGtMaxK];
-      float psum = 0.f;
-      // fully unrolled over k x N' (a rolled selection loop is 13% faster at
-      // 64 tokens but 30-40% slower at 16-64K tokens, where the epilogue
-      // overlaps the next tile's MMAs and must keep up)
+      int32_t sel_k[kGtMaxK];
+      uint64_t taken = 0;      // a bit mask, not stores into key[]: a store at the
+                               // winner's index became local memory (STL)
 #pragma unroll
       for (int s = 0; s < kGtMaxK; ++s) {
         sel_e[s] = 0;
-        sel_p[s] = 0.f;
+        sel_k[s] = INT_MIN;
         if (s < K) {
-          // descending scan with >=: the largest logit, lowest slot on exact
-          // ties (ties broken in s-EG slot space, test_acceptance.py:179-193)
-          float bv = -INFINITY;
-          int bi = 0;
+          // max-tree: the right child wins only when strictly larger, so
+          // equal logits resolve to the lower s-EG slot (test_acceptance.py:179-193)
+          int32_t tv[NT / 2];
+          int ti[NT / 2];
 #pragma unroll
-          for (int e = NP - 1; e >= 0; --e)
-            if (lg[e] >= bv) { bv = lg[e]; bi = e; }
+          for (int i = 0; i < NT / 2; ++i) {
+            const int32_t k0 = ((taken >> (2 * i)) & 1) ? INT_MIN : key[2 * i];
+            const int32_t k1 = ((taken >> (2 * i + 1)) & 1) ? INT_MIN : key[2 * i + 1];
+            const bool r = k1 > k0;
+            tv[i] = r ? k1 : k0;
+            ti[i] = r ? 2 * i + 1 : 2 * i;
+          }
 #pragma unroll
-          for (int e = 0; e < NP; ++e)
-            if (e == bi) lg[e] = __int_as_float(0x7fffffff);
-          sel_e[s] = bi;
-          sel_p[s] = __expf(bv - mx) * inv;
-          psum += sel_p[s];
+          for (int w = NT / 4; w >= 1; w >>= 1) {
+#pragma unroll
+            for (int i = 0; i < w; ++i) {
+              const bool r = tv[2 * i + 1] > tv[2 * i];
+              tv[i] = r ? tv[2 * i + 1] : tv[2 * i];
+              ti[i] = r ? ti[2 * i + 1] : ti[2 * i];
+            }
+          }
+          sel_e[s] = ti[0];
+          sel_k[s] = tv[0];
+          taken |= 1ull << ti[0];
         }
+      }
+      auto key_to_f = [](int32_t k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); };
+      const float mx = key_to_f(sel_k[0]);
+      float ex = 0.f;
+#pragma unroll
+      for (int e = 0; e < NP; ++e)
+        if (e < N) ex += __expf(__uint_as_float(v[e]) + s_bias[e] - mx);
+      const float inv = 1.0f / ex;
+      float sel_p[kGtMaxK];
+      float psum = 0.f;
+#pragma unroll
+      for (int s = 0; s < kGtMaxK; ++s) {
+        sel_p[s] = s < K ? __expf(key_to_f(sel_k[s]) - mx) * inv : 0.f;
+        psum += sel_p[s];
       }
       const int32_t g = a.shard_begin + gl;
       int32_t* ids = reinterpret_cast<int32_t*>(s_ids[gl]) + j * K;
@@ -329,29 +334,21 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
   }
 }
 
-template <int NP, int SUB, int ST, bool LOGITS>
-static int launch_cfg_l(const CUtensorMap& mh, const CUtensorMap& mw, const GateTcArgs& a,
-                        int64_t n_rows_bound, cudaStream_t st) {
+template <int NP, int SUB, int ST>
+static int launch_cfg(const CUtensorMap& mh, const CUtensorMap& mw, const GateTcArgs& a,
+                      int64_t n_rows_bound, cudaStream_t st) {
   using S = GtShape<NP, SUB, ST>;
   static bool attr = false;
   if (!attr) {
-    SMOE_CUDA_TRY(cudaFuncSetAttribute(gate_tc_kernel<NP, SUB, ST, LOGITS>,
+    SMOE_CUDA_TRY(cudaFuncSetAttribute(gate_tc_kernel<NP, SUB, ST>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::kSmem));
     attr = true;
   }
   const int64_t tiles = ceil_div(n_rows_bound, kGtRows) + a.shard_count;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms()));
-  SMOE_CUDA_TRY(launch_pdl(gate_tc_kernel<NP, SUB, ST, LOGITS>, grid, kGtThreads, S::kSmem, st,
-                           mh, mw, a));
+  SMOE_CUDA_TRY(launch_pdl(gate_tc_kernel<NP, SUB, ST>, grid, kGtThreads, S::kSmem, st, mh, mw, a));
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
-}
-
-template <int NP, int SUB, int ST>
-static int launch_cfg(const CUtensorMap& mh, const CUtensorMap& mw, const GateTcArgs& a,
-                      int64_t n_rows_bound, cudaStream_t st) {
-  return a.logits ? launch_cfg_l<NP, SUB, ST, true>(mh, mw, a, n_rows_bound, st)
-                  : launch_cfg_l<NP, SUB, ST, false>(mh, mw, a, n_rows_bound, st);
 }
 
 // Ring shape (SMOE_GATE_RING=<k-blocks per stage>x<stages>, tuning only):

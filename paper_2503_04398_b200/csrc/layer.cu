@@ -46,6 +46,10 @@ struct smoe_layer {
   // tensor-core gate: hidden rows of the resident shards (one arena) and W_g
   bool gate_tc = false;
   CUtensorMap map_hs, map_wg;
+  // SMOE_PIPELINE_DSMOE: all-reduce + slice instead of SRS, combine into
+  // all-gather blocks + resume gather instead of the fused SAG
+  int32_t pipeline = SMOE_PIPELINE_SMOE;
+  int64_t ag_rows = 0;
 };
 
 static bool valid_cfg(const smoe_layer_config* c) {
@@ -60,18 +64,10 @@ static size_t plan_ws_aligned(const smoe_layer_config* cfg) {
   return (smoe_plan_workspace_bytes(cfg->max_tokens, cfg->n_shards) + 255) & ~size_t(255);
 }
 
-// split gate logits [shard_count * max_tokens, N] fp32 after the plan and
-// route scratch
-static size_t gate_ws_offset(const smoe_layer_config* cfg) {
-  return (plan_ws_aligned(cfg) +
-          route_workspace_bytes(cfg->max_tokens, cfg->top_k, cfg->n_experts, cfg->shard_count) +
-          255) & ~size_t(255);
-}
-
 extern "C" size_t smoe_layer_workspace_bytes(const smoe_layer_config* cfg) {
   if (!cfg) return 0;
-  return gate_ws_offset(cfg) +
-         sizeof(float) * (size_t)cfg->shard_count * cfg->max_tokens * cfg->n_experts;
+  return plan_ws_aligned(cfg) +
+         route_workspace_bytes(cfg->max_tokens, cfg->top_k, cfg->n_experts, cfg->shard_count);
 }
 
 extern "C" int smoe_layer_create(const smoe_layer_config* cfg, smoe_layer** out) {
@@ -137,6 +133,20 @@ extern "C" int smoe_layer_set_tables(smoe_layer* L, const int16_t* t_labels, con
   return SMOE_OK;
 }
 
+extern "C" int smoe_layer_set_pipeline(smoe_layer* L, int32_t pipeline, int64_t ag_rows) {
+  if (!L) return SMOE_ERR_INVALID_ARG;
+  if (pipeline == SMOE_PIPELINE_SMOE) {
+    L->pipeline = pipeline;
+    return SMOE_OK;
+  }
+  if (pipeline != SMOE_PIPELINE_DSMOE || ag_rows <= 0) return SMOE_ERR_INVALID_ARG;
+  for (int g = 0; g < L->cfg.n_shards; ++g)
+    if (!L->buf[SMOE_BUF_AR][g] || !L->buf[SMOE_BUF_AG][g]) return SMOE_ERR_INVALID_ARG;
+  L->pipeline = pipeline;
+  L->ag_rows = ag_rows;
+  return SMOE_OK;
+}
+
 extern "C" int smoe_layer_set_weights(smoe_layer* L, const void* w_gate, const float* b_gate,
                                       const void* w13, const void* w2) {
   if (!L || !w_gate || !w13 || !w2) return SMOE_ERR_INVALID_ARG;
@@ -182,6 +192,16 @@ static ShardPtrs distinct_ptrs(const smoe_layer* L, int slot, int32_t* count) {
     if (!seen) p.p[n++] = q;
   }
   *count = n;
+  return p;
+}
+
+// distinct buffers of a per-process slot, this process's own first (kernels
+// that re-read what they stored read the local copy, not a peer's)
+static ShardPtrs distinct_ptrs_local_first(const smoe_layer* L, int slot, int32_t* count) {
+  ShardPtrs p = distinct_ptrs(L, slot, count);
+  char* mine = static_cast<char*>(L->buf[slot][L->cfg.shard_begin]);
+  for (int i = 1; i < *count; ++i)
+    if (p.p[i] == mine) { p.p[i] = p.p[0]; p.p[0] = mine; }
   return p;
 }
 
@@ -366,6 +386,20 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       // reads them (and the previous batch's reads ended at its ROUTE barrier)
       rc = smoe_layer_barrier(L, stream);
       if (rc) return rc;
+      if (L->pipeline == SMOE_PIPELINE_DSMOE) {
+        // DS-MoE: every process receives the full sum (two-shot all-reduce),
+        // then each rank takes its own rows of it
+        int32_t n_ar = 0;
+        const ShardPtrs ar = distinct_ptrs_local_first(L, SMOE_BUF_AR, &n_ar);
+        rc = launch_allreduce(peer_ptrs(L, SMOE_BUF_PARTIAL), c.hidden, n, c.shard_begin,
+                              c.shard_count, c.n_shards, ar, n_ar, st);
+        if (rc) return rc;
+        rc = smoe_layer_barrier(L, stream);
+        if (rc) return rc;
+        ShardPtrs src{};
+        src.p[0] = ar.p[0];
+        return launch_srs(lr, src, c.hidden, local_ptrs(L, SMOE_BUF_HS), n, st, 1);
+      }
       return launch_srs(lr, peer_ptrs(L, SMOE_BUF_PARTIAL), c.hidden, local_ptrs(L, SMOE_BUF_HS),
                         n, st);
     case SMOE_STAGE_GATE:
@@ -384,17 +418,6 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
         g.topk_ids = local_ptrs(L, SMOE_BUF_TOPK_IDS);
         g.topk_w = local_ptrs(L, SMOE_BUF_TOPK_W);
         g.stats = stats;
-        if (gate_split_enabled()) {
-          // logits (tensor cores, HBM-bound) then selection (warp per row)
-          g.logits = reinterpret_cast<float*>(static_cast<char*>(L->buf[SMOE_BUF_WORKSPACE][0]) +
-                                              gate_ws_offset(&c));
-          rc = launch_gate_tc(L->map_hs, L->map_wg, g, n, st);
-          if (rc) return rc;
-          return launch_gate_select(lr, g.logits, c.max_tokens, c.n_experts, c.top_k,
-                                    c.renormalize, L->slot_owner_d,
-                                    local_ptrs(L, SMOE_BUF_TOPK_IDS),
-                                    local_ptrs(L, SMOE_BUF_TOPK_W), stats, n, st);
-        }
         return launch_gate_tc(L->map_hs, L->map_wg, g, n, st);
       }
       return launch_gate(lr, local_ptrs(L, SMOE_BUF_HS), c.hidden, L->w_gate, L->b_gate,
@@ -472,6 +495,20 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       // SAG: each token's row goes once to every distinct output buffer (one
       // per process: co-resident shards share their process's output)
       int32_t n_outs = 0;
+      if (L->pipeline == SMOE_PIPELINE_DSMOE) {
+        // DS-MoE: combine into every process's all-gather buffer at the
+        // token's block slot, then restore the original order locally
+        const ShardPtrs ag = distinct_ptrs_local_first(L, SMOE_BUF_AG, &n_outs);
+        rc = launch_combine_sag(lr, c.top_k, c.hidden, resident_ptrs(L, SMOE_BUF_YPAIR),
+                                local_ptrs(L, SMOE_BUF_TOPK_W), ag, n_outs, hu, n, st,
+                                L->ag_rows, err);
+        if (rc) return rc;
+        rc = smoe_layer_barrier(L, stream);
+        if (rc) return rc;
+        return smoe_gather_rows(ag.p[0], L->ag_rows, 2, c.hidden,
+                                static_cast<const int64_t*>(L->buf[SMOE_BUF_INVERSE][0]), n, 0,
+                                0, L->buf[SMOE_BUF_OUT][c.shard_begin], err, stream);
+      }
       const ShardPtrs outs = distinct_ptrs(L, SMOE_BUF_OUT, &n_outs);
       rc = launch_combine_sag(lr, c.top_k, c.hidden, resident_ptrs(L, SMOE_BUF_YPAIR),
                               local_ptrs(L, SMOE_BUF_TOPK_W), outs, n_outs, hu, n, st);
@@ -560,10 +597,6 @@ extern "C" int smoe_set_option(int32_t key, int32_t value) {
       if (value < 0) return SMOE_ERR_INVALID_ARG;
       set_gemm_narrow_max_rows(value);
       return SMOE_OK;
-    case SMOE_OPT_GATE_SPLIT:
-      if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
-      set_gate_split_enabled(value);
-      return SMOE_OK;
     case SMOE_OPT_PDL:
       if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
       set_pdl_enabled(value);
@@ -584,7 +617,6 @@ extern "C" int smoe_get_option(int32_t key) {
   if (key == SMOE_OPT_GEMM_PAIR_MIN_ROWS) return gemm_pair_min_rows();
   if (key == SMOE_OPT_GEMM_NARROW_MAX_ROWS) return gemm_narrow_max_rows();
   if (key == SMOE_OPT_PDL) return pdl_enabled();
-  if (key == SMOE_OPT_GATE_SPLIT) return gate_split_enabled();
   if (key == SMOE_OPT_PDL_STAGES) return pdl_stage_mask();
   return -1;
 }

@@ -21,6 +21,7 @@
 //                          shuffled all-gather: one store per shard straight
 //                          to the token's original position (resume fused)
 #include "layer_kernels.cuh"
+#include "gate_select.cuh"
 #include <algorithm>
 #include <cstdlib>
 
@@ -172,12 +173,12 @@ srs_kernel(LocalRows lr, ShardPtrs partials, int64_t d, ShardPtrs hs, int32_t wh
 }
 
 int launch_srs(const LocalRows& lr, const ShardPtrs& partials, int64_t d, const ShardPtrs& hs,
-               int64_t n_rows_bound, cudaStream_t st) {
+               int64_t n_rows_bound, cudaStream_t st, int32_t n_sources) {
   if (d % 8) return SMOE_ERR_UNSUPPORTED;
   if (n_rows_bound <= 0) return SMOE_OK;
   const int grid = grid_items(n_rows_bound, d);
   const int32_t wr = whole_rows_from();
-  switch (lr.n_shards) {
+  switch (n_sources > 0 ? n_sources : lr.n_shards) {
 #define SMOE_SRS_CASE(G_) \
     case G_: SMOE_CUDA_TRY(launch_pdl(srs_kernel<G_>, grid, 256, 0, st, lr, partials, d, hs, wr)); break;
     SMOE_SRS_CASE(1) SMOE_SRS_CASE(2) SMOE_SRS_CASE(3) SMOE_SRS_CASE(4) SMOE_SRS_CASE(5)
@@ -191,165 +192,78 @@ int launch_srs(const LocalRows& lr, const ShardPtrs& partials, int64_t d, const 
   return SMOE_OK;
 }
 
+// ------------------------------------------------------------------ DS-MoE all-reduce
+// The DS-MoE baseline's all-reduce (comm.py:99-108, two-shot: reduce-scatter
+// + all-gather, 2(G-1)/G of the batch per GPU like the reference's volume
+// model): shard g sums rows [g*c, (g+1)*c) of the G partials (c = ceil(n/G),
+// natural token order) and stores them into every process's all-reduce
+// buffer.  The ranks then use their own rows of the full sum (launch_srs
+// with one source), where the s-MoE SRS delivers only a shard's own group.
+template <int G>
+__global__ void __launch_bounds__(256)
+allreduce_kernel(ShardPtrs partials, int64_t d, int64_t n, int32_t shard_begin,
+                 int32_t shard_count, int32_t n_shards, ShardPtrs outs, int32_t n_outs,
+                 int32_t whole_rows) {
+  pdl_enter();
+  __shared__ char* s_out[SMOE_MAX_SHARDS];
+  stage_ptrs(s_out, outs);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t vecs = d / 8;
+  const int64_t c = (n + n_shards - 1) / n_shards;
+  const int64_t r0 = min(n, (int64_t)shard_begin * c);
+  const int64_t rows = min(n, (int64_t)(shard_begin + shard_count) * c) - r0;
+  const bool whole = rows >= whole_rows;
+  const int64_t chunks = whole ? 1 : (vecs + kChunkVecs - 1) / kChunkVecs;
+  const int64_t cv = whole ? vecs : kChunkVecs;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const char* src_base[G];
+#pragma unroll
+  for (int r = 0; r < G; ++r) src_base[r] = partials.p[r];
+  for (int64_t it = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+       it < rows * chunks; it += nwarps) {
+    const int64_t q = whole ? it : it / chunks, ch = it - q * chunks;
+    const int64_t row = r0 + q;
+    char* first = s_out[0] + row * d * 2;
+    srs_span<G>(src_base, row * d * 2, first, ch * cv, min(vecs, (ch + 1) * cv), lane);
+    if (n_outs > 1) {
+      __syncwarp();
+      for (int64_t v = ch * cv + lane; v < min(vecs, (ch + 1) * cv); v += 32) {
+        const uint4 x = ld_v4(first + v * 16);
+        for (int o = 1; o < n_outs; ++o) st_v4(s_out[o] + (row * d + v * 8) * 2, x);
+      }
+    }
+  }
+}
+
+int launch_allreduce(const ShardPtrs& partials, int64_t d, int64_t n, int32_t shard_begin,
+                     int32_t shard_count, int32_t n_shards, const ShardPtrs& outs,
+                     int32_t n_outs, cudaStream_t st) {
+  if (d % 8) return SMOE_ERR_UNSUPPORTED;
+  if (n <= 0) return SMOE_OK;
+  const int64_t c = (n + n_shards - 1) / n_shards;
+  const int grid = grid_items(c * shard_count, d);
+  const int32_t wr = whole_rows_from();
+  switch (n_shards) {
+#define SMOE_AR_CASE(G_) \
+    case G_: SMOE_CUDA_TRY(launch_pdl(allreduce_kernel<G_>, grid, 256, 0, st, partials, d, n, \
+                                      shard_begin, shard_count, n_shards, outs, n_outs, wr)); break;
+    SMOE_AR_CASE(1) SMOE_AR_CASE(2) SMOE_AR_CASE(3) SMOE_AR_CASE(4) SMOE_AR_CASE(5)
+    SMOE_AR_CASE(6) SMOE_AR_CASE(7) SMOE_AR_CASE(8) SMOE_AR_CASE(9) SMOE_AR_CASE(10)
+    SMOE_AR_CASE(11) SMOE_AR_CASE(12) SMOE_AR_CASE(13) SMOE_AR_CASE(14) SMOE_AR_CASE(15)
+    SMOE_AR_CASE(16)
+#undef SMOE_AR_CASE
+    default: return SMOE_ERR_UNSUPPORTED;
+  }
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
 // ------------------------------------------------------------------ K4 gate
 constexpr int kGateRows = 32;
 constexpr int kGateKC = 128;                 // hidden elements per smem chunk
 constexpr int kGateWords = kGateKC / 2;      // bf16x2 words per row chunk
 constexpr int kGatePad = kGateWords + 1;     // conflict-free row stride (words)
-constexpr int kGateMaxN = 64;
-constexpr int kGateMaxK = 8;
-
-// Softmax + ordered top-k of one row with a warp: lane holds the logits of
-// slots `lane` (v0) and `lane + 32` (v1), NaN for slots >= N.  Larger logit
-// first, lowest slot on exact ties (the stable argsort of -logits over the
-// s-EG slot order, test_acceptance.py:179-193); NaN marks "not a candidate"
-// (slots >= N, slots already taken), so -inf logits stay candidates and fewer
-// than k finite logits still give k distinct slots.  Every lane returns the
-// same selection.
-__device__ __forceinline__ void warp_topk(float v0, float v1, int32_t N, int32_t k,
-                                          int lane, int (&sel_e)[kGateMaxK],
-                                          float (&sel_p)[kGateMaxK], float& psum) {
-  float mx = fmaxf(v0, v1);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  float ex = (lane < N ? __expf(v0 - mx) : 0.f) + (lane + 32 < N ? __expf(v1 - mx) : 0.f);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) ex += __shfl_xor_sync(0xffffffffu, ex, o);
-  const float inv = 1.0f / ex;
-  psum = 0.f;
-#pragma unroll
-  for (int s = 0; s < kGateMaxK; ++s) {
-    sel_e[s] = 0;
-    sel_p[s] = 0.f;
-    if (s < k) {
-      float bv; int bi;
-      if (v1 == v1 && !(v0 >= v1)) { bv = v1; bi = lane + 32; }
-      else if (v0 == v0) { bv = v0; bi = lane; }
-      else { bv = -INFINITY; bi = 1 << 20; }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-      }
-      sel_e[s] = bi;
-      sel_p[s] = __expf(bv - mx) * inv;
-      psum += sel_p[s];
-      if (bi == lane) v0 = __int_as_float(0x7fffffff);
-      if (bi == lane + 32) v1 = __int_as_float(0x7fffffff);
-    }
-  }
-}
-
-// Lane s < k of the warp stores selection s of row j of local shard gl and
-// counts its pair as local / remote (and whether it is the first pair of
-// the row to that remote shard).
-__device__ __forceinline__ void warp_store_topk(int lane, int32_t k, int32_t renorm,
-                                                const int (&sel_e)[kGateMaxK],
-                                                const float (&sel_p)[kGateMaxK], float psum,
-                                                int32_t* ids, float* wts, int64_t g,
-                                                const int32_t* slot_owner,
-                                                unsigned long long& my_local,
-                                                unsigned long long& my_remote,
-                                                unsigned long long& my_rrows) {
-  if (lane >= k) return;
-  float p = 0.f; int e = 0;
-#pragma unroll
-  for (int s = 0; s < kGateMaxK; ++s) if (s == lane) { p = sel_p[s]; e = sel_e[s]; }
-  ids[lane] = e;
-  wts[lane] = renorm ? p / psum : p;
-  const int32_t o = slot_owner[e];
-  if (o == g) {
-    ++my_local;
-  } else {
-    ++my_remote;
-    bool seen = false;                               // first pair to this shard?
-#pragma unroll
-    for (int s2 = 0; s2 < kGateMaxK; ++s2)
-      if (s2 < lane) seen |= slot_owner[sel_e[s2]] == o;
-    if (!seen) ++my_rrows;
-  }
-}
-
-__device__ __forceinline__ void flush_pair_stats(unsigned long long my_local,
-                                                 unsigned long long my_remote,
-                                                 unsigned long long my_rrows, int64_t* stats) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    my_local += __shfl_xor_sync(0xffffffffu, my_local, o);
-    my_remote += __shfl_xor_sync(0xffffffffu, my_remote, o);
-    my_rrows += __shfl_xor_sync(0xffffffffu, my_rrows, o);
-  }
-  if ((threadIdx.x & 31) == 0 && stats && (my_local | my_remote)) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_LOCAL_PAIRS), my_local);
-    atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_REMOTE_PAIRS), my_remote);
-    atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_REMOTE_ROWS), my_rrows);
-  }
-}
-
-// Second half of the split tensor-core gate: the tcgen05 kernel streams the
-// hidden rows through the MMA and stores the biased logits (fp32, N per row,
-// ~4-32 MB for 16K tokens -- a few % of the bytes it read); here a warp per
-// row does softmax, top-k and the locality count.  Selection is a chain of k
-// dependent passes: one thread per row (the fused epilogue) left only 4 warps
-// per SM to hide it, 12 us of a 27 us DeepSeek-V2-Lite gate at 16K tokens.
-__global__ void __launch_bounds__(256)
-gate_select_kernel(LocalRows lr, const float* __restrict__ logits, int64_t rows_per_shard,
-                   int32_t N, int32_t k, int32_t renorm, const int32_t* __restrict__ slot_owner,
-                   ShardPtrs topk_ids, ShardPtrs topk_w, int64_t* stats) {
-  pdl_enter();
-  __shared__ RowMap rm;
-  __shared__ char* s_ids[SMOE_MAX_SHARDS];
-  __shared__ char* s_wts[SMOE_MAX_SHARDS];
-  __shared__ int32_t s_owner[kGateMaxN];
-  stage_ptrs(s_ids, topk_ids);
-  stage_ptrs(s_wts, topk_w);
-  if (threadIdx.x < kGateMaxN) s_owner[threadIdx.x] = threadIdx.x < N ? slot_owner[threadIdx.x] : -1;
-  load_rowmap(rm, lr);
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t w0 = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  unsigned long long my_local = 0, my_remote = 0, my_rrows = 0;
-  for (int64_t q = w0; q < rm.total; q += nwarps) {
-    int32_t gl; int64_t j;
-    decode_row(rm, lr.shard_count, q, gl, j);
-    const float* lg = logits + (gl * rows_per_shard + j) * N;
-    const float v0 = lane < N ? __ldg(lg + lane) : __int_as_float(0x7fffffff);
-    const float v1 = lane + 32 < N ? __ldg(lg + lane + 32) : __int_as_float(0x7fffffff);
-    int sel_e[kGateMaxK];
-    float sel_p[kGateMaxK];
-    float psum;
-    warp_topk(v0, v1, N, k, lane, sel_e, sel_p, psum);
-    warp_store_topk(lane, k, renorm, sel_e, sel_p, psum,
-                    reinterpret_cast<int32_t*>(s_ids[gl]) + j * k,
-                    reinterpret_cast<float*>(s_wts[gl]) + j * k, lr.shard_begin + gl, s_owner,
-                    my_local, my_remote, my_rrows);
-  }
-  flush_pair_stats(my_local, my_remote, my_rrows, stats);
-}
-
-int launch_gate_select(const LocalRows& lr, const float* logits, int64_t rows_per_shard,
-                       int32_t N, int32_t k, int32_t renorm, const int32_t* slot_owner,
-                       const ShardPtrs& topk_ids, const ShardPtrs& topk_w, int64_t* stats,
-                       int64_t n_rows_bound, cudaStream_t st) {
-  if (N > kGateMaxN || k > kGateMaxK || k > N) return SMOE_ERR_UNSUPPORTED;
-  if (n_rows_bound <= 0) return SMOE_OK;
-  const int grid = grid_cap(ceil_div(n_rows_bound, 8), 16);
-  SMOE_CUDA_TRY(launch_pdl(gate_select_kernel, grid, 256, 0, st, lr, logits, rows_per_shard, N,
-                           k, renorm, slot_owner, topk_ids, topk_w, stats));
-  SMOE_LAUNCH_CHECK();
-  return SMOE_OK;
-}
-
-static int g_gate_split = -1;
-int gate_split_enabled() {
-  if (g_gate_split < 0) {
-    const char* e = getenv("SMOE_GATE_SPLIT");
-    g_gate_split = (e && e[0] == '0') ? 0 : 1;
-  }
-  return g_gate_split;
-}
-void set_gate_split_enabled(int on) { g_gate_split = on ? 1 : 0; }
 
 __global__ void __launch_bounds__(256)
 gate_kernel(LocalRows lr, ShardPtrs hs, int64_t d, const uint32_t* __restrict__ w_gate,
@@ -978,7 +892,8 @@ __device__ __forceinline__ void combine_span(char* const (&dst_base)[G], const c
 template <int G, int MINB>
 __global__ void __launch_bounds__(256, MINB)
 combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtrs topk_w,
-                   ShardPtrs outs, HistUpdate hu, int32_t whole_rows) {
+                   ShardPtrs outs, HistUpdate hu, int32_t whole_rows, int64_t block_rows,
+                   int32_t* err) {
   pdl_enter();
   __shared__ RowMap rm;
   __shared__ char* s_y[SMOE_MAX_SHARDS];
@@ -1007,6 +922,13 @@ combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtr
     decode_row(rm, lr.shard_count, q, gl, j);
     const int64_t g = lr.shard_begin + gl;
     const int64_t i = lr.forward[g * rm.group + j];    // original token position
+    // block_rows > 0 (DS-MoE pipeline): the row goes to its all-gather slot
+    // g * group + j instead (the resume is a separate gather, not fused)
+    const int64_t i_dst = block_rows > 0 ? g * rm.group + j : i;
+    if (i_dst >= block_rows && block_rows > 0) {
+      if (lane == 0 && c == 0) set_err(err, SMOE_ERRBIT_CAPACITY);
+      continue;
+    }
     if (c == 0 && hu.n_hist_outs > 0 && lane < hu.hist_len) {
       // next layer's window: drop the oldest digit, append the cluster of the
       // top-1 expert (the device of this routing event, predictor.py:165-166)
@@ -1027,14 +949,15 @@ combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtr
     float wk[kGateMaxK];
 #pragma unroll
     for (int s = 0; s < kGateMaxK; ++s) wk[s] = s < k ? w[s] : 0.f;
-    combine_span<G>(dst_base, s_y[gl] + j * k * d * 2, wk, k, d, i, c * cv,
+    combine_span<G>(dst_base, s_y[gl] + j * k * d * 2, wk, k, d, i_dst, c * cv,
                     min(vecs, (c + 1) * cv), lane);
   }
 }
 
 int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtrs& ypair,
                        const ShardPtrs& topk_w, const ShardPtrs& outs, int32_t n_outs,
-                       const HistUpdate& hu, int64_t n_rows_bound, cudaStream_t st) {
+                       const HistUpdate& hu, int64_t n_rows_bound, cudaStream_t st,
+                       int64_t block_rows, int32_t* err) {
   if (k > kGateMaxK || d % 8) return SMOE_ERR_UNSUPPORTED;
   if (n_rows_bound <= 0) return SMOE_OK;
   const int grid = grid_items(n_rows_bound, d);
@@ -1043,9 +966,9 @@ int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtr
 #define SMOE_CMB_CASE(G_) \
     case G_:                                                                             \
       SMOE_CUDA_TRY(k <= 2 ? launch_pdl(combine_sag_kernel<G_, 2>, grid, 256, 0, st, lr, k, d,  \
-                                        ypair, topk_w, outs, hu, wr)                         \
+                                        ypair, topk_w, outs, hu, wr, block_rows, err)        \
                            : launch_pdl(combine_sag_kernel<G_, 3>, grid, 256, 0, st, lr, k, d,  \
-                                        ypair, topk_w, outs, hu, wr));                       \
+                                        ypair, topk_w, outs, hu, wr, block_rows, err));      \
       break;
     SMOE_CMB_CASE(1) SMOE_CMB_CASE(2) SMOE_CMB_CASE(3) SMOE_CMB_CASE(4) SMOE_CMB_CASE(5)
     SMOE_CMB_CASE(6) SMOE_CMB_CASE(7) SMOE_CMB_CASE(8) SMOE_CMB_CASE(9) SMOE_CMB_CASE(10)

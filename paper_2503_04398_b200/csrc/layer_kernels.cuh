@@ -19,8 +19,15 @@ struct LocalRows {
   int64_t single_rows;       // counts == nullptr: one block of `single_rows` rows (shard 0)
 };
 
+// n_sources: partials summed (default: one per shard, lr.n_shards)
 int launch_srs(const LocalRows& lr, const ShardPtrs& partials, int64_t d, const ShardPtrs& hs,
-               int64_t n_rows_bound, cudaStream_t st);
+               int64_t n_rows_bound, cudaStream_t st, int32_t n_sources = 0);
+
+// DS-MoE baseline all-reduce: the resident shards' natural row slices of the
+// sum of the n_shards partials, stored into every output (one per process)
+int launch_allreduce(const ShardPtrs& partials, int64_t d, int64_t n, int32_t shard_begin,
+                     int32_t shard_count, int32_t n_shards, const ShardPtrs& outs,
+                     int32_t n_outs, cudaStream_t st);
 
 int launch_gate(const LocalRows& lr, const ShardPtrs& hs, int64_t d, const void* w_gate,
                 const float* b_gate, int32_t N, int32_t k, int32_t renorm,
@@ -40,10 +47,6 @@ struct GateTcArgs {
   const int32_t* slot_owner;
   ShardPtrs topk_ids, topk_w;
   int64_t* stats;
-  // non-null: the kernel only writes the biased logits, fp32 [i * rows_per_shard
-  // + j, N] for resident shard i, row j, and launch_gate_select does the
-  // softmax / top-k / locality with a warp per row
-  float* logits;
 };
 bool gate_tc_supported(int32_t n_experts, int32_t top_k, int64_t d);
 int gate_tc_enabled();                 // SMOE_OPT_GATE_TENSOR
@@ -52,13 +55,6 @@ int gate_tc_rows(int32_t n_experts);   // W box rows (N rounded up to 16)
 int launch_gate_tc(const CUtensorMap& map_h, const CUtensorMap& map_w, const GateTcArgs& a,
                    int64_t n_rows_bound, cudaStream_t st);
 
-int gate_split_enabled();              // SMOE_OPT_GATE_SPLIT
-void set_gate_split_enabled(int on);
-// softmax + top-k + locality over logits written by the tcgen05 gate (warp per row)
-int launch_gate_select(const LocalRows& lr, const float* logits, int64_t rows_per_shard,
-                       int32_t N, int32_t k, int32_t renorm, const int32_t* slot_owner,
-                       const ShardPtrs& topk_ids, const ShardPtrs& topk_w, int64_t* stats,
-                       int64_t n_rows_bound, cudaStream_t st);
 
 size_t route_workspace_bytes(int64_t max_tokens, int32_t k, int32_t N, int32_t shard_count);
 int launch_route(const LocalRows& lr, int32_t N, int32_t k, const ShardPtrs& topk_ids,
@@ -81,9 +77,13 @@ struct HistUpdate {
   ShardPtrs topk_ids;         // per resident shard [n, k]
 };
 
+// block_rows > 0: DS-MoE layout -- row j of shard g goes to row g * group + j
+// of each output (an all-gather buffer of block_rows rows), not to the
+// token's original position
 int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtrs& ypair,
                        const ShardPtrs& topk_w, const ShardPtrs& outs, int32_t n_outs,
-                       const HistUpdate& hu, int64_t n_rows_bound, cudaStream_t st);
+                       const HistUpdate& hu, int64_t n_rows_bound, cudaStream_t st,
+                       int64_t block_rows = 0, int32_t* err = nullptr);
 
 // Standalone shuffled all-gather (smoe_sag): row j of blocks[g] -> every
 // outs[o] at forward[g*group + j].

@@ -248,7 +248,7 @@ class SpecMoELayer:
         """Digits of the n-gram window (the bundle's n, predictor.py:57-82)."""
         return int(self.tables.ngram_n)
 
-    def _device_inputs(self, tokens_t, hist_t, hist_depth):
+    def _device_inputs(self, tokens_t, hist_t, hist_depth, max_tokens=None):
         """Validated, contiguous int64 device views of the token ids and the
         history window, and the window's valid depth.  The kernels index the
         window as [n, history_width] with a fixed stride, so any other shape
@@ -258,8 +258,9 @@ class SpecMoELayer:
         dev = self.w_gate.device
         tok = tokens_t.reshape(-1).to(device=dev, dtype=t.int64).contiguous()
         n = int(tok.shape[0])
-        if n > self.max_tokens:
-            raise SchedulerError(f"{n} tokens exceed max_tokens={self.max_tokens}")
+        cap = self.max_tokens if max_tokens is None else int(max_tokens)
+        if n > cap:
+            raise SchedulerError(f"{n} tokens exceed max_tokens={cap}")
         if hist_t is None:
             return tok, None, 0
         h = self.history_width
@@ -710,7 +711,8 @@ class MicroBatchedSpecMoE:
         tok = t.as_tensor(token_ids).to(device=dev, dtype=t.int64).reshape(-1).contiguous()
         hist = None if histories is None else t.as_tensor(histories).to(
             device=dev, dtype=t.int64).contiguous()
-        self.layers[0]._device_inputs(tok, hist, history_depth)   # validate the whole batch
+        self.layers[0]._device_inputs(tok, hist, history_depth,   # validate the whole batch
+                                      max_tokens=self.max_tokens)
         if self.group is None:
             self.partial_views(int(tok.numel())).copy_(hp)
         else:

@@ -15,6 +15,8 @@ numpy inputs give numpy outputs; CUDA tensors stay on the device.
 
 from __future__ import annotations
 
+import weakref
+import zlib
 from dataclasses import dataclass
 
 import numpy as np
@@ -107,16 +109,33 @@ class DeviceTables:
         del t
 
 
-_TABLE_CACHE: dict[int, tuple[object, DeviceTables]] = {}
+# id(bundle) -> (weakref to the bundle, content fingerprint, DeviceTables).
+# Entries die with their bundle (weakref callback), and a bundle whose arrays
+# were edited in place since the upload is re-uploaded (fingerprint).
+_TABLE_CACHE: dict[int, tuple[weakref.ref, int, DeviceTables]] = {}
+
+
+def _fingerprint(bundle) -> int:
+    tok, ng = bundle.token_table, bundle.ngram_table
+    h = 0
+    for a in (tok.labels, tok.confidence, ng.best, ng.confidence):
+        a = np.ascontiguousarray(np.asarray(a))
+        h = zlib.adler32(memoryview(a).cast("B"), h)
+    return h
 
 
 def device_tables(bundle) -> DeviceTables:
     key = id(bundle)
+    fp = _fingerprint(bundle)
     hit = _TABLE_CACHE.get(key)
-    if hit is not None and hit[0] is bundle:
-        return hit[1]
+    if hit is not None and hit[0]() is bundle and hit[1] == fp:
+        return hit[2]
     dt = DeviceTables(bundle)
-    _TABLE_CACHE[key] = (bundle, dt)
+    try:
+        ref = weakref.ref(bundle, lambda _r, k=key: _TABLE_CACHE.pop(k, None))
+    except TypeError:                       # not weak-referenceable: do not cache
+        return dt
+    _TABLE_CACHE[key] = (ref, fp, dt)
     return dt
 
 

@@ -5,6 +5,30 @@ import os
 import numpy as np
 
 
+def collect(q, procs, timeout=540):
+    """One result per process from `q`, keyed by rank (the first tuple item).
+    Fails fast when a worker dies instead of waiting out the timeout."""
+    import queue
+    import time
+    res = {}
+    deadline = time.monotonic() + timeout
+    while len(res) < len(procs):
+        try:
+            item = q.get(timeout=5)
+            res[item[0]] = item[1:]
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            if dead or time.monotonic() > deadline:
+                for p in procs:
+                    p.kill()
+                raise RuntimeError(f"worker failed (exit codes {dead}) or timed out")
+    for p in procs:
+        p.join(timeout=60)
+        if p.exitcode != 0:
+            raise RuntimeError(f"worker exit code {p.exitcode}")
+    return res
+
+
 def bind_device(rank, world):
     """Rank r on cuda:r when the box has a GPU per rank (then the IPC peer
     buffers, peer stores and signal-pad barriers really cross NVLink);

@@ -50,14 +50,7 @@ def _run_dsmoe_procs(world, over, n, backend):
              for r in range(world)]
     for p in procs:
         p.start()
-    res = {}
-    for _ in range(world):
-        r, outs, st = q.get(timeout=540)
-        res[r] = (outs, st)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    return res
+    return mp_worker.collect(q, procs)
 
 
 @pytest.mark.timeout(600)

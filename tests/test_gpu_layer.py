@@ -39,22 +39,16 @@ CASES = [
 ]
 
 
-@pytest.fixture(params=[(1, 1), (1, 0), (0, 1)],
-                ids=["gate_tcgen05_split", "gate_tcgen05_fused", "gate_mma_sync"])
+@pytest.fixture(params=[1, 0], ids=["gate_tcgen05", "gate_mma_sync"])
 def gate_kernel(request):
-    """Run a test with each gate variant: the tcgen05 logits kernel + warp
-    selection kernel (default), the tcgen05 kernel selecting in its own
-    epilogue (SMOE_OPT_GATE_SPLIT = 0), and the mma.sync / CUDA-core kernels
-    (SMOE_OPT_GATE_TENSOR = 0)."""
+    """Run a test with each gate kernel: tcgen05 (default) and the mma.sync /
+    CUDA-core kernels (SMOE_OPT_GATE_TENSOR = 0)."""
     from paper_2503_04398_b200 import _native as N
     lib = N.lib()
-    old = (lib.smoe_get_option(N.OPT_GATE_TENSOR), lib.smoe_get_option(N.OPT_GATE_SPLIT))
-    tc, split = request.param
-    N.check(lib.smoe_set_option(N.OPT_GATE_TENSOR, tc), "set_option")
-    N.check(lib.smoe_set_option(N.OPT_GATE_SPLIT, split), "set_option")
-    yield tc
-    N.check(lib.smoe_set_option(N.OPT_GATE_TENSOR, old[0]), "set_option")
-    N.check(lib.smoe_set_option(N.OPT_GATE_SPLIT, old[1]), "set_option")
+    old = lib.smoe_get_option(N.OPT_GATE_TENSOR)
+    N.check(lib.smoe_set_option(N.OPT_GATE_TENSOR, request.param), "set_option")
+    yield request.param
+    N.check(lib.smoe_set_option(N.OPT_GATE_TENSOR, old), "set_option")
 
 
 @pytest.mark.parametrize("name,n,eps,over", CASES)

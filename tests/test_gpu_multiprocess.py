@@ -36,13 +36,7 @@ def test_two_process_layer_matches_single_process(world, over):
              for r in range(world)]
     for p in procs:
         p.start()
-    res = {}
-    for _ in range(world):
-        r, outs, st, all_out = q.get(timeout=540)
-        res[r] = (outs, st, all_out)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    res = mp_worker.collect(q, procs)
     w = synth.make_workload("toy", n=n, eps=0.3, seed=11, cfg_override=over)
     ref_layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=w.cfg["k"], max_tokens=n)
     ref = ref_layer.forward(torch.from_numpy(w.partials).cuda(), w.tokens, w.hist)
@@ -73,13 +67,7 @@ def test_multi_process_forward_async_matches_single_process(world, over):
              for r in range(world)]
     for p in procs:
         p.start()
-    res = {}
-    for _ in range(world):
-        r, got = q.get(timeout=540)
-        res[r] = got
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    res = {r: v[0] for r, v in mp_worker.collect(q, procs).items()}
     ws = [synth.make_workload("toy", n=n, eps=0.3, seed=20 + i, cfg_override=over)
           for i, n in enumerate(sizes)]
     base = ws[0]
@@ -104,13 +92,7 @@ def test_two_process_graph_capture():
              for r in range(world)]
     for p in procs:
         p.start()
-    res = {}
-    for _ in range(world):
-        r, got = q.get(timeout=540)
-        res[r] = got
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    res = {r: v[0] for r, v in mp_worker.collect(q, procs).items()}
     ws = [synth.make_workload("toy", n=n, eps=0.3, seed=s, cfg_override=over) for s in seeds]
     base = ws[0]
     ref_layer = SpecMoELayer(base.bundle, base.gate_w, base.w1, base.w3, base.w2,
@@ -135,13 +117,7 @@ def test_two_process_microbatched_matches_single_process(M):
              for r in range(world)]
     for p in procs:
         p.start()
-    res = {}
-    for _ in range(world):
-        r, outs, hist = q.get(timeout=540)
-        res[r] = (outs, hist)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    res = mp_worker.collect(q, procs)
     w = synth.make_workload("toy", n=n, eps=0.3, seed=12, cfg_override=over)
     ref_layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=w.cfg["k"], max_tokens=n)
     want = ref_layer.forward(torch.from_numpy(w.partials).to(torch.bfloat16), w.tokens,

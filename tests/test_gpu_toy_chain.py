@@ -60,7 +60,7 @@ def test_toy_bundle_layer_chain(ci):
         assert m["imbalance"] == float(ch[pre + "imbalance"])
         ref = layer_ref.layer_forward(
             partials=partials, tokens=tokens,
-            hist=None if win is None else win.cpu().numpy(), hist_depth=depth,
+            hist=None if hist_in is None else hist_in.cpu().numpy(), hist_depth=depth,
             t_labels=b.token_table.labels, t_conf=b.token_table.confidence,
             a_best=b.ngram_table.best, a_conf=b.ngram_table.confidence, n_clusters=2,
             expert_labels=C, gate_w=gate, w1=w1, w3=w3, w2=w2, k=k)
