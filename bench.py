@@ -309,7 +309,6 @@ def main():
         import torch.distributed as dist
         if same_gpu:
             dist.init_process_group("gloo")
-            args.no_dsmoe = True            # NCCL cannot put two ranks on one GPU
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         from paper_2503_04398_b200.dist import ShardGroup
@@ -486,35 +485,55 @@ def main():
         del g
 
     # ---------------- DS-MoE pipeline baseline (AR -> A2A -> A2A -> AG), same kernels
-    dsm = None
-    if not args.no_dsmoe and world in (1, G):
-        from paper_2503_04398_b200.baseline import DSMoELayer
-        base = DSMoELayer(w.gate_w, w.w1, w.w3, w.w2, n_ranks=G, top_k=k, max_tokens=n,
-                          distributed=world > 1)
-        parts = [layer.partial_views(n)[i] for i in range(L)]
-        for _ in range(max(2, args.warmup)):
-            base.forward(parts, n)
+    def timed_stages(lay, run, steps):
+        """Whole-step and per-stage device time of `steps` forwards (events
+        between stages on the launching stream), max over ranks."""
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(NS + 1)] for _ in range(steps)]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         torch.cuda.synchronize()
-        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        bsteps = max(3, args.steps // 2)
-        b0.record(stream)
-        for _ in range(bsteps):
-            base.forward(parts, n)
-        b1.record(stream)
+        e0.record(stream)
+        for s_ in range(steps):
+            evs[s_][0].record(stream)
+            for j in range(NS):
+                run(stages=[j])
+                evs[s_][j + 1].record(stream)
+        e1.record(stream)
         torch.cuda.synchronize()
-        b_ms = b0.elapsed_time(b1)
-        b_ms = max_over_ranks(b_ms)
-        bst = base.stats()
+        barrier()
+        per = {nm: max_over_ranks(float(np.mean([evs[s_][j].elapsed_time(evs[s_][j + 1])
+                                                 for s_ in range(steps)])))
+               for j, nm in enumerate(N.STAGE_NAMES)}
+        return max_over_ranks(e0.elapsed_time(e1)), per
+
+    dsm = None
+    if not args.no_dsmoe:
+        from paper_2503_04398_b200.baseline import DSMoEPipelineLayer
+        base = DSMoEPipelineLayer(w.gate_w, w.w1, w.w3, w.w2, n_ranks=G, top_k=k, max_tokens=n,
+                                  group=group)
+        base.partial_views(n).copy_(w.partials[base.shard_begin:base.shard_begin + L])
+        for _ in range(max(2, args.warmup)):
+            base.run_device(n=n)
+        torch.cuda.synchronize()
+        base.check_errors()
+        bsteps = max(3, args.steps // 2)
+        b_ms, b_stage = timed_stages(base, lambda stages: base.run_device(n=n, stages=stages),
+                                     bsteps)
+        base.check_errors()
+        bst = base.stats(n)
         dsm = {"value": n * bsteps / (b_ms / 1e3), "unit": "tokens/s",
                "ms_per_step": b_ms / bsteps, "local_activation_rate": bst["measured_alpha"],
-               "a2a_bytes_per_step": bst["bytes"]["a2a_dispatch"] * 2,
-               "impl": "NCCL all_reduce / all_to_all_single / all_gather_into_tensor"
-                       if world > 1 else f"{G} ranks emulated on one GPU (collectives = "
-                                         "device copies)",
+               "a2a_bytes_per_step": bst["bytes"]["a2a_dispatch"] + bst["bytes"]["a2a_combine"],
+               "stages_ms": b_stage,
+               "stage_delta_ms_smoe_minus_dsmoe": {nm: stage_ms[nm] - b_stage[nm]
+                                                   for nm in N.STAGE_NAMES},
+               "impl": "DSMoEPipelineLayer: the s-MoE kernels and runtime with "
+                       "SMOE_PIPELINE_DSMOE (two-shot all-reduce + slice instead of SRS, "
+                       "combine into all-gather blocks + resume instead of SAG) and "
+                       "position-sharding tables (token i -> rank i % G, contiguous experts)",
                "speedup_smoe_over_dsmoe": (n * args.steps / (ms_total / 1e3)) /
                                           (n * bsteps / (b_ms / 1e3))}
-        del base, parts
+        del base
         torch.cuda.empty_cache()
 
     # ---------------- CPU baseline (rank 0, N=1 only)

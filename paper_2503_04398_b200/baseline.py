@@ -3,12 +3,24 @@
 The comparison point of the north star.  Densely-replicated attention output
 is all-reduced on every rank, tokens are sharded by position
 (token_dev = i % G, comm.py:202), experts sit in contiguous blocks
-(expert_dev = e // (N/G), comm.py:201), the dispatch / combine all-to-alls
-are all2allv with host-synchronised split sizes, and an all-gather restores
-the batch on every rank.  The compute uses the same sm_100a kernels as the
-s-MoE layer (tensor-core gate, tcgen05 grouped GEMM); the collectives are
-NCCL through torch.distributed (one rank per GPU), or — with G virtual ranks
-in one process — the equivalent device copies.
+(expert_dev = e // (N/G), comm.py:201), and an all-gather restores the batch
+on every rank.  Two implementations:
+
+* `DSMoEPipelineLayer` -- the like-for-like baseline.  It runs on the s-MoE
+  layer runtime itself (same plan, tcgen05 gate, route, dispatch, grouped
+  GEMMs with the combine fused into the down projection, same buffers and
+  shard groups), with SMOE_PIPELINE_DSMOE switching the two stages whose
+  STRUCTURE differs: a two-shot all-reduce into every process plus each
+  rank's slice (instead of the shuffled reduce-scatter), and the combine
+  into all-gather blocks plus a resume gather (instead of the fused SAG).
+  Position-sharding tables make the plan the DS-MoE one.  s-MoE vs this
+  layer therefore differ only in pipeline structure and token placement.
+* `DSMoELayer` -- the stock collective pipeline: NCCL all_reduce,
+  all_to_all_single with host-synchronised split sizes (x2) and
+  all_gather_into_tensor through torch.distributed (one rank per GPU), or,
+  with G virtual ranks in one process, the same data movement as device
+  copies.  It is the pipeline as DeepSpeed-MoE runs it, kept to exercise
+  the NCCL path; it is not the like-for-like comparison.
 """
 
 from __future__ import annotations
@@ -16,6 +28,76 @@ from __future__ import annotations
 import numpy as np
 
 from . import _dev, _native as N
+from .layer import SpecMoELayer
+from .predictor import DeviceNGramTable, TokenDeviceTable
+from .scheduler import LookupBundle
+
+
+def position_bundle(n_positions: int, n_ranks: int, n_experts: int) -> LookupBundle:
+    """Tables under which the s-MoE plan IS the DS-MoE placement: "token"
+    (position) i -> rank i % G (comm.py:202) with confidence 1 and no n-gram
+    rows, experts in contiguous blocks e // (N/G) (comm.py:201)."""
+    G = int(n_ranks)
+    if n_experts % G:
+        raise ValueError("DS-MoE contiguous placement needs G | N")
+    pos = np.arange(int(n_positions))
+    tt = TokenDeviceTable(labels=pos % G, confidence=np.ones(len(pos), np.float32),
+                          provenance=np.zeros(len(pos), np.uint8), n_clusters=G)
+    ng = DeviceNGramTable(n=1, n_clusters=G, probs=np.zeros((G, G)),
+                          counts=np.zeros((G, G), np.int64))
+    return LookupBundle(token_table=tt, ngram_table=ng,
+                        expert_labels=np.arange(n_experts) // (n_experts // G), layers=1)
+
+
+class DSMoEPipelineLayer(SpecMoELayer):
+    """The DS-MoE pipeline on the s-MoE kernels (see the module docstring).
+
+    forward(hidden_partials, n) -> [n, d]: hidden_partials as for
+    SpecMoELayer.forward; token ids are the positions 0..n-1."""
+
+    def __init__(self, gate_w, w1, w3, w2, *, n_ranks: int, top_k: int, max_tokens: int,
+                 renormalize: bool = True, gate_b=None, group=None, expert_rows=None):
+        N_exp = int(np.asarray(gate_w.shape)[0])
+        G = int(n_ranks)
+        self._ag_rows = G * (-(-int(max_tokens) // G))
+        super().__init__(position_bundle(max_tokens, G, N_exp), gate_w, w1, w3, w2,
+                         top_k=top_k, max_tokens=max_tokens, renormalize=renormalize,
+                         gate_b=gate_b, group=group, expert_rows=expert_rows)
+        N.check(self.lib.smoe_layer_set_pipeline(self._h, N.PIPELINE_DSMOE, self._ag_rows),
+                "set_pipeline")
+        t = _dev.torch()
+        self._positions = t.arange(self.max_tokens, dtype=t.int64, device=self.w_gate.device)
+
+    def process_row_buffers(self) -> dict:
+        return {"ar": self.max_tokens, "ag": self._ag_rows}
+
+    def stats(self, n: int | None = None) -> dict:
+        """As SpecMoELayer.stats, with the DS-MoE collectives' bytes in place
+        of the SRS / SAG ones: the two-shot all-reduce moves every token row
+        G - 1 times in (reduce-scatter) and G - 1 times out (all-gather), the
+        final all-gather G * group rows G - 1 times."""
+        st = super().stats(n)
+        b = st["bytes"]
+        rows = int(sum(st["device_counts"]))
+        row = 2 * self.d
+        b.pop("srs"), b.pop("sag"), b.pop("srs_padded_model")
+        b["all_reduce"] = 2 * (self.G - 1) * rows * row
+        b["all_gather"] = (self.G - 1) * self.G * st["group_size"] * row
+        return st
+
+    def positions(self, n: int):
+        return self._positions[:n]
+
+    def forward(self, hidden_partials, n: int | None = None, out=None):
+        hp = hidden_partials
+        n = int(hp.shape[-2]) if n is None else int(n)
+        return super().forward(hp, self._positions[:n], None, out=out)
+
+    def run_device(self, tokens_t=None, hist_t=None, stream=None, stages=None, hist_depth=None,
+                   n: int | None = None):
+        if tokens_t is None:
+            tokens_t = self._positions[:n]
+        return super().run_device(tokens_t, None, stream=stream, stages=stages)
 
 
 class DSMoELayer:

@@ -102,8 +102,10 @@ class ShardGroup:
         h = max(int(layer.tables.ngram_n), 1)
         # one output (and next-layer history) per process: the SAG delivers
         # every token's row to each process once, whichever of its shards
+        extra = layer.process_row_buffers()      # e.g. the DS-MoE pipeline's AR / AG
         peer, local = self.peer_tables(G, layer.N, per_shard,
-                                       {"hist": n * h * 8, "out": n * d * 2})
+                                       {"hist": n * h * 8, "out": n * d * 2,
+                                        **{name: rows * d * 2 for name, rows in extra.items()}})
 
         def tensor(ptr, shape, typestr):
             return torch.as_tensor(_CudaArray(ptr, shape, typestr), device=device)
@@ -113,6 +115,8 @@ class ShardGroup:
         peer["partial_b_local"] = tensor(local["partial_b"], (L, n, d),
                                          "<i2").view(torch.bfloat16)
         peer["out_local"] = tensor(local["out"], (n, d), "<i2").view(torch.bfloat16)
+        for name, rows in extra.items():
+            peer[name + "_local"] = tensor(local[name], (rows, d), "<i2").view(torch.bfloat16)
         peer["counts_local"] = tensor(local["counts"], (G, layer.N), "<i4")
         peer["hist_local"] = tensor(local["hist"], (n, h), "<i8")
         tensor(local["signal"], (64,), "<i4").zero_()

@@ -120,6 +120,13 @@ class SpecMoELayer:
                 del src
 
     # ------------------------------------------------------------ buffers
+    def process_row_buffers(self) -> dict:
+        """Extra per-process [rows, d] bf16 peer buffers {name: rows} bound to
+        the C slots of `_EXTRA_SLOTS` (none for the speculative pipeline)."""
+        return {}
+
+    _EXTRA_SLOTS = {"ar": N.BUF_AR, "ag": N.BUF_AG}
+
     def _alloc_buffers(self):
         t = _dev.torch()
         dev = self.w_gate.device
@@ -142,6 +149,10 @@ class SpecMoELayer:
                     "counts": [self.counts_mat] * G,
                     "hist": [self.hist_next] * G,
                     "signal": [None] * G}
+            for name, rows in self.process_row_buffers().items():
+                buf = t.empty((rows, d), dtype=bf, device=dev)
+                peer[name] = [buf] * G
+                peer[name + "_local"] = buf
         else:
             peer = self.group.alloc_layer_buffers(self, dev)
             self.partial = peer["partial_local"]
@@ -149,6 +160,8 @@ class SpecMoELayer:
             self.counts_mat = peer["counts_local"]
             self.hist_next = peer["hist_local"]
         self._peer = peer
+        for name in self.process_row_buffers():
+            setattr(self, name + "_local", peer[name + "_local"])
         # every resident shard's output is the process's single output buffer
         # (indexable per shard for the reference-style per-rank view)
         self.out = self.out_buf.unsqueeze(0).expand(G if self.group is None else L, n, d)
@@ -195,6 +208,8 @@ class SpecMoELayer:
             bind(N.BUF_HIST_OUT, g, p["hist"][g])
             if p["signal"][g] is not None:
                 bind(N.BUF_SIGNAL, g, p["signal"][g])
+            for name in self.process_row_buffers():
+                bind(self._EXTRA_SLOTS[name], g, p[name][g])
         for i in range(self.shard_count):
             bind(N.BUF_HS, i, self.hs[i])
             bind(N.BUF_TOPK_IDS, i, self.topk_ids[i])

@@ -187,3 +187,29 @@ def dsmoe_worker(rank, world, port, cfg_over, n, backend, result_q):
         dist.barrier()
     finally:
         dist.destroy_process_group()
+
+
+def dsmoe_pipeline_worker(rank, world, port, cfg_over, n, result_q):
+    """DSMoEPipelineLayer over a ShardGroup: G / world shards per process."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    bind_device(rank, world)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2503_04398_b200 import synth
+        from paper_2503_04398_b200.baseline import DSMoEPipelineLayer
+        from paper_2503_04398_b200.dist import ShardGroup
+        w = synth.make_workload("toy", n=n, eps=0.3, seed=12, cfg_override=cfg_over)
+        grp = ShardGroup.from_torch_distributed()
+        layer = DSMoEPipelineLayer(w.gate_w, w.w1, w.w3, w.w2, n_ranks=w.cfg["G"],
+                                   top_k=w.cfg["k"], max_tokens=n, group=grp)
+        L = layer.shard_count
+        mine = torch.from_numpy(w.partials[layer.shard_begin:layer.shard_begin + L]).cuda()
+        outs = [layer.forward(mine).float().cpu().numpy() for _ in range(2)]
+        st = layer.stats_t.cpu().numpy()[:2].tolist()
+        result_q.put((rank, outs, tuple(int(x) for x in st)))
+        dist.barrier()
+        grp.close()
+    finally:
+        dist.destroy_process_group()
