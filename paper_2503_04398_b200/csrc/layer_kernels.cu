@@ -667,8 +667,11 @@ route_rank_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids, ShardP
   const int64_t g = lr.shard_begin + gl;
   const int64_t P = (int64_t)lr.counts[g] * k;
   const int32_t nchunks = (int32_t)((P + kRouteThreads - 1) / kRouteThreads);
-  const int32_t* cc = chunk_counts + (int64_t)gl * max_chunks * N;
-  if (blockIdx.x == 0) {             // publish row g of the [G, N] count matrix
+  // chunk_counts == nullptr: every shard's pairs fit one chunk (decode-sized
+  // batches) and this kernel counts them itself -- route_count is skipped
+  const bool single = chunk_counts == nullptr;
+  const int32_t* cc = single ? nullptr : chunk_counts + (int64_t)gl * max_chunks * N;
+  if (blockIdx.x == 0 && !single) {  // publish row g of the [G, N] count matrix
     for (int e = tid; e < N; e += kRouteThreads) {
       int32_t tot = 0;
       for (int c = 0; c < nchunks; ++c) tot += cc[c * N + e];
@@ -679,7 +682,7 @@ route_rank_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids, ShardP
   for (int b = blockIdx.x; b < nchunks; b += gridDim.x) {
     for (int e = tid; e < N; e += kRouteThreads) {
       int32_t pre = 0;
-      for (int c = 0; c < b; ++c) pre += cc[c * N + e];
+      for (int c = 0; c < b && !single; ++c) pre += cc[c * N + e];
       s_pre[e] = pre;
     }
     for (int e = tid; e < 32 * N; e += kRouteThreads) s_w[e] = 0;
@@ -695,7 +698,19 @@ route_rank_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids, ShardP
       for (int w = 0; w < warp; ++w) r += s_w[w * N + e];
       reinterpret_cast<int32_t*>(s_rank[gl])[p] = r;
     }
+    if (single) {                    // the only chunk: its totals are row g
+      for (int ee = tid; ee < N; ee += kRouteThreads) {
+        int32_t tot = 0;
+        for (int w = 0; w < kRouteThreads / 32; ++w) tot += s_w[w * N + ee];
+        for (int i = 0; i < n_count_bufs; ++i)
+          reinterpret_cast<int32_t*>(s_cb[i])[g * N + ee] = tot;
+      }
+    }
     __syncthreads();
+  }
+  if (single && nchunks == 0 && blockIdx.x == 0) {   // no pairs: a zero row
+    for (int ee = tid; ee < N; ee += kRouteThreads)
+      for (int i = 0; i < n_count_bufs; ++i) reinterpret_cast<int32_t*>(s_cb[i])[g * N + ee] = 0;
   }
 }
 
@@ -714,6 +729,14 @@ int launch_route(const LocalRows& lr, int32_t N, int32_t k, const ShardPtrs& top
   const int32_t per_shard = (int32_t)std::max<int64_t>(
       1, std::min<int64_t>(max_chunks, ceil_div(2 * num_sms(), lr.shard_count)));
   const dim3 grid(per_shard, lr.shard_count);
+  if (max_chunks == 1) {
+    // one chunk per shard: the rank kernel counts too (one launch, not two)
+    SMOE_CUDA_TRY(launch_pdl(route_rank_kernel, grid, kRouteThreads, 0, st, lr, N, k, topk_ids,
+                             pair_rank, (const int32_t*)nullptr, max_chunks, count_bufs,
+                             n_count_bufs));
+    SMOE_LAUNCH_CHECK();
+    return SMOE_OK;
+  }
   SMOE_CUDA_TRY(launch_pdl(route_count_kernel, grid, kRouteThreads, 0, st, lr, N, k, topk_ids, chunk_counts,
                                                       max_chunks));
   SMOE_LAUNCH_CHECK();
@@ -731,7 +754,8 @@ __global__ void __launch_bounds__(256)
 dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __restrict__ C,
                 const int32_t* __restrict__ slot_owner, const int32_t* __restrict__ slot_first,
                 ShardPtrs hs, ShardPtrs topk_ids, ShardPtrs pair_rank, ShardPtrs xin,
-                ShardPtrs xmeta, int64_t expert_rows, int64_t* problems, int32_t* err) {
+                ShardPtrs xmeta, int64_t expert_rows, int64_t* problems, int32_t* err,
+                int32_t whole_rows) {
   pdl_enter();
   __shared__ RowMap rm;
   __shared__ int32_t s_M[kGateMaxN];
@@ -780,11 +804,16 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
       pr[0] = a_off; pr[1] = m; pr[2] = e - e0; pr[3] = a_off;
     }
   }
-  // one warp per token: the row is read once and written to its k slots
+  // one warp per token (or, for decode-sized batches, per 1 KiB chunk of a
+  // token's row, as in the SRS): the row is read once and written to its k slots
   const int64_t vecs = d / 8;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t q = blockIdx.x * (int64_t)(blockDim.x >> 5) + (tid >> 5); q < rm.total;
-       q += nwarps) {
+  const bool whole = rm.total >= whole_rows;
+  const int64_t chunks = whole ? 1 : (vecs + kChunkVecs - 1) / kChunkVecs;
+  const int64_t cv = whole ? vecs : kChunkVecs;
+  for (int64_t it = blockIdx.x * (int64_t)(blockDim.x >> 5) + (tid >> 5);
+       it < (int64_t)rm.total * chunks; it += nwarps) {
+    const int64_t q = whole ? it : it / chunks, c = it - q * chunks;
     int32_t gl; int64_t j;
     decode_row(rm, lr.shard_count, q, gl, j);
     const int32_t g = lr.shard_begin + gl;
@@ -798,12 +827,13 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
       const int64_t pos = (int64_t)s_off[g * N + e] + rk[s];
       if (pos >= expert_rows) { if (lane == 0) set_err(err, SMOE_ERRBIT_CAPACITY); continue; }
       dst[nd++] = s_xin[o] + pos * d * 2;
-      if (lane == 0)
+      if (lane == 0 && c == 0)
         reinterpret_cast<int64_t*>(s_xmeta[o])[pos] = ((int64_t)g << 40) | (j * k + s);
     }
     const char* src = s_hs[gl] + j * d * 2;
-    int64_t v = lane;
-    for (; v + 224 < vecs; v += 256) {                 // 8 loads in flight per lane
+    const int64_t v1 = min(vecs, (c + 1) * cv);
+    int64_t v = c * cv + lane;
+    for (; v + 224 < v1; v += 256) {                   // 8 loads in flight per lane
       uint4 a[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) a[u] = ld_nc_v4(src + (v + 32 * u) * 16);
@@ -812,7 +842,7 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
         for (int u = 0; u < 8; ++u) DISPATCH_ST(dst[i] + (v + 32 * u) * 16, a[u]);
       }
     }
-    for (; v < vecs; v += 32) {
+    for (; v < v1; v += 32) {
       const uint4 a = ld_nc_v4(src + v * 16);
       for (int i = 0; i < nd; ++i) DISPATCH_ST(dst[i] + v * 16, a);
     }
@@ -826,10 +856,10 @@ int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
                     int64_t expert_rows, int64_t* problems, int32_t* err, int64_t n_rows_bound,
                     cudaStream_t st) {
   if (N > kGateMaxN || d % 8) return SMOE_ERR_UNSUPPORTED;
-  const int64_t blocks = std::max<int64_t>(1, ceil_div(n_rows_bound, 8));
-  SMOE_CUDA_TRY(launch_pdl(dispatch_kernel, grid_cap(blocks, 16), 256, 0, st, lr, N, k, d, counts_mat, slot_owner,
-                                                        slot_first, hs, topk_ids, pair_rank, xin,
-                                                        xmeta, expert_rows, problems, err));
+  SMOE_CUDA_TRY(launch_pdl(dispatch_kernel, grid_items(std::max<int64_t>(n_rows_bound, 1), d),
+                           256, 0, st, lr, N, k, d, counts_mat, slot_owner, slot_first, hs,
+                           topk_ids, pair_rank, xin, xmeta, expert_rows, problems, err,
+                           whole_rows_from()));
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }

@@ -163,6 +163,81 @@ plan_scatter_kernel(const int32_t* __restrict__ dev_ws, int64_t n, int32_t G,
   }
 }
 
+// Both passes in one CTA when the batch is a single tile (n <= 512, decode):
+// the labels stay in registers and the tile prefix is zero, so one launch
+// replaces two (identical results: the same match_any ranks in the same order).
+__global__ void __launch_bounds__(kPlanThreads)
+plan_single_kernel(LookupTables t, int use_lookup, const int64_t* __restrict__ tokens,
+                   const int64_t* __restrict__ devices, int64_t n, int32_t G,
+                   int64_t* __restrict__ dev_out, int64_t* __restrict__ forward,
+                   int64_t* __restrict__ inverse, int32_t* __restrict__ counts_out,
+                   int64_t* __restrict__ group_out, int32_t* err) {
+  pdl_enter();
+  extern __shared__ int32_t smem[];
+  int32_t* s_cnt = smem;                  // [G] tokens per device
+  int32_t* s_base = smem + G;             // [G] running offset per device
+  int32_t* s_wcnt = smem + 2 * G;         // [8 warps][G]
+  __shared__ int32_t s_group;
+  if (threadIdx.x == 0) s_group = 0;
+  for (int d = threadIdx.x; d < 10 * G; d += blockDim.x) smem[d] = 0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t dv[kPlanChunks];
+#pragma unroll
+  for (int c = 0; c < kPlanChunks; ++c) {
+    const int64_t i = c * kPlanThreads + threadIdx.x;
+    int32_t d = -1;
+    if (i < n) {
+      int64_t lab = use_lookup ? lookup_one(t, i, __ldg(tokens + i), err) : __ldg(devices + i);
+      if (dev_out) dev_out[i] = lab;
+      if (lab < 0 || lab >= G) set_err(err, SMOE_ERRBIT_DEVICE_RANGE);
+      else d = (int32_t)lab;
+    }
+    dv[c] = d;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    if (d >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[d], __popc(peers));
+  }
+  __syncthreads();
+  int32_t local_max = 0;
+  for (int d = threadIdx.x; d < G; d += blockDim.x) {
+    local_max = max(local_max, s_cnt[d]);
+    counts_out[d] = s_cnt[d];
+  }
+  atomicMax(&s_group, local_max);
+  __syncthreads();
+  const int64_t group = s_group;
+  if (threadIdx.x == 0) *group_out = group;
+#pragma unroll
+  for (int c = 0; c < kPlanChunks; ++c) {
+    const int64_t i = c * kPlanThreads + threadIdx.x;
+    const int32_t d = dv[c];
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const int32_t rank_w = __popc(peers & lanemask_lt());
+    if (d >= 0 && lane == __ffs(peers) - 1) s_wcnt[warp * G + d] = __popc(peers);
+    __syncthreads();
+    if (d >= 0) {
+      int32_t off = s_base[d] + rank_w;
+      for (int w = 0; w < warp; ++w) off += s_wcnt[w * G + d];
+      const int64_t slot = (int64_t)d * group + off;
+      inverse[i] = slot;
+      forward[slot] = i;
+    }
+    __syncthreads();
+    for (int dd = threadIdx.x; dd < G; dd += blockDim.x) {
+      int32_t sum = 0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) { sum += s_wcnt[w * G + dd]; s_wcnt[w * G + dd] = 0; }
+      s_base[dd] += sum;
+    }
+    __syncthreads();
+  }
+  const int64_t total_slots = (int64_t)G * group;
+  for (int64_t sl = threadIdx.x; sl < total_slots; sl += blockDim.x) {
+    const int64_t d = sl / group, r = sl - d * group;
+    if (r >= s_cnt[d]) forward[sl] = -1;
+  }
+}
+
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static int plan_impl(const LookupTables& t, int use_lookup, const int64_t* tokens,
@@ -179,13 +254,23 @@ static int plan_impl(const LookupTables& t, int use_lookup, const int64_t* token
   }
   if (n > INT32_MAX) return SMOE_ERR_UNSUPPORTED;
   const int32_t n_blocks = (int32_t)ceil_div(n, kPlanTile);
+  const size_t smem2 = sizeof(int32_t) * (size_t)G * 10;
+  if (n_blocks == 1) {
+    if (smem2 > 48 * 1024)
+      SMOE_CUDA_TRY(cudaFuncSetAttribute(plan_single_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    SMOE_CUDA_TRY(launch_pdl(plan_single_kernel, 1, kPlanThreads, smem2, st, t, use_lookup,
+                             tokens, devices, n, G, dev_out, forward, inverse, counts, group,
+                             err));
+    SMOE_LAUNCH_CHECK();
+    return SMOE_OK;
+  }
   char* w = static_cast<char*>(ws);
   int32_t* dev_ws = reinterpret_cast<int32_t*>(w);
   int32_t* block_counts = reinterpret_cast<int32_t*>(w + align256(sizeof(int32_t) * n));
   SMOE_CUDA_TRY(launch_pdl(plan_count_kernel, n_blocks, kPlanThreads, sizeof(int32_t) * G, st,
       t, use_lookup, tokens, devices, n, G, dev_ws, dev_out, block_counts, err));
   SMOE_LAUNCH_CHECK();
-  const size_t smem2 = sizeof(int32_t) * (size_t)G * 10;
   if (smem2 > 48 * 1024)
     SMOE_CUDA_TRY(cudaFuncSetAttribute(plan_scatter_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));

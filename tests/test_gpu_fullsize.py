@@ -93,3 +93,10 @@ def test_full_size_layer_properties(name, ep):
     got = out[sample].float()
     err = float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref))
     assert err <= TOL, err
+    # per row and per element, not only in aggregate: every sampled row within
+    # 2e-2 relative (row norm), every element within 2e-2 of its row's peak
+    # magnitude (bf16 output + bf16 SwiGLU activations: ~4e-3 expected)
+    row_err = torch.linalg.norm(got - ref, dim=1) / torch.linalg.norm(ref, dim=1)
+    assert float(row_err.max()) <= 2e-2, float(row_err.max())
+    peak = ref.abs().amax(dim=1, keepdim=True)
+    assert float(((got - ref).abs() / peak).max()) <= 2e-2
