@@ -172,6 +172,19 @@ int smoe_event_metrics(const int64_t* experts, const int64_t* weights, int64_t o
                        const int64_t* token_dev, int32_t n_clusters,
                        int64_t* local_out, int64_t* loads_out, int32_t* err, void* stream);
 
+/* solve_ceo's per-iteration sample scoring (solver.py:380-404, §8f rank 4):
+ * counts_nt int32 [n_experts, t] (the token x expert activation counts of
+ * the active tokens, TRANSPOSED), ep_samples int32 [n_samples, n_experts]
+ * and tk_samples int32 [n_samples, t] cluster labels in [0, n_clusters).
+ * ep_score[k] = sum_j max_c mass(k, j, c) and joint[k] = sum_j
+ * mass(k, j, tk[k, j]), mass(k, j, c) = sum of counts[j, n] over experts n
+ * with ep[k, n] == c (the reference's tensordot + max / gather).  Exact
+ * int64 sums.  n_experts <= 64, n_clusters <= 16. */
+int smoe_ceo_sample_scores(const int32_t* counts_nt, int32_t t, int32_t n_experts,
+                           const int32_t* ep_samples, const int32_t* tk_samples,
+                           int32_t n_samples, int32_t n_clusters, int64_t* ep_score,
+                           int64_t* joint, void* stream);
+
 /* schedule_requests_dp (scheduler.py:160-183): request r goes to the
  * highest-affinity device still open in its window of n_devices consecutive
  * requests (first maximum wins).  affinities f64[n_requests, n_devices]. */

@@ -20,7 +20,7 @@ from .comm import (CommError, PipelineSpec, Stage, VolumeReport, dense_pipeline,
                    simulate_trace, sweep_alpha, tensor_parallel_pipeline, vanilla_token_labels,
                    volume_collective)
 from .tables import TableError, export_token_csv, read_bundle, write_bundle
-from .solver import Assignment, SolverError, metrics
+from .solver import Assignment, SolverError, ceo_sample_scores, metrics
 
 __version__ = "0.1.0"
 

@@ -36,6 +36,7 @@ SIGNATURES = [
     ("smoe_remap_index", C.c_int, [P, c_i64, P, c_i64, P, P, P]),
     ("smoe_count_local", C.c_int, [P, c_i64, c_i32, P, c_i32, P, P, P, P]),
     ("smoe_event_metrics", C.c_int, [P, P, c_i64, c_i32, P, c_i32, P, c_i32, P, P, P, P]),
+    ("smoe_ceo_sample_scores", C.c_int, [P, c_i32, c_i32, P, P, c_i32, c_i32, P, P, P]),
     ("smoe_schedule_requests_dp", C.c_int, [P, c_i64, c_i32, P, P]),
     ("smoe_layer_workspace_bytes", c_sz, [P]),
     ("smoe_layer_create", C.c_int, [P, P]),

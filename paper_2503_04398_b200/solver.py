@@ -4,8 +4,10 @@ reference solver.py:766-800), with the event counting on the GPU
 (`smoe_event_metrics`).
 
 The offline co-clustering search itself (`solve_ceo`, `solve_alternating`,
-solver.py:200-760) is out of scope: it runs once per
-deployment and is a sequential accept/reject search, not a data-parallel path.
+solver.py:200-760) runs once per deployment; its sequential greedy polish
+stays on the host.  Its one batched dense step -- scoring the
+K sampled (expert, token) labelings of every cross-entropy iteration
+(solver.py:380-404) -- runs on the GPU: `ceo_sample_scores`.
 """
 
 from __future__ import annotations
@@ -104,3 +106,54 @@ def layer_metrics(layer) -> dict:
     return {"lar": st["local_tokens"] / total if total else 0.0,
             "imbalance": float(loads.max() / median) if median > 0 else math.inf,
             "events": total, "local_events": st["local_tokens"], "loads": loads.tolist()}
+
+
+def ceo_sample_scores(counts, ep_samples, tk_samples, p_ep=None):
+    """One iteration's sample scores of solve_ceo (solver.py:380-404).
+
+    counts: [t, N] activation counts of the active tokens (the reference's
+    `sub_counts`); ep_samples int [K, N] and tk_samples int [K, t] cluster
+    labels.  Returns (ep_scores, tk_scores, joint), float64 [K] each:
+
+      ep_scores[k] = sum_j max_c cluster_mass[k, j, c]        (:388-393)
+      joint[k]     = sum_j cluster_mass[k, j, tk[k, j]]       (:397-399)
+      tk_scores[k] = sum_j (counts @ p_ep)[j, tk[k, j]]       (:395-396)
+
+    ep_scores and joint (the K x t x N tensordot) come from the GPU as exact
+    integer sums, so they equal the reference's float64 values bit for bit;
+    tk_scores (a float64 reduction the reference does with numpy's pairwise
+    sum) is only computed when p_ep is given, on the host with the reference's
+    own expression so it too is bit-identical.
+    """
+    L = _native.lib()
+    t = _dev.torch()
+    c = np.asarray(counts)
+    if c.ndim != 2:
+        raise SolverError("counts must be [tokens, experts]")
+    ep = np.asarray(ep_samples, dtype=np.int64)
+    tk = np.asarray(tk_samples, dtype=np.int64)
+    T, N = c.shape
+    K = ep.shape[0]
+    if ep.shape != (K, N) or tk.shape != (K, T):
+        raise SolverError("sample shapes do not match the count matrix")
+    E = int(max(ep.max(initial=0), tk.max(initial=0))) + 1
+    if ep.size and ep.min() < 0 or tk.size and tk.min() < 0:
+        raise SolverError("cluster labels must be non-negative")
+    if c.size and (c.min() < 0 or c.max() > np.iinfo(np.int32).max):
+        raise SolverError("counts must be non-negative int32 values")
+    cnt = _dev.to_device(np.ascontiguousarray(c.T, dtype=np.int32))
+    ep_d = _dev.to_device(np.ascontiguousarray(ep, dtype=np.int32))
+    tk_d = _dev.to_device(np.ascontiguousarray(tk, dtype=np.int32))
+    es = t.empty(max(K, 1), dtype=t.int64, device=cnt.device)
+    js = t.empty(max(K, 1), dtype=t.int64, device=cnt.device)
+    _native.check(L.smoe_ceo_sample_scores(_native.ptr(cnt), T, N, _native.ptr(ep_d),
+                                           _native.ptr(tk_d), K, E, _native.ptr(es),
+                                           _native.ptr(js), _native.stream_ptr()),
+                  "ceo_sample_scores")
+    ep_scores = es[:K].cpu().numpy().astype(np.float64)
+    joint = js[:K].cpu().numpy().astype(np.float64)
+    tk_scores = None
+    if p_ep is not None:
+        W = np.asarray(c, dtype=np.float64) @ np.asarray(p_ep, dtype=np.float64)
+        tk_scores = W[np.arange(T)[None, :], tk].sum(axis=1)
+    return ep_scores, tk_scores, joint

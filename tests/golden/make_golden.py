@@ -254,6 +254,46 @@ def metrics_cases():
     np.savez_compressed(OUT / "metrics.npz", **out)
 
 
+def ceo_cases():
+    """solve_ceo's per-iteration sample scoring (solver.py:380-404): samples
+    drawn by the reference's own capacity-masked `sample_labels`, `joint`
+    from the reference's `_sample_scores`, ep_scores / tk_scores with the
+    expressions of solver.py:388-396 (the reference computes them inline)."""
+    out = {}
+    ci = 0
+    specs = [(dict(devices=4, clusters=4, experts=16, top_k=2, layers=3, vocab=1024), 0.2, 32),
+             (dict(devices=2, clusters=2, experts=8, top_k=2, layers=2, vocab=512), 0.5, 16),
+             (dict(devices=8, clusters=8, experts=64, top_k=6, layers=2, vocab=4096), 0.3, 64)]
+    for spec, noise, K in specs:
+        topo = profiles.Topology(**spec)
+        mats, trace, truth = profiles.synthesize_planted_profile(
+            topo, noise=noise, tokens_per_cluster=40, seed=ci, reps=4)
+        agg = aggregate(mats)
+        active = np.nonzero(agg.freq > 0)[0]
+        sub = profiles.TokenExpertMatrix(layer=agg.layer, counts=agg.counts[active])
+        sub_counts = agg.counts[active].astype(np.float64)
+        E, N = topo.clusters, topo.experts
+        rng = np.random.default_rng(100 + ci)
+        p_ep = rng.dirichlet(np.ones(E), size=N)
+        p_tk = rng.dirichlet(np.ones(E), size=len(active))
+        ep = solver.sample_labels(p_ep, "expert", None, 1.1, rng, K)
+        tk = solver.sample_labels(p_tk, "token", sub, 1.1, rng, K)
+        onehot = np.zeros((K, N, E))
+        onehot[np.arange(K)[:, None], np.arange(N)[None, :], ep] = 1.0
+        cm = np.tensordot(sub_counts, onehot, axes=([1], [1])).transpose(1, 0, 2)
+        ep_scores = cm.max(axis=2).sum(axis=1)
+        W = sub_counts @ p_ep
+        tk_scores = W[np.arange(len(active))[None, :], tk].sum(axis=1)
+        joint = solver._sample_scores(ep, tk, sub_counts)
+        pre = f"c{ci}_"
+        out[pre + "counts"] = agg.counts[active].astype(np.int64)
+        out[pre + "ep"], out[pre + "tk"], out[pre + "p_ep"] = ep, tk, p_ep
+        out[pre + "ep_scores"], out[pre + "tk_scores"], out[pre + "joint"] = ep_scores, tk_scores, joint
+        ci += 1
+    out["n_cases"] = np.int64(ci)
+    np.savez_compressed(OUT / "ceo.npz", **out)
+
+
 if __name__ == "__main__":
     lookup_cases()
     rebatch_cases()
@@ -262,5 +302,6 @@ if __name__ == "__main__":
     toy_bundle()
     toy_chain()
     metrics_cases()
+    ceo_cases()
     for p in sorted(OUT.glob("*.npz")) + sorted(OUT.glob("*.bin")):
         print(p.name, p.stat().st_size)

@@ -174,3 +174,14 @@ def test_gate_topk_slot_space_ties():
     # identity slot order = the reference's argsort over original ids
     ids, _, _ = layer_ref.gate_topk(None, None, 2, True, logits=logits)
     assert ids[0].tolist() == [0, 1] and ids[2].tolist() == [2, 0]
+
+
+@pytest.mark.parametrize("c", cases("ceo"), ids=lambda c: f"t{c['counts'].shape[0]}")
+def test_ceo_scores_golden(c):
+    """oracle.solver_ref vs the reference's solve_ceo scoring expressions and
+    its `_sample_scores` (tests/golden/ceo.npz), bit for bit."""
+    from oracle import solver_ref
+    ep_s, tk_s, joint = solver_ref.ceo_scores(c["counts"], c["ep"], c["tk"], c["p_ep"])
+    assert np.array_equal(ep_s, c["ep_scores"])
+    assert np.array_equal(joint, c["joint"])
+    assert np.array_equal(tk_s, c["tk_scores"])
