@@ -67,6 +67,10 @@ const char* smoe_version(void);
 #define SMOE_OPT_GEMM_NARROW_MAX_ROWS 6 /* layer GEMMs: 32-row m-blocks, 5-stage     */
                                         /* weight ring while n*k <= this * n_experts */
                                         /* (default 0 = off)                         */
+#define SMOE_OPT_DEDUP_DISPATCH      7  /* layers spanning processes: 1 (default) =   */
+                                        /* send each token row once per remote shard */
+                                        /* (the owner fans it out to its experts),   */
+                                        /* 0 = one row per remote (token, expert)    */
 int smoe_set_option(int32_t key, int32_t value);
 int smoe_get_option(int32_t key);
 const char* smoe_status_string(int status);
@@ -247,6 +251,9 @@ enum {
                           /* next layer's n-gram window = this window shifted by one  */
                           /* plus the cluster of each token's top-1 expert            */
                           /* (predictor.py:165-166)                                   */
+  SMOE_BUF_XFAN,          /* peer, per shard (processes > 1): int32 [expert_rows]     */
+                          /* fan-out table of the deduplicated dispatch (-1 = row    */
+                          /* stored; else the row to copy it from)                   */
   SMOE_BUF_AR,            /* bf16 [max_tokens, d], per process (bind for every shard; */
                           /* co-resident shards share): DS-MoE all-reduce output     */
   SMOE_BUF_AG,            /* bf16 [ag_rows, d], per process: DS-MoE all-gather of the */
@@ -262,6 +269,9 @@ enum {
   SMOE_STAT_GROUP,             /* max group (scheduler.py:135)                              */
   SMOE_STAT_REMOTE_ROWS,       /* distinct (token, other shard) pairs: rows a dispatch that */
                                /* deduplicates per destination shard would send             */
+  SMOE_STAT_SENT_ROWS,         /* rows the dispatch stored into shards of OTHER processes   */
+                               /* (with SMOE_OPT_DEDUP_DISPATCH: one per (token, remote     */
+                               /* shard), else one per remote-process pair)                 */
   SMOE_STAT__COUNT = 16
 };
 

@@ -83,13 +83,15 @@ OPT_GEMM_PAIR_MIN_ROWS = 3
 OPT_PDL = 4
 OPT_PDL_STAGES = 5
 OPT_GEMM_NARROW_MAX_ROWS = 6
+OPT_DEDUP_DISPATCH = 7
 
 (BUF_PARTIAL, BUF_XIN, BUF_XMETA, BUF_YPAIR, BUF_OUT, BUF_COUNTS, BUF_SIGNAL, BUF_HS,
  BUF_TOPK_IDS, BUF_TOPK_W, BUF_PAIR_RANK, BUF_HMID, BUF_FORWARD, BUF_INVERSE, BUF_DEV,
  BUF_PLAN_COUNTS, BUF_GROUP, BUF_STATS, BUF_ERR, BUF_WORKSPACE, BUF_PROBLEMS,
- BUF_EPOCH, BUF_HIST_OUT, BUF_AR, BUF_AG) = range(25)
+ BUF_EPOCH, BUF_HIST_OUT, BUF_XFAN, BUF_AR, BUF_AG) = range(26)
 PIPELINE_SMOE, PIPELINE_DSMOE = 0, 1
-STAT_LOCAL_PAIRS, STAT_REMOTE_PAIRS, STAT_SRS_ROWS, STAT_GROUP, STAT_REMOTE_ROWS = range(5)
+(STAT_LOCAL_PAIRS, STAT_REMOTE_PAIRS, STAT_SRS_ROWS, STAT_GROUP, STAT_REMOTE_ROWS,
+ STAT_SENT_ROWS) = range(6)
 STAT_COUNT = 16
 (STAGE_PLAN, STAGE_SRS, STAGE_GATE, STAGE_ROUTE, STAGE_DISPATCH, STAGE_EXPERT_UP,
  STAGE_EXPERT_DOWN, STAGE_COMBINE_SAG) = range(8)

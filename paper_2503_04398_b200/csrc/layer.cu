@@ -205,6 +205,8 @@ static ShardPtrs distinct_ptrs_local_first(const smoe_layer* L, int slot, int32_
   return p;
 }
 
+static int g_dedup_dispatch = 1;      // SMOE_OPT_DEDUP_DISPATCH
+
 static int check_bound(const smoe_layer* L) {
   const auto& c = L->cfg;
   for (int g = 0; g < c.n_shards; ++g)
@@ -435,15 +437,25 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       return smoe_layer_barrier(L, stream);
     }
     case SMOE_STAGE_DISPATCH: {
+      // deduplicated dispatch across processes (every shard's fan-out table bound)
+      bool dedup = g_dedup_dispatch && c.world_size > 1;
+      for (int g = 0; g < c.n_shards && dedup; ++g) dedup = L->buf[SMOE_BUF_XFAN][g] != nullptr;
+      const ShardPtrs xfan = dedup ? peer_ptrs(L, SMOE_BUF_XFAN) : ShardPtrs{};
+      int64_t* problems = static_cast<int64_t*>(L->buf[SMOE_BUF_PROBLEMS][0]);
       rc = launch_dispatch(lr, c.n_experts, c.top_k, c.hidden,
                            static_cast<const int32_t*>(L->buf[SMOE_BUF_COUNTS][c.shard_begin]),
                            L->slot_owner_d, L->slot_first_d, local_ptrs(L, SMOE_BUF_HS),
                            local_ptrs(L, SMOE_BUF_TOPK_IDS), local_ptrs(L, SMOE_BUF_PAIR_RANK),
                            peer_ptrs(L, SMOE_BUF_XIN), peer_ptrs(L, SMOE_BUF_XMETA),
-                           c.expert_rows, static_cast<int64_t*>(L->buf[SMOE_BUF_PROBLEMS][0]),
-                           err, n, st);
+                           c.expert_rows, problems, err, n, st, xfan, stats);
       if (rc) return rc;
-      return smoe_layer_barrier(L, stream);
+      rc = smoe_layer_barrier(L, stream);
+      if (rc || !dedup) return rc;
+      // the owners' side: copy each remote token row to its other experts here
+      return launch_fanout(problems, L->local_slots, peer_ptrs(L, SMOE_BUF_XIN), xfan,
+                           c.shard_begin, c.expert_rows, c.hidden, L->slot_owner_d,
+                           L->slot_first_d,
+                           std::min<int64_t>(n * c.top_k, c.expert_rows * c.shard_count), st);
     }
     case SMOE_STAGE_EXPERT_UP: {
       GemmArgs a{};
@@ -597,6 +609,10 @@ extern "C" int smoe_set_option(int32_t key, int32_t value) {
       if (value < 0) return SMOE_ERR_INVALID_ARG;
       set_gemm_narrow_max_rows(value);
       return SMOE_OK;
+    case SMOE_OPT_DEDUP_DISPATCH:
+      if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
+      g_dedup_dispatch = value;
+      return SMOE_OK;
     case SMOE_OPT_PDL:
       if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
       set_pdl_enabled(value);
@@ -618,6 +634,7 @@ extern "C" int smoe_get_option(int32_t key) {
   if (key == SMOE_OPT_GEMM_NARROW_MAX_ROWS) return gemm_narrow_max_rows();
   if (key == SMOE_OPT_PDL) return pdl_enabled();
   if (key == SMOE_OPT_PDL_STAGES) return pdl_stage_mask();
+  if (key == SMOE_OPT_DEDUP_DISPATCH) return g_dedup_dispatch;
   return -1;
 }
 

@@ -755,7 +755,7 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
                 const int32_t* __restrict__ slot_owner, const int32_t* __restrict__ slot_first,
                 ShardPtrs hs, ShardPtrs topk_ids, ShardPtrs pair_rank, ShardPtrs xin,
                 ShardPtrs xmeta, int64_t expert_rows, int64_t* problems, int32_t* err,
-                int32_t whole_rows) {
+                int32_t whole_rows, ShardPtrs xfan, int64_t* stats) {
   pdl_enter();
   __shared__ RowMap rm;
   __shared__ int32_t s_M[kGateMaxN];
@@ -766,11 +766,13 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
   __shared__ char* s_rank[SMOE_MAX_SHARDS];
   __shared__ char* s_xin[SMOE_MAX_SHARDS];
   __shared__ char* s_xmeta[SMOE_MAX_SHARDS];
+  __shared__ char* s_xfan[SMOE_MAX_SHARDS];
   stage_ptrs(s_hs, hs);
   stage_ptrs(s_ids, topk_ids);
   stage_ptrs(s_rank, pair_rank);
   stage_ptrs(s_xin, xin);
   stage_ptrs(s_xmeta, xmeta);
+  stage_ptrs(s_xfan, xfan);     // all null: no deduplication (every pair carries its row)
   const int G = lr.n_shards;
   const int tid = threadIdx.x, lane = tid & 31;
   // the [G, N] count matrix -> shared memory in one round of loads (it was
@@ -821,12 +823,47 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
     const int32_t* rk = reinterpret_cast<const int32_t*>(s_rank[gl]) + j * k;
     char* dst[kGateMaxK];
     int32_t nd = 0;
-    for (int s = 0; s < k; ++s) {
-      const int32_t e = ids[s];
-      const int32_t o = slot_owner[e];
-      const int64_t pos = (int64_t)s_off[g * N + e] + rk[s];
+    int64_t pos_s[kGateMaxK];
+    int32_t own_s[kGateMaxK];
+#pragma unroll
+    for (int s = 0; s < kGateMaxK; ++s) {
+      pos_s[s] = -1;
+      own_s[s] = -1;
+      if (s < k) {
+        const int32_t e = ids[s];
+        own_s[s] = slot_owner[e];
+        pos_s[s] = (int64_t)s_off[g * N + e] + rk[s];
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < kGateMaxK; ++s) {
+      if (s >= k) break;
+      const int32_t o = own_s[s];
+      const int64_t pos = pos_s[s];
       if (pos >= expert_rows) { if (lane == 0) set_err(err, SMOE_ERRBIT_CAPACITY); continue; }
-      dst[nd++] = s_xin[o] + pos * d * 2;
+      // deduplicated dispatch (xfan bound): an owner in another process gets
+      // the row once, in the slot of the token's FIRST pair there; its other
+      // pairs there only record that slot, and the owner copies the row
+      // locally (fanout_kernel) -- one NVLink row per (token, remote shard)
+      // instead of one per (token, expert), DeepEP-style
+      const bool remote_proc = o < lr.shard_begin || o >= lr.shard_begin + lr.shard_count;
+      int64_t first = -1;
+      if (s_xfan[o] != nullptr) {
+        if (remote_proc) {
+#pragma unroll
+          for (int s2 = 0; s2 < kGateMaxK; ++s2)
+            if (s2 < s && first < 0 && own_s[s2] == o && pos_s[s2] < expert_rows)
+              first = pos_s[s2];
+        }
+        // every row of the owner's buffer gets its entry for this batch (-1:
+        // the row itself was stored), so the fan-out never acts on stale ones
+        if (lane == 0 && c == 0) reinterpret_cast<int32_t*>(s_xfan[o])[pos] = (int32_t)first;
+      }
+      if (first < 0) {
+        dst[nd++] = s_xin[o] + pos * d * 2;
+        if (lane == 0 && c == 0 && remote_proc && stats)
+          atomicAdd(reinterpret_cast<unsigned long long*>(stats + SMOE_STAT_SENT_ROWS), 1ull);
+      }
       if (lane == 0 && c == 0)
         reinterpret_cast<int64_t*>(s_xmeta[o])[pos] = ((int64_t)g << 40) | (j * k + s);
     }
@@ -849,17 +886,61 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
   }
 }
 
+// Owner side of the deduplicated dispatch: every expert-input row whose
+// xfan entry names another row of the same buffer (a token's non-first pair
+// at this shard, sent from another process) is copied from it.  Warp per row
+// (or 1 KiB chunk), over the resident shards' problem rows.
+__global__ void __launch_bounds__(256)
+fanout_kernel(const int64_t* __restrict__ problems, int32_t n_problems, ShardPtrs xin,
+              ShardPtrs xfan, int32_t shard_begin, int64_t expert_rows, int64_t d,
+              const int32_t* __restrict__ slot_owner, const int32_t* __restrict__ slot_first) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  const int64_t vecs = d / 8;
+  const int64_t chunks = (vecs + kChunkVecs - 1) / kChunkVecs;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int32_t e0 = slot_first[shard_begin];
+  for (int32_t p = 0; p < n_problems; ++p) {
+    const int64_t m = problems[4 * p + 1];
+    const int32_t o = slot_owner[e0 + p];
+    const int64_t seg = problems[4 * p] - (int64_t)(o - shard_begin) * expert_rows;
+    const int32_t* fan = reinterpret_cast<const int32_t*>(xfan.p[o]);
+    char* base = xin.p[o];
+    for (int64_t it = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+         it < m * chunks; it += nwarps) {
+      const int64_t r = seg + it / chunks, c = it % chunks;
+      const int32_t f = fan[r];
+      if (f < 0) continue;
+      const int64_t v1 = min(vecs, (c + 1) * kChunkVecs);
+      for (int64_t v = c * kChunkVecs + lane; v < v1; v += 32)
+        st_v4(base + (r * d + v * 8) * 2, ld_v4(base + ((int64_t)f * d + v * 8) * 2));
+    }
+  }
+}
+
+int launch_fanout(const int64_t* problems, int32_t n_problems, const ShardPtrs& xin,
+                  const ShardPtrs& xfan, int32_t shard_begin, int64_t expert_rows, int64_t d,
+                  const int32_t* slot_owner, const int32_t* slot_first, int64_t rows_bound,
+                  cudaStream_t st) {
+  if (n_problems <= 0 || rows_bound <= 0) return SMOE_OK;
+  SMOE_CUDA_TRY(launch_pdl(fanout_kernel, grid_items(rows_bound, d), 256, 0, st, problems,
+                           n_problems, xin, xfan, shard_begin, expert_rows, d, slot_owner,
+                           slot_first));
+  SMOE_LAUNCH_CHECK();
+  return SMOE_OK;
+}
+
 int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
                     const int32_t* counts_mat, const int32_t* slot_owner,
                     const int32_t* slot_first, const ShardPtrs& hs, const ShardPtrs& topk_ids,
                     const ShardPtrs& pair_rank, const ShardPtrs& xin, const ShardPtrs& xmeta,
                     int64_t expert_rows, int64_t* problems, int32_t* err, int64_t n_rows_bound,
-                    cudaStream_t st) {
+                    cudaStream_t st, const ShardPtrs& xfan, int64_t* stats) {
   if (N > kGateMaxN || d % 8) return SMOE_ERR_UNSUPPORTED;
   SMOE_CUDA_TRY(launch_pdl(dispatch_kernel, grid_items(std::max<int64_t>(n_rows_bound, 1), d),
                            256, 0, st, lr, N, k, d, counts_mat, slot_owner, slot_first, hs,
                            topk_ids, pair_rank, xin, xmeta, expert_rows, problems, err,
-                           whole_rows_from()));
+                           whole_rows_from(), xfan, stats));
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }

@@ -61,12 +61,18 @@ int launch_route(const LocalRows& lr, int32_t N, int32_t k, const ShardPtrs& top
                  const ShardPtrs& pair_rank, const ShardPtrs& count_bufs, int32_t n_count_bufs,
                  int32_t* chunk_counts, int64_t n_rows_bound, cudaStream_t st);
 
+// xfan: per-shard int32 [expert_rows] fan-out tables of the deduplicated
+// dispatch, non-null only for shards in OTHER processes (see dispatch_kernel)
 int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
                     const int32_t* counts_mat, const int32_t* slot_owner,
                     const int32_t* slot_first, const ShardPtrs& hs, const ShardPtrs& topk_ids,
                     const ShardPtrs& pair_rank, const ShardPtrs& xin, const ShardPtrs& xmeta,
                     int64_t expert_rows, int64_t* problems, int32_t* err, int64_t n_rows_bound,
-                    cudaStream_t st);
+                    cudaStream_t st, const ShardPtrs& xfan, int64_t* stats);
+int launch_fanout(const int64_t* problems, int32_t n_problems, const ShardPtrs& xin,
+                  const ShardPtrs& xfan, int32_t shard_begin, int64_t expert_rows, int64_t d,
+                  const int32_t* slot_owner, const int32_t* slot_first, int64_t rows_bound,
+                  cudaStream_t st);
 
 struct HistUpdate {
   const int64_t* hist_in;     // [n, hist_len] or nullptr (first layers)

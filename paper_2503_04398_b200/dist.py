@@ -98,7 +98,7 @@ class ShardGroup:
         # two partial-input buffers: forward_async fills one while the peers'
         # SRS reads the other
         per_shard = {"partial": n * d * 2, "partial_b": n * d * 2, "xin": R * d * 2,
-                     "xmeta": R * 8, "ypair": n * k * d * 2}
+                     "xmeta": R * 8, "xfan": R * 4, "ypair": n * k * d * 2}
         h = max(int(layer.tables.ngram_n), 1)
         # one output (and next-layer history) per process: the SAG delivers
         # every token's row to each process once, whichever of its shards

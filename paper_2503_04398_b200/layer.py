@@ -202,6 +202,8 @@ class SpecMoELayer:
             bind(N.BUF_PARTIAL, g, p["partial"][g])
             bind(N.BUF_XIN, g, p["xin"][g])
             bind(N.BUF_XMETA, g, p["xmeta"][g])
+            if "xfan" in p:                     # processes > 1: deduplicated dispatch
+                bind(N.BUF_XFAN, g, p["xfan"][g])
             bind(N.BUF_YPAIR, g, p["ypair"][g])
             bind(N.BUF_OUT, g, p["out"][g])
             bind(N.BUF_COUNTS, g, p["counts"][g])
@@ -585,19 +587,25 @@ class SpecMoELayer:
         sag_bytes = int(counts.sum()) * (G - 1) * row      # rows pushed to other shards
         a2a = remote * row
         rrows = int(s[N.STAT_REMOTE_ROWS])
+        # the dispatch sends one row per (token, remote shard) when the
+        # deduplicated dispatch is on (SMOE_OPT_DEDUP_DISPATCH, the default),
+        # else one per remote (token, expert) pair -- the reference's event
+        # model (comm.py:86); the combine returns one row per remote pair
+        dedup = bool(self.lib.smoe_get_option(N.OPT_DEDUP_DISPATCH))
         return {
             "local_tokens": local, "remote_tokens": remote,
             "measured_alpha": local / max(local + remote, 1),
             "group_size": group, "device_counts": counts.tolist(),
             "pair_counts": cm.tolist(),
-            "bytes": {"srs": srs_bytes, "a2a_dispatch": a2a, "a2a_combine": a2a,
-                      "sag": sag_bytes,
+            "bytes": {"srs": srs_bytes, "a2a_dispatch": (rrows if dedup else remote) * row,
+                      "a2a_combine": a2a, "sag": sag_bytes,
                       "srs_padded_model": G * group * (G - 1) * row,
                       "reference_model_a2a": a2a,
-                      # one row per (token, destination shard) instead of one
-                      # per (token, expert): a deduplicating dispatch (not built)
                       "a2a_dispatch_dedup_model": rrows * row},
             "remote_rows": rrows,
+            # rows the dispatch actually stored into other processes' shards
+            # (deduplicated: one per (token, remote shard), SMOE_OPT_DEDUP_DISPATCH)
+            "sent_rows": int(s[N.STAT_SENT_ROWS]),
         }
 
 

@@ -213,3 +213,29 @@ def dsmoe_pipeline_worker(rank, world, port, cfg_over, n, result_q):
         grp.close()
     finally:
         dist.destroy_process_group()
+
+
+def dedup_worker(rank, world, port, cfg_over, n, dedup, result_q):
+    """SpecMoELayer over a ShardGroup with the deduplicated dispatch on / off:
+    outputs and the rows the dispatch stored into other processes."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    bind_device(rank, world)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2503_04398_b200 import SpecMoELayer, synth, _native as N
+        from paper_2503_04398_b200.dist import ShardGroup
+        N.check(N.lib().smoe_set_option(N.OPT_DEDUP_DISPATCH, int(dedup)), "set_option")
+        w = synth.make_workload("toy", n=n, eps=0.3, seed=21, cfg_override=cfg_over)
+        grp = ShardGroup.from_torch_distributed()
+        layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=w.cfg["k"],
+                             max_tokens=n, group=grp)
+        L = layer.shard_count
+        mine = torch.from_numpy(w.partials[layer.shard_begin:layer.shard_begin + L]).cuda()
+        outs = [layer.forward(mine, w.tokens, w.hist).float().cpu().numpy() for _ in range(2)]
+        result_q.put((rank, outs, layer.stats()["sent_rows"]))
+        dist.barrier()
+        grp.close()
+    finally:
+        dist.destroy_process_group()
