@@ -5,8 +5,9 @@
 
 namespace smoe {
 
-constexpr int kGateMaxN = 64;
+constexpr int kGateMaxN = 64;      // CUDA-core / mma.sync gates and warp_topk
 constexpr int kGateMaxK = 8;
+constexpr int kMaxExperts = 256;   // the layer (tcgen05 gate, route, dispatch)
 
 // Softmax + ordered top-k of one row with a warp: lane holds the logits of
 // slots `lane` (v0) and `lane + 32` (v1), NaN for slots >= N.  Larger logit

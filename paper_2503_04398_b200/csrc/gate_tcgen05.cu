@@ -28,6 +28,7 @@
 // N are TMA out-of-bounds fills (zeros) and are masked to -inf.  Rows past a
 // shard's token count are computed and discarded.
 #include "common.cuh"
+#include "gate_select.cuh"
 #include "gemm.h"
 #include "layer_kernels.cuh"
 #include "tc_ptx.cuh"
@@ -51,7 +52,8 @@ template <int NP, int SUB, int ST> struct GtShape {
   static constexpr uint32_t kWBox = NP * kGemmBK * 2;     // NP rows of 128 B
   static constexpr uint32_t kWBytes = SUB * kWBox;
   static constexpr uint32_t kStageBytes = kHBytes + kWBytes;
-  static constexpr uint32_t kTmemCols = 2 * NP <= 32 ? 32 : (2 * NP <= 64 ? 64 : 128);
+  static constexpr uint32_t kTmemCols =
+      2 * NP <= 32 ? 32 : 2 * NP <= 64 ? 64 : 2 * NP <= 128 ? 128 : 2 * NP <= 256 ? 256 : 512;
   static constexpr uint32_t kAccCols = kTmemCols / 2;      // column stride of the 2 accumulators
   static constexpr size_t kSmem = 1024 + ST * kStageBytes + 128;
   // D f32, A/B bf16, both K-major, N = NP, M = 128
@@ -216,71 +218,146 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
       decode(t, gl, blk);
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      uint32_t v[NP];
       const uint32_t taddr = tmem_base + acc * S::kAccCols + ((uint32_t)(ew * 32) << 16);
-#pragma unroll
-      for (int c = 0; c < NP / 16; ++c) SMOE_TMEM_LD16(taddr + c * 16, (v + c * 16));
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty0 + 8 * acc);     // accumulator free for tile t + 2
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
-
       const int64_t j = (int64_t)blk * kGtRows + ew * 32 + lane;
-      if (j >= s_cnt[gl]) continue;
       // order-preserving int keys (+0 and -0 merged, -inf an ordinary
       // candidate); INT_MIN marks "not a candidate" (slots >= N, slots
       // already taken), so fewer than k finite logits still give k distinct
       // slots, as the stable argsort of the reference idiom does
-      constexpr int NT = NP <= 16 ? 16 : (NP <= 32 ? 32 : 64);   // tree leaves (power of 2)
-      int32_t key[NT];
-#pragma unroll
-      for (int e = 0; e < NT; ++e) {
-        const int32_t b = e < NP ? __float_as_int(__uint_as_float(v[e]) + s_bias[e] + 0.0f) : 0;
-        key[e] = e < N ? (b >= 0 ? b : b ^ 0x7fffffff) : INT_MIN;
-      }
+      auto to_key = [](float x) {
+        const int32_t b = __float_as_int(x + 0.0f);
+        return b >= 0 ? b : b ^ 0x7fffffff;
+      };
+      auto key_to_f = [](int32_t k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); };
       int sel_e[kGtMaxK];
       int32_t sel_k[kGtMaxK];
-      uint64_t taken = 0;      // a bit mask, not stores into key[]: a store at the
-                               // winner's index became local memory (STL)
-#pragma unroll
-      for (int s = 0; s < kGtMaxK; ++s) {
-        sel_e[s] = 0;
-        sel_k[s] = INT_MIN;
-        if (s < K) {
-          // max-tree: the right child wins only when strictly larger, so
-          // equal logits resolve to the lower s-EG slot (test_acceptance.py:179-193)
-          int32_t tv[NT / 2];
-          int ti[NT / 2];
-#pragma unroll
-          for (int i = 0; i < NT / 2; ++i) {
-            const int32_t k0 = ((taken >> (2 * i)) & 1) ? INT_MIN : key[2 * i];
-            const int32_t k1 = ((taken >> (2 * i + 1)) & 1) ? INT_MIN : key[2 * i + 1];
-            const bool r = k1 > k0;
-            tv[i] = r ? k1 : k0;
-            ti[i] = r ? 2 * i + 1 : 2 * i;
-          }
-#pragma unroll
-          for (int w = NT / 4; w >= 1; w >>= 1) {
-#pragma unroll
-            for (int i = 0; i < w; ++i) {
-              const bool r = tv[2 * i + 1] > tv[2 * i];
-              tv[i] = r ? tv[2 * i + 1] : tv[2 * i];
-              ti[i] = r ? ti[2 * i + 1] : ti[2 * i];
-            }
-          }
-          sel_e[s] = ti[0];
-          sel_k[s] = tv[0];
-          taken |= 1ull << ti[0];
-        }
-      }
-      auto key_to_f = [](int32_t k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); };
-      const float mx = key_to_f(sel_k[0]);
       float ex = 0.f;
+      if constexpr (NP <= 64) {
+        // every logit of the row in registers; the accumulator is released
+        // before the selection so the MMAs of tile t + 2 can start
+        uint32_t v[NP];
 #pragma unroll
-      for (int e = 0; e < NP; ++e)
-        if (e < N) ex += __expf(__uint_as_float(v[e]) + s_bias[e] - mx);
+        for (int c = 0; c < NP / 16; ++c) SMOE_TMEM_LD16(taddr + c * 16, (v + c * 16));
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty0 + 8 * acc);     // accumulator free for tile t + 2
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        if (j >= s_cnt[gl]) continue;
+        constexpr int NT = NP <= 16 ? 16 : (NP <= 32 ? 32 : 64);   // tree leaves (power of 2)
+        int32_t key[NT];
+#pragma unroll
+        for (int e = 0; e < NT; ++e)
+          key[e] = e < N ? to_key(__uint_as_float(v[e < NP ? e : 0]) + s_bias[e < NP ? e : 0])
+                         : INT_MIN;
+        uint64_t taken = 0;      // a bit mask, not stores into key[]: a store at the
+                                 // winner's index became local memory (STL)
+#pragma unroll
+        for (int s = 0; s < kGtMaxK; ++s) {
+          sel_e[s] = 0;
+          sel_k[s] = INT_MIN;
+          if (s < K) {
+            // max-tree: the right child wins only when strictly larger, so
+            // equal logits resolve to the lower s-EG slot (test_acceptance.py:179-193)
+            int32_t tv[NT / 2];
+            int ti[NT / 2];
+#pragma unroll
+            for (int i = 0; i < NT / 2; ++i) {
+              const int32_t k0 = ((taken >> (2 * i)) & 1) ? INT_MIN : key[2 * i];
+              const int32_t k1 = ((taken >> (2 * i + 1)) & 1) ? INT_MIN : key[2 * i + 1];
+              const bool r = k1 > k0;
+              tv[i] = r ? k1 : k0;
+              ti[i] = r ? 2 * i + 1 : 2 * i;
+            }
+#pragma unroll
+            for (int w = NT / 4; w >= 1; w >>= 1) {
+#pragma unroll
+              for (int i = 0; i < w; ++i) {
+                const bool r = tv[2 * i + 1] > tv[2 * i];
+                tv[i] = r ? tv[2 * i + 1] : tv[2 * i];
+                ti[i] = r ? ti[2 * i + 1] : ti[2 * i];
+              }
+            }
+            sel_e[s] = ti[0];
+            sel_k[s] = tv[0];
+            taken |= 1ull << ti[0];
+          }
+        }
+        const float mx = key_to_f(sel_k[0]);
+#pragma unroll
+        for (int e = 0; e < NP; ++e)
+          if (e < N) ex += __expf(__uint_as_float(v[e]) + s_bias[e] - mx);
+      } else {
+        // N' > 64 (e.g. DeepSeek-V2, 160 experts): too many logits for one
+        // thread's registers -- each selection pass re-reads the row from
+        // TMEM 16 columns at a time (max-tree per chunk, the earlier chunk
+        // winning ties), then one more pass sums the softmax denominator;
+        // the accumulator is released after the last read
+        constexpr int NC = NP / 16;
+        uint32_t tk[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) tk[c] = 0;
+#pragma unroll 1
+        for (int s = 0; s < kGtMaxK; ++s) {
+          sel_e[s] = 0;
+          sel_k[s] = INT_MIN;
+          if (s >= K) continue;
+          int32_t bk = INT_MIN;
+          int bi = 0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            uint32_t v[16];
+            SMOE_TMEM_LD16(taddr + c * 16, v);
+            tmem_wait_ld();
+            int32_t tv[8];
+            int ti[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int e0 = c * 16 + 2 * i, e1 = e0 + 1;
+              const int32_t k0 = (e0 < N && !((tk[c] >> (2 * i)) & 1))
+                                     ? to_key(__uint_as_float(v[2 * i]) + s_bias[e0]) : INT_MIN;
+              const int32_t k1 = (e1 < N && !((tk[c] >> (2 * i + 1)) & 1))
+                                     ? to_key(__uint_as_float(v[2 * i + 1]) + s_bias[e1]) : INT_MIN;
+              const bool r = k1 > k0;
+              tv[i] = r ? k1 : k0;
+              ti[i] = r ? e1 : e0;
+            }
+#pragma unroll
+            for (int w = 4; w >= 1; w >>= 1) {
+#pragma unroll
+              for (int i = 0; i < w; ++i) {
+                const bool r = tv[2 * i + 1] > tv[2 * i];
+                tv[i] = r ? tv[2 * i + 1] : tv[2 * i];
+                ti[i] = r ? ti[2 * i + 1] : ti[2 * i];
+              }
+            }
+            if (tv[0] > bk) { bk = tv[0]; bi = ti[0]; }
+          }
+          sel_e[s] = bi;
+          sel_k[s] = bk;
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+            if (c == (bi >> 4)) tk[c] |= 1u << (bi & 15);
+        }
+        const float mx = key_to_f(sel_k[0]);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          uint32_t v[16];
+          SMOE_TMEM_LD16(taddr + c * 16, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c * 16 + i < N) ex += __expf(__uint_as_float(v[i]) + s_bias[c * 16 + i] - mx);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        if (j >= s_cnt[gl]) continue;
+      }
+      const float mx = key_to_f(sel_k[0]);
       const float inv = 1.0f / ex;
       float sel_p[kGtMaxK];
       float psum = 0.f;
@@ -365,10 +442,15 @@ static int ring_sub() {
 template <int NP>
 static int launch_np(const CUtensorMap& mh, const CUtensorMap& mw, const GateTcArgs& a,
                      int64_t n_rows_bound, cudaStream_t st) {
-  switch (ring_sub()) {
-    case 1: return launch_cfg<NP, 1, 8>(mh, mw, a, n_rows_bound, st);
-    case 4: return launch_cfg<NP, 4, 2>(mh, mw, a, n_rows_bound, st);
-    default: return launch_cfg<NP, 2, 4>(mh, mw, a, n_rows_bound, st);
+  // wide gates: one k-block per stage keeps 4 stages of H + W(N' x 64) in smem
+  if constexpr (NP > 64) {
+    return launch_cfg<NP, 1, 4>(mh, mw, a, n_rows_bound, st);
+  } else {
+    switch (ring_sub()) {
+      case 1: return launch_cfg<NP, 1, 8>(mh, mw, a, n_rows_bound, st);
+      case 4: return launch_cfg<NP, 4, 2>(mh, mw, a, n_rows_bound, st);
+      default: return launch_cfg<NP, 2, 4>(mh, mw, a, n_rows_bound, st);
+    }
   }
 }
 
@@ -376,10 +458,15 @@ static int g_gate_tc = 1;
 int gate_tc_enabled() { return g_gate_tc; }
 void set_gate_tc_enabled(int on) { g_gate_tc = on ? 1 : 0; }
 
-int gate_tc_rows(int32_t n_experts) { return std::max(16, (n_experts + 15) / 16 * 16); }
+// W box rows N': N rounded up to 16, and above 64 to 128 / 160 / 192 / 256
+int gate_tc_rows(int32_t n_experts) {
+  const int r = std::max(16, (n_experts + 15) / 16 * 16);
+  if (r <= 64) return r;
+  return r <= 128 ? 128 : r <= 160 ? 160 : r <= 192 ? 192 : 256;
+}
 
 bool gate_tc_supported(int32_t n_experts, int32_t top_k, int64_t d) {
-  return n_experts >= 1 && n_experts <= 64 && top_k >= 1 && top_k <= kGtMaxK &&
+  return n_experts >= 1 && n_experts <= kMaxExperts && top_k >= 1 && top_k <= kGtMaxK &&
          top_k <= n_experts && d % (4 * kGemmBK) == 0;
 }
 
@@ -391,6 +478,10 @@ int launch_gate_tc(const CUtensorMap& map_h, const CUtensorMap& map_w, const Gat
     case 32: return launch_np<32>(map_h, map_w, a, n_rows_bound, st);
     case 48: return launch_np<48>(map_h, map_w, a, n_rows_bound, st);
     case 64: return launch_np<64>(map_h, map_w, a, n_rows_bound, st);
+    case 128: return launch_np<128>(map_h, map_w, a, n_rows_bound, st);
+    case 160: return launch_np<160>(map_h, map_w, a, n_rows_bound, st);
+    case 192: return launch_np<192>(map_h, map_w, a, n_rows_bound, st);
+    case 256: return launch_np<256>(map_h, map_w, a, n_rows_bound, st);
     default: return SMOE_ERR_UNSUPPORTED;
   }
 }

@@ -9,6 +9,7 @@
 #include "common.cuh"
 #include "gemm.h"
 #include "layer_kernels.cuh"
+#include "gate_select.cuh"
 
 #include <cstring>
 #include <vector>
@@ -73,7 +74,7 @@ extern "C" size_t smoe_layer_workspace_bytes(const smoe_layer_config* cfg) {
 extern "C" int smoe_layer_create(const smoe_layer_config* cfg, smoe_layer** out) {
   if (!valid_cfg(cfg) || !out) return SMOE_ERR_INVALID_ARG;
   if (cfg->hidden % kGemmBN != 0 || cfg->ffn % 128 != 0 || (2 * cfg->ffn) % kGemmBN != 0 ||
-      cfg->n_experts > 64 || cfg->top_k > 8)
+      cfg->n_experts > kMaxExperts || cfg->top_k > 8)
     return SMOE_ERR_UNSUPPORTED;
   smoe_layer* L = new smoe_layer();
   L->cfg = *cfg;

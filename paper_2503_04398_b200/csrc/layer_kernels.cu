@@ -628,7 +628,7 @@ __global__ void __launch_bounds__(kRouteThreads)
 route_count_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids,
                    int32_t* __restrict__ chunk_counts, int32_t max_chunks) {
   pdl_enter();
-  __shared__ int32_t s_cnt[kGateMaxN];
+  __shared__ int32_t s_cnt[kMaxExperts];
   __shared__ char* s_ids[SMOE_MAX_SHARDS];
   stage_ptrs(s_ids, topk_ids);
   const int gl = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
@@ -654,8 +654,8 @@ route_rank_kernel(LocalRows lr, int32_t N, int32_t k, ShardPtrs topk_ids, ShardP
                   const int32_t* __restrict__ chunk_counts, int32_t max_chunks,
                   ShardPtrs count_bufs, int32_t n_count_bufs) {
   pdl_enter();
-  __shared__ int32_t s_pre[kGateMaxN];
-  __shared__ int32_t s_w[32 * kGateMaxN];
+  __shared__ int32_t s_pre[kMaxExperts];
+  __shared__ int32_t s_w[32 * kMaxExperts];
   __shared__ char* s_ids[SMOE_MAX_SHARDS];
   __shared__ char* s_rank[SMOE_MAX_SHARDS];
   __shared__ char* s_cb[SMOE_MAX_SHARDS];
@@ -722,7 +722,7 @@ size_t route_workspace_bytes(int64_t max_tokens, int32_t k, int32_t N, int32_t s
 int launch_route(const LocalRows& lr, int32_t N, int32_t k, const ShardPtrs& topk_ids,
                  const ShardPtrs& pair_rank, const ShardPtrs& count_bufs, int32_t n_count_bufs,
                  int32_t* chunk_counts, int64_t n_rows_bound, cudaStream_t st) {
-  if (N > kGateMaxN) return SMOE_ERR_UNSUPPORTED;
+  if (N > kMaxExperts) return SMOE_ERR_UNSUPPORTED;
   const int32_t max_chunks =
       (int32_t)ceil_div(std::max<int64_t>(n_rows_bound * k, 1), kRouteThreads);
   // grid-strided over a shard's chunks: enough CTAs for ~2 per SM in total
@@ -758,9 +758,9 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
                 int32_t whole_rows, ShardPtrs xfan, int64_t* stats) {
   pdl_enter();
   __shared__ RowMap rm;
-  __shared__ int32_t s_M[kGateMaxN];
-  __shared__ int32_t s_seg[kGateMaxN];
-  __shared__ int32_t s_off[SMOE_MAX_SHARDS * kGateMaxN];
+  __shared__ int32_t s_M[kMaxExperts];
+  __shared__ int32_t s_seg[kMaxExperts];
+  __shared__ int32_t s_off[SMOE_MAX_SHARDS * kMaxExperts];
   __shared__ char* s_hs[SMOE_MAX_SHARDS];
   __shared__ char* s_ids[SMOE_MAX_SHARDS];
   __shared__ char* s_rank[SMOE_MAX_SHARDS];
@@ -936,7 +936,7 @@ int launch_dispatch(const LocalRows& lr, int32_t N, int32_t k, int64_t d,
                     const ShardPtrs& pair_rank, const ShardPtrs& xin, const ShardPtrs& xmeta,
                     int64_t expert_rows, int64_t* problems, int32_t* err, int64_t n_rows_bound,
                     cudaStream_t st, const ShardPtrs& xfan, int64_t* stats) {
-  if (N > kGateMaxN || d % 8) return SMOE_ERR_UNSUPPORTED;
+  if (N > kMaxExperts || d % 8) return SMOE_ERR_UNSUPPORTED;
   SMOE_CUDA_TRY(launch_pdl(dispatch_kernel, grid_items(std::max<int64_t>(n_rows_bound, 1), d),
                            256, 0, st, lr, N, k, d, counts_mat, slot_owner, slot_first, hs,
                            topk_ids, pair_rank, xin, xmeta, expert_rows, problems, err,

@@ -28,6 +28,10 @@ CONFIGS = {
     "mixtral": dict(d=4096, N=8, k=2, f=14336, G=8, vocab=32000),
     "dsv2_lite": dict(d=2048, N=64, k=6, f=1408, G=8, vocab=102400),
     "qwen2_57b": dict(d=3584, N=64, k=8, f=2560, G=8, vocab=151936),
+    # DeepSeek-V2 (the paper's own model): 160 routed experts
+    # top-6, hidden 5120, expert ffn 1536 (public config; shared experts are
+    # not part of the routed path)
+    "deepseek_v2": dict(d=5120, N=160, k=6, f=1536, G=8, vocab=102400),
 }
 
 

@@ -26,7 +26,7 @@ TOL = 1e-2
 
 
 @pytest.mark.parametrize("name,ep", [("mixtral", 8), ("dsv2_lite", 8), ("qwen2_57b", 8),
-                                     ("qwen2_57b", 2)])
+                                     ("qwen2_57b", 2), ("deepseek_v2", 8)])
 def test_full_size_layer_properties(name, ep):
     n = 16384
     w = synth.make_workload(name, n=n, eps=0.2, seed=3, device=True, cfg_override={"G": ep})
