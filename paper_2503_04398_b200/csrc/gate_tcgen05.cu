@@ -55,7 +55,12 @@ template <int NP, int SUB, int ST> struct GtShape {
   static constexpr uint32_t kTmemCols =
       2 * NP <= 32 ? 32 : 2 * NP <= 64 ? 64 : 2 * NP <= 128 ? 128 : 2 * NP <= 256 ? 256 : 512;
   static constexpr uint32_t kAccCols = kTmemCols / 2;      // column stride of the 2 accumulators
-  static constexpr size_t kSmem = 1024 + ST * kStageBytes + 128;
+  // N' > 64: each epilogue thread stages its row's logits in shared memory
+  // (kWideRows rows at a time: 128, or 64 in two phases for N' > 192)
+  static constexpr int kWideRows = NP > 192 ? 64 : 128;
+  static constexpr int kWideLd = NP + 4;                   // floats per staged row (16 B pad)
+  static constexpr uint32_t kWideBytes = NP > 64 ? kWideRows * kWideLd * 4 : 0;
+  static constexpr size_t kSmem = 1024 + ST * kStageBytes + 128 + kWideBytes;
   // D f32, A/B bf16, both K-major, N = NP, M = 128
   static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) |
                                      (uint32_t(NP >> 3) << 17) | (uint32_t(kGtRows >> 4) << 24);
@@ -74,6 +79,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
   uint8_t* smem_w = smem + kGtStages * S::kHBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_w + kGtStages * S::kWBytes);
   // bars: full[kGtStages], empty[kGtStages], tfull[2], tempty[2]
+  float* wide = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 128);
   __shared__ uint32_t tmem_holder;
   __shared__ int32_t s_cnt[SMOE_MAX_SHARDS];
   __shared__ int32_t s_prefix[SMOE_MAX_SHARDS + 1];
@@ -290,69 +296,123 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
           if (e < N) ex += __expf(__uint_as_float(v[e]) + s_bias[e] - mx);
       } else {
         // N' > 64 (e.g. DeepSeek-V2, 160 experts): too many logits for one
-        // thread's registers -- each selection pass re-reads the row from
-        // TMEM 16 columns at a time (max-tree per chunk, the earlier chunk
-        // winning ties), then one more pass sums the softmax denominator;
-        // the accumulator is released after the last read
+        // thread's registers.  A two-level tournament: one pass over the row
+        // in 16-column TMEM chunks (warp-uniform loads) stages the biased
+        // logits in shared memory and keeps each chunk's winner (max-tree,
+        // the lower slot winning ties) plus an online softmax denominator;
+        // each selection takes the best chunk winner (the lower chunk on
+        // ties) and refills only that chunk -- from shared memory, since the
+        // winning chunk differs between the rows of a warp and a TMEM load
+        // address must not.  For N' > 192 the rows are staged 64 at a time.
         constexpr int NC = NP / 16;
+        constexpr int kGroups = 128 / S::kWideRows;          // 1, or 2 for N' > 192
+        constexpr int kWarpsPerGroup = 4 / kGroups;
+        float* myrow = wide + ((ew % kWarpsPerGroup) * 32 + lane) * S::kWideLd;
+        int32_t cwk[NC];
+        int cwi[NC];
         uint32_t tk[NC];
+        // max-tree over the keys of chunk c (x = staged logits, taken /
+        // invalid slots -> INT_MIN)
+        auto chunk_best = [&](int c, const float (&x)[16], uint32_t taken, int32_t& bk,
+                              int& bi) {
+          int32_t tv[8];
+          int ti[8];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) tk[c] = 0;
-#pragma unroll 1
-        for (int s = 0; s < kGtMaxK; ++s) {
-          sel_e[s] = 0;
-          sel_k[s] = INT_MIN;
-          if (s >= K) continue;
-          int32_t bk = INT_MIN;
-          int bi = 0;
+          for (int i = 0; i < 8; ++i) {
+            const int e0 = c * 16 + 2 * i, e1 = e0 + 1;
+            const int32_t k0 = (e0 < N && !((taken >> (2 * i)) & 1)) ? to_key(x[2 * i]) : INT_MIN;
+            const int32_t k1 = (e1 < N && !((taken >> (2 * i + 1)) & 1)) ? to_key(x[2 * i + 1])
+                                                                            : INT_MIN;
+            const bool r = k1 > k0;
+            tv[i] = r ? k1 : k0;
+            ti[i] = r ? e1 : e0;
+          }
 #pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            uint32_t v[16];
-            SMOE_TMEM_LD16(taddr + c * 16, v);
-            tmem_wait_ld();
-            int32_t tv[8];
-            int ti[8];
+          for (int w = 4; w >= 1; w >>= 1) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int e0 = c * 16 + 2 * i, e1 = e0 + 1;
-              const int32_t k0 = (e0 < N && !((tk[c] >> (2 * i)) & 1))
-                                     ? to_key(__uint_as_float(v[2 * i]) + s_bias[e0]) : INT_MIN;
-              const int32_t k1 = (e1 < N && !((tk[c] >> (2 * i + 1)) & 1))
-                                     ? to_key(__uint_as_float(v[2 * i + 1]) + s_bias[e1]) : INT_MIN;
-              const bool r = k1 > k0;
-              tv[i] = r ? k1 : k0;
-              ti[i] = r ? e1 : e0;
+            for (int i = 0; i < w; ++i) {
+              const bool r = tv[2 * i + 1] > tv[2 * i];
+              tv[i] = r ? tv[2 * i + 1] : tv[2 * i];
+              ti[i] = r ? ti[2 * i + 1] : ti[2 * i];
             }
+          }
+          bk = tv[0];
+          bi = ti[0];
+        };
+#pragma unroll 1
+        for (int grp = 0; grp < kGroups; ++grp) {
+          if (ew / kWarpsPerGroup == grp) {
+            float m = -INFINITY;
 #pragma unroll
-            for (int w = 4; w >= 1; w >>= 1) {
+            for (int c = 0; c < NC; ++c) {
+              uint32_t v[16];
+              SMOE_TMEM_LD16(taddr + c * 16, v);
+              tmem_wait_ld();
+              float x[16];
 #pragma unroll
-              for (int i = 0; i < w; ++i) {
-                const bool r = tv[2 * i + 1] > tv[2 * i];
-                tv[i] = r ? tv[2 * i + 1] : tv[2 * i];
-                ti[i] = r ? ti[2 * i + 1] : ti[2 * i];
+              for (int i = 0; i < 16; ++i) x[i] = __uint_as_float(v[i]) + s_bias[c * 16 + i];
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                *reinterpret_cast<float4*>(myrow + c * 16 + 4 * q) =
+                    make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+              tk[c] = 0;
+              chunk_best(c, x, 0u, cwk[c], cwi[c]);
+              float cm = -INFINITY;
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (c * 16 + i < N) cm = fmaxf(cm, x[i]);
+              const float mn = fmaxf(m, cm);
+              if (mn > -INFINITY) {
+                ex = (m > -INFINITY ? ex * __expf(m - mn) : 0.f);
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                  if (c * 16 + i < N) ex += __expf(x[i] - mn);
+                m = mn;
               }
             }
-            if (tv[0] > bk) { bk = tv[0]; bi = ti[0]; }
+            // every TMEM read of this warp is done: release its accumulator lanes
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+#pragma unroll
+            for (int s = 0; s < kGtMaxK; ++s) {
+              sel_e[s] = 0;
+              sel_k[s] = INT_MIN;
+              if (s < K) {
+                int32_t bk = cwk[0];
+                int bc = 0;
+#pragma unroll
+                for (int c = 1; c < NC; ++c)
+                  if (cwk[c] > bk) { bk = cwk[c]; bc = c; }
+                int bi = 0;
+                uint32_t taken = 0;
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+                  if (c == bc) { bi = cwi[c]; tk[c] |= 1u << (cwi[c] & 15); taken = tk[c]; }
+                sel_e[s] = bi;
+                sel_k[s] = bk;
+                if (s + 1 < K) {                   // refill the winning chunk (own row, smem)
+                  float x[16];
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    const float4 f = *reinterpret_cast<const float4*>(myrow + bc * 16 + 4 * q);
+                    x[4 * q] = f.x; x[4 * q + 1] = f.y; x[4 * q + 2] = f.z; x[4 * q + 3] = f.w;
+                  }
+                  int32_t nk;
+                  int ni;
+                  chunk_best(bc, x, taken, nk, ni);
+#pragma unroll
+                  for (int c = 0; c < NC; ++c)
+                    if (c == bc) { cwk[c] = nk; cwi[c] = ni; }
+                }
+              }
+            }
           }
-          sel_e[s] = bi;
-          sel_k[s] = bk;
-#pragma unroll
-          for (int c = 0; c < NC; ++c)
-            if (c == (bi >> 4)) tk[c] |= 1u << (bi & 15);
+          if constexpr (kGroups > 1) {
+            // the next group's warps reuse the staging rows
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+          }
         }
-        const float mx = key_to_f(sel_k[0]);
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          uint32_t v[16];
-          SMOE_TMEM_LD16(taddr + c * 16, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (c * 16 + i < N) ex += __expf(__uint_as_float(v[i]) + s_bias[c * 16 + i] - mx);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
         if (j >= s_cnt[gl]) continue;
@@ -444,7 +504,9 @@ static int launch_np(const CUtensorMap& mh, const CUtensorMap& mw, const GateTcA
                      int64_t n_rows_bound, cudaStream_t st) {
   // wide gates: one k-block per stage keeps 4 stages of H + W(N' x 64) in smem
   if constexpr (NP > 64) {
-    return launch_cfg<NP, 1, 4>(mh, mw, a, n_rows_bound, st);
+    // wide gates: one k-block per stage, and fewer stages to leave room for
+    // the staged logits (NP <= 160: 3 stages, else 2)
+    return launch_cfg<NP, 1, (NP <= 160 ? 3 : 2)>(mh, mw, a, n_rows_bound, st);
   } else {
     switch (ring_sub()) {
       case 1: return launch_cfg<NP, 1, 8>(mh, mw, a, n_rows_bound, st);

@@ -26,8 +26,12 @@ def main():
     ap.add_argument("--tokens", type=int, default=0, help="override every config's token count")
     args = ap.parse_args()
     knobs = {k: v for k, v in os.environ.items() if k.startswith("SMOE_")}
-    for name, n, ep in (("mixtral", 16384, None), ("dsv2_lite", 16384, None),
-                        ("dsv2_lite", 65536, None), ("qwen2_57b", 65536, 8)):
+    cfgs = (("mixtral", 16384, None), ("dsv2_lite", 16384, None),
+            ("dsv2_lite", 65536, None), ("qwen2_57b", 65536, 8), ("deepseek_v2", 16384, None))
+    only = os.environ.get("SMOE_PROBE_CFGS")          # comma list of config names
+    for name, n, ep in cfgs:
+        if (only and name not in only.split(",")) or (not only and name == "deepseek_v2"):
+            continue
         if args.tokens:
             if n == 65536 and name == "dsv2_lite":
                 continue
