@@ -478,9 +478,13 @@ def main():
         torch.cuda.synchronize()
         layer.check_errors()
         us = d0.elapsed_time(d1) / reps * 1e3
-        w_bytes = 2.0 * 3 * cfg["N"] * d * f          # every expert's weights, bf16
+        # the experts this batch activates stream their weights once (bf16)
+        active = int((np.asarray(layer.stats(nd)["pair_counts"]).sum(0) > 0).sum())
+        w_bytes = 2.0 * 3 * active * d * f
         decode = {"tokens": nd, "us_per_step": us, "tokens_per_s": nd / (us / 1e6),
+                  "active_experts": active,
                   "weight_stream_roofline_us": w_bytes / (pk["hbm"] * 1e3),
+                  "roofline_frac": w_bytes / (pk["hbm"] * 1e3) / us,
                   "mode": "CUDA-graph replay of the whole layer (SpecMoELayer.capture)"}
         del g
 
