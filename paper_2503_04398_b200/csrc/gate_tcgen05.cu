@@ -46,9 +46,16 @@ constexpr int kGtMaxK = 8;
 // NP = W rows (N rounded up to 16); SUB = 64-wide k-blocks per stage (one TMA
 // box each, so a stage reads SUB * 128 contiguous bytes of every hidden row);
 // ST = stages in the ring.
-template <int NP, int SUB, int ST> struct GtShape {
+// HALF: 64-row tiles (two CTAs per SM) for batches whose 128-row tiles would
+// leave SMs idle.  The MMA stays M = 128: rows 64..127 of its A operand are
+// the next 8 KiB of shared memory (the next box, or the W region), computed
+// and never read back -- a TMEM lane (= row) only depends on its own A row,
+// so every real row's logits are bit-identical to the 128-row kernel's.
+template <int NP, int SUB, int ST, int HALF = 0> struct GtShape {
   static constexpr int kStages = ST;
-  static constexpr uint32_t kHBytes = SUB * kGtBoxBytes;
+  static constexpr int kRows = HALF ? 64 : kGtRows;        // real rows per tile
+  static constexpr uint32_t kBox = kRows * kGemmBK * 2;    // one H box (TMA)
+  static constexpr uint32_t kHBytes = SUB * kBox;
   static constexpr uint32_t kWBox = NP * kGemmBK * 2;     // NP rows of 128 B
   static constexpr uint32_t kWBytes = SUB * kWBox;
   static constexpr uint32_t kStageBytes = kHBytes + kWBytes;
@@ -66,11 +73,12 @@ template <int NP, int SUB, int ST> struct GtShape {
                                      (uint32_t(NP >> 3) << 17) | (uint32_t(kGtRows >> 4) << 24);
 };
 
-template <int NP, int SUB, int ST>
-__global__ void __launch_bounds__(kGtThreads, 1)
+template <int NP, int SUB, int ST, int HALF>
+__global__ void __launch_bounds__(HALF ? kGtThreads - 64 : kGtThreads, HALF ? 2 : 1)
 gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
                const __grid_constant__ CUtensorMap tmap_w, const GateTcArgs a) {
-  using S = GtShape<NP, SUB, ST>;
+  using S = GtShape<NP, SUB, ST, HALF>;
+  static_assert(!HALF || NP <= 64, "64-row tiles: register-resident logits only");
   constexpr int kGtStages = S::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -102,7 +110,9 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_addr(&bars[2 * kGtStages + b]), 1);
-      mbar_init(smem_addr(&bars[2 * kGtStages + 2 + b]), 4);   // one arrival per epilogue warp
+      // one arrival per epilogue warp (64-row tiles: warps 4 and 5 only, the
+      // warps whose TMEM lane quarters hold rows 0..63)
+      mbar_init(smem_addr(&bars[2 * kGtStages + 2 + b]), HALF ? 2 : 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -125,7 +135,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
     int32_t c = 0;
     if (i < a.shard_count)
       c = a.counts ? a.counts[a.shard_begin + i] : (i == 0 ? (int32_t)a.single_rows : 0);
-    const int32_t tiles = (c + kGtRows - 1) / kGtRows;
+    const int32_t tiles = (c + S::kRows - 1) / S::kRows;
     int32_t incl = tiles;                  // inclusive prefix of the tile counts
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -169,14 +179,14 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
       for (int32_t t = blockIdx.x; t < total; t += gridDim.x) {
         int32_t gl, blk;
         decode(t, gl, blk);
-        const int32_t row = (int32_t)(gl * a.rows_per_shard + (int64_t)blk * kGtRows);
+        const int32_t row = (int32_t)(gl * a.rows_per_shard + (int64_t)blk * S::kRows);
         for (int32_t kb = 0; kb < a.num_k_blocks; kb += SUB) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
           mbar_expect_tx(fb, S::kStageBytes);
 #pragma unroll
           for (int u = 0; u < SUB; ++u) {
-            tma_load_2d(smem_addr(smem_h + stage * S::kHBytes + u * kGtBoxBytes), &tmap_h, fb,
+            tma_load_2d(smem_addr(smem_h + stage * S::kHBytes + u * S::kBox), &tmap_h, fb,
                         (kb + u) * kGemmBK, row);
             tma_load_2d(smem_addr(smem_w + stage * S::kWBytes + u * S::kWBox), &tmap_w, fb,
                         (kb + u) * kGemmBK, 0);
@@ -199,7 +209,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
           tc_fence_after();
 #pragma unroll
           for (int u = 0; u < SUB; ++u) {
-            const uint64_t hd = sdesc(smem_addr(smem_h + stage * S::kHBytes + u * kGtBoxBytes));
+            const uint64_t hd = sdesc(smem_addr(smem_h + stage * S::kHBytes + u * S::kBox));
             const uint64_t wd = sdesc(smem_addr(smem_w + stage * S::kWBytes + u * S::kWBox));
 #pragma unroll
             for (int k = 0; k < kGemmBK / 16; ++k)
@@ -225,7 +235,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * S::kAccCols + ((uint32_t)(ew * 32) << 16);
-      const int64_t j = (int64_t)blk * kGtRows + ew * 32 + lane;
+      const int64_t j = (int64_t)blk * S::kRows + ew * 32 + lane;
       // order-preserving int keys (+0 and -0 merged, -inf an ordinary
       // candidate); INT_MIN marks "not a candidate" (slots >= N, slots
       // already taken), so fewer than k finite logits still give k distinct
@@ -471,19 +481,23 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
   }
 }
 
-template <int NP, int SUB, int ST>
+template <int NP, int SUB, int ST, int HALF = 0>
 static int launch_cfg(const CUtensorMap& mh, const CUtensorMap& mw, const GateTcArgs& a,
                       int64_t n_rows_bound, cudaStream_t st) {
-  using S = GtShape<NP, SUB, ST>;
+  using S = GtShape<NP, SUB, ST, HALF>;
+  static_assert(!HALF || 2 * (S::kSmem + 2048) <= 228 * 1024, "two CTAs per SM");
   static bool attr = false;
   if (!attr) {
-    SMOE_CUDA_TRY(cudaFuncSetAttribute(gate_tc_kernel<NP, SUB, ST>,
+    SMOE_CUDA_TRY(cudaFuncSetAttribute(gate_tc_kernel<NP, SUB, ST, HALF>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::kSmem));
     attr = true;
   }
-  const int64_t tiles = ceil_div(n_rows_bound, kGtRows) + a.shard_count;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms()));
-  SMOE_CUDA_TRY(launch_pdl(gate_tc_kernel<NP, SUB, ST>, grid, kGtThreads, S::kSmem, st, mh, mw, a));
+  const int64_t tiles = ceil_div(n_rows_bound, S::kRows) + a.shard_count;
+  const int grid =
+      (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (HALF ? 2 : 1) * num_sms()));
+  SMOE_CUDA_TRY(launch_pdl(gate_tc_kernel<NP, SUB, ST, HALF>, grid,
+                           HALF ? kGtThreads - 64 : kGtThreads, S::kSmem, st,
+                           mh, mw, a));
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }
@@ -499,9 +513,24 @@ static int ring_sub() {
   return sub;
 }
 
+// 64-row tiles while the 128-row tiles would not fill ~1.25 waves of SMs
+// (SMOE_GATE_HALF = 0 / 1 forces them off / on, tuning only)
+static bool use_half(int64_t n_rows_bound) {
+  static int mode = [] {
+    const char* e = getenv("SMOE_GATE_HALF");
+    return e ? atoi(e) : -1;
+  }();
+  if (mode >= 0) return mode == 1;
+  return 4 * ceil_div(n_rows_bound, kGtRows) <= 5 * (int64_t)num_sms();
+}
+
 template <int NP>
-static int launch_np(const CUtensorMap& mh, const CUtensorMap& mw, const GateTcArgs& a,
-                     int64_t n_rows_bound, cudaStream_t st) {
+static int launch_np(const CUtensorMap& mh, const CUtensorMap* mh64, const CUtensorMap& mw,
+                     const GateTcArgs& a, int64_t n_rows_bound, cudaStream_t st) {
+  if constexpr (NP <= 64) {
+    if (mh64 && use_half(n_rows_bound))
+      return launch_cfg<NP, 2, (NP <= 32 ? 4 : 3), 1>(*mh64, mw, a, n_rows_bound, st);
+  }
   // wide gates: one k-block per stage keeps 4 stages of H + W(N' x 64) in smem
   if constexpr (NP > 64) {
     // wide gates: one k-block per stage, and fewer stages to leave room for
@@ -532,18 +561,19 @@ bool gate_tc_supported(int32_t n_experts, int32_t top_k, int64_t d) {
          top_k <= n_experts && d % (4 * kGemmBK) == 0;
 }
 
-int launch_gate_tc(const CUtensorMap& map_h, const CUtensorMap& map_w, const GateTcArgs& a,
-                   int64_t n_rows_bound, cudaStream_t st) {
+int launch_gate_tc(const CUtensorMap& map_h, const CUtensorMap* map_h64,
+                   const CUtensorMap& map_w, const GateTcArgs& a, int64_t n_rows_bound,
+                   cudaStream_t st) {
   if (n_rows_bound <= 0) return SMOE_OK;
   switch (gate_tc_rows(a.n_experts)) {
-    case 16: return launch_np<16>(map_h, map_w, a, n_rows_bound, st);
-    case 32: return launch_np<32>(map_h, map_w, a, n_rows_bound, st);
-    case 48: return launch_np<48>(map_h, map_w, a, n_rows_bound, st);
-    case 64: return launch_np<64>(map_h, map_w, a, n_rows_bound, st);
-    case 128: return launch_np<128>(map_h, map_w, a, n_rows_bound, st);
-    case 160: return launch_np<160>(map_h, map_w, a, n_rows_bound, st);
-    case 192: return launch_np<192>(map_h, map_w, a, n_rows_bound, st);
-    case 256: return launch_np<256>(map_h, map_w, a, n_rows_bound, st);
+    case 16: return launch_np<16>(map_h, map_h64, map_w, a, n_rows_bound, st);
+    case 32: return launch_np<32>(map_h, map_h64, map_w, a, n_rows_bound, st);
+    case 48: return launch_np<48>(map_h, map_h64, map_w, a, n_rows_bound, st);
+    case 64: return launch_np<64>(map_h, map_h64, map_w, a, n_rows_bound, st);
+    case 128: return launch_np<128>(map_h, map_h64, map_w, a, n_rows_bound, st);
+    case 160: return launch_np<160>(map_h, map_h64, map_w, a, n_rows_bound, st);
+    case 192: return launch_np<192>(map_h, map_h64, map_w, a, n_rows_bound, st);
+    case 256: return launch_np<256>(map_h, map_h64, map_w, a, n_rows_bound, st);
     default: return SMOE_ERR_UNSUPPORTED;
   }
 }

@@ -24,6 +24,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--stages", default="gate")
     ap.add_argument("--tokens", type=int, default=0, help="override every config's token count")
+    ap.add_argument("--flush", action="store_true",
+                    help="write 512 MiB before every timed call (cold L2) and time each call")
     args = ap.parse_args()
     knobs = {k: v for k, v in os.environ.items() if k.startswith("SMOE_")}
     cfgs = (("mixtral", 16384, None), ("dsv2_lite", 16384, None),
@@ -51,15 +53,29 @@ def main():
             for _ in range(3):
                 layer.run_device(tok, stages=[j])
             reps = 50
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            e0.record()
-            for _ in range(reps):
-                layer.run_device(tok, stages=[j])
-            e1.record()
-            torch.cuda.synchronize()
-            us = e0.elapsed_time(e1) / reps * 1e3
+            if args.flush:
+                junk = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+                evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                       for _ in range(reps)]
+                for a, b in evs:
+                    junk.fill_(1)
+                    a.record()
+                    layer.run_device(tok, stages=[j])
+                    b.record()
+                torch.cuda.synchronize()
+                us = sum(a.elapsed_time(b) for a, b in evs) / reps * 1e3
+                del junk
+            else:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record()
+                for _ in range(reps):
+                    layer.run_device(tok, stages=[j])
+                e1.record()
+                torch.cuda.synchronize()
+                us = e0.elapsed_time(e1) / reps * 1e3
             print(json.dumps({"config": name, "tokens": n, "stage": st, "us": us,
+                              "cold_l2": bool(args.flush),
                               "hidden_row_gbs": n * d * 2 / us / 1e3} | knobs), flush=True)
         del layer
         torch.cuda.empty_cache()
