@@ -49,6 +49,9 @@ def __getattr__(name):
     if name == "DSMoELayer":
         from .baseline import DSMoELayer
         return DSMoELayer
+    if name == "DSMoEPipelineLayer":
+        from .baseline import DSMoEPipelineLayer
+        return DSMoEPipelineLayer
     if name in _OFFLINE:
         raise AttributeError(f"moesched.{name} is part of the offline toolkit (profiling / "
                              "solver search / CLI), out of scope for the B200 online path "

@@ -37,13 +37,18 @@ def _stale(obj: Path, src: Path) -> bool:
     return any(d.stat().st_mtime > obj.stat().st_mtime for d in deps)
 
 
-def build(verbose: bool = False, ptxas_info: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build(verbose: bool = False, ptxas_info: bool = False, variant: str = "",
+          defines: tuple[str, ...] = ()) -> Path:
+    """variant: an A/B or instrumented build (`-D` defines) into
+    _build/<variant>/ and libsmoe_<variant>.so, loaded with SMOE_LIB=<path>."""
+    bdir = BUILD / variant if variant else BUILD
+    lib = PKG / f"libsmoe_{variant}.so" if variant else LIB
+    bdir.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
-    extra = ["-Xptxas", "-v"] if ptxas_info else []
+    extra = (["-Xptxas", "-v"] if ptxas_info else []) + [f"-D{d}" for d in defines]
 
     def compile_one(src: Path) -> Path:
-        obj = BUILD / (src.stem + ".o")
+        obj = bdir / (src.stem + ".o")
         if _stale(obj, src) or ptxas_info:
             cmd = [nvcc, *ARCH, *FLAGS, *extra, "-c", str(src), "-o", str(obj)]
             if verbose:
@@ -57,13 +62,17 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> Path:
 
     with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         objs = list(ex.map(compile_one, sources()))
-    if not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs)]
+    if not lib.exists() or any(o.stat().st_mtime > lib.stat().st_mtime for o in objs):
+        cmd = [nvcc, *ARCH, "-shared", "-o", str(lib), *map(str, objs)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, ptxas_info="--ptxas" in sys.argv))
+    # python -m paper_2503_04398_b200.build [-v] [--ptxas] [--variant NAME -DFOO ...]
+    av = sys.argv[1:]
+    var = av[av.index("--variant") + 1] if "--variant" in av else ""
+    defs = tuple(a[2:] for a in av if a.startswith("-D"))
+    print(build(verbose="-v" in av, ptxas_info="--ptxas" in av, variant=var, defines=defs))

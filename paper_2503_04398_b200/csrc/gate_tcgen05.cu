@@ -38,6 +38,22 @@
 
 namespace smoe {
 
+// Timeline probe (build variant -DSMOE_GATE_PROBE only, tools/probe/gate_timeline.py):
+// %globaltimer per CTA at fixed points of its first tile.
+#ifdef SMOE_GATE_PROBE
+__device__ unsigned long long g_gate_ts[2048][8];
+#define GATE_TS(i)                                                                   \
+  do {                                                                               \
+    unsigned long long t_;                                                           \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+    if (blockIdx.x < 2048) g_gate_ts[blockIdx.x][i] = t_;                            \
+  } while (0)
+#else
+#define GATE_TS(i) \
+  do {             \
+  } while (0)
+#endif
+
 constexpr int kGtThreads = 256;
 constexpr int kGtRows = 128;                               // MMA M: rows per tile
 constexpr uint32_t kGtBoxBytes = kGtRows * kGemmBK * 2;   // one 128 x 64 H box: 16 KiB
@@ -97,6 +113,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
   __shared__ int32_t s_owner[NP];        // cluster of each expert slot (locality count)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) GATE_TS(0);
   if (threadIdx.x < NP) {
     s_bias[threadIdx.x] = (a.b_gate && threadIdx.x < a.n_experts) ? a.b_gate[threadIdx.x] : 0.f;
     // staged once: the epilogue's k owner lookups per row would otherwise be
@@ -160,6 +177,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
   tc_fence_after();
   const uint32_t tmem_base = tmem_holder;
   const int32_t total = s_prefix[a.shard_count];
+  if (threadIdx.x == 0) GATE_TS(1);
   const uint32_t full0 = smem_addr(&bars[0]);
   const uint32_t empty0 = smem_addr(&bars[kGtStages]);
   const uint32_t tfull0 = smem_addr(&bars[2 * kGtStages]);
@@ -193,6 +211,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
           }
           if (++stage == kGtStages) { stage = 0; phase ^= 1; }
         }
+        if (t == (int32_t)blockIdx.x) GATE_TS(2);         // last TMA of the first tile issued
       }
     }
   } else if (warp == 1) {
@@ -207,6 +226,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
         for (int32_t kb = 0; kb < a.num_k_blocks; kb += SUB) {
           mbar_wait(full0 + 8 * stage, phase);
           tc_fence_after();
+          if (kb == 0 && t == (int32_t)blockIdx.x) GATE_TS(3);   // first stage landed
 #pragma unroll
           for (int u = 0; u < SUB; ++u) {
             const uint64_t hd = sdesc(smem_addr(smem_h + stage * S::kHBytes + u * S::kBox));
@@ -219,6 +239,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
           if (++stage == kGtStages) { stage = 0; phase ^= 1; }
         }
         tc_commit(tfull0 + 8 * acc);
+        if (t == (int32_t)blockIdx.x) GATE_TS(4);         // last MMA of the first tile issued
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -234,6 +255,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
       decode(t, gl, blk);
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
+      if (ew == 0 && lane == 0 && t == (int32_t)blockIdx.x) GATE_TS(5);   // accumulator ready
       const uint32_t taddr = tmem_base + acc * S::kAccCols + ((uint32_t)(ew * 32) << 16);
       const int64_t j = (int64_t)blk * S::kRows + ew * 32 + lane;
       // order-preserving int keys (+0 and -0 merged, -inf an ordinary
@@ -459,6 +481,8 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
         }
       }
     }
+    __syncwarp();
+    if (ew == 0 && lane == 0) GATE_TS(6);                 // epilogue warp 4 done
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       my_local += __shfl_xor_sync(0xffffffffu, my_local, o);
@@ -474,6 +498,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) GATE_TS(7);
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
@@ -579,3 +604,17 @@ int launch_gate_tc(const CUtensorMap& map_h, const CUtensorMap* map_h64,
 }
 
 }  // namespace smoe
+
+#ifdef SMOE_GATE_PROBE
+extern "C" int smoe_probe_gate_ts(unsigned long long* host, int rows) {
+  if (rows > 2048) rows = 2048;
+  return cudaMemcpyFromSymbol(host, smoe::g_gate_ts, sizeof(unsigned long long) * 8 * rows) ==
+                 cudaSuccess
+             ? 0
+             : -1;
+}
+extern "C" int smoe_probe_gate_reset() {
+  static unsigned long long zero[2048 * 8];
+  return cudaMemcpyToSymbol(smoe::g_gate_ts, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -7,9 +7,10 @@ size-independent properties, since the CPU oracle would take minutes here:
   the looked-up devices equal the reference lookup (oracle, numpy) bit-exactly;
 * routing: the ordered top-k experts equal the planted choice (synth builds
   margin-guarded logits), local + remote = n*k, local = #{label(expert) = device};
-* output: a sample of tokens against a torch fp32 restatement of the layer
-  (SRS sum in shard order -> bf16, fp32 gate softmax, fp32 SwiGLU on the bf16
-  weights, renormalised top-k combine); relative Frobenius error <= 1e-2;
+* output: every token against a torch fp32 restatement of the layer (SRS
+  sum in shard order -> bf16, fp32 gate softmax, fp32 SwiGLU on the bf16
+  weights, renormalised top-k combine); relative Frobenius error <= 1e-2,
+  every row <= 2e-2 (row norm), every element <= 2e-2 of its row's peak;
 * next-layer history: shifted window + cluster of the top-1 expert.
 """
 
@@ -70,9 +71,9 @@ def test_full_size_layer_properties(name, ep):
     assert np.array_equal(hn[:, -1], labels[w.chosen[:, 0]])
     assert np.array_equal(hn[:, :-1], w.hist[:, 1:])
 
-    # ---- output vs a torch fp32 restatement on a token sample
-    rng = np.random.default_rng(0)
-    sample = torch.as_tensor(np.sort(rng.choice(n, 256, replace=False)), device="cuda")
+    # ---- output vs a torch fp32 restatement on EVERY token (the fp32
+    # reference of the whole batch is a few TFLOP: well under a second here)
+    sample = torch.arange(n, device="cuda")
     P = w.partials[:, sample].float()                      # [G, s, d]
     h = P[0].clone()
     for g in range(1, G):

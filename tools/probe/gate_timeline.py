@@ -1,6 +1,15 @@
-"""Per-CTA timeline of the tcgen05 gate at decode sizes (needs the
-instrumented probe build libsmoe_gateprobe.so via SMOE_LIB)."""
+"""Per-CTA timeline of the tcgen05 gate (instrumented build):
+
+    python -m paper_2503_04398_b200.build --variant gateprobe -DSMOE_GATE_PROBE
+    SMOE_LIB=$PWD/paper_2503_04398_b200/libsmoe_gateprobe.so python tools/probe/gate_timeline.py dsv2_lite 16384
+
+Points (per CTA, first tile, %globaltimer ns): 0 entry, 1 set-up done (TMEM,
+barriers, counts), 2 last TMA of the tile issued, 3 first stage landed, 4 last
+MMA issued, 5 accumulator ready in the epilogue, 6 epilogue warp done, 7 exit.
+Prints the median / max over CTAs of each point relative to the earliest entry.
+"""
 import ctypes as C
+import json
 import sys
 import numpy as np
 import torch
@@ -14,19 +23,25 @@ tok = torch.as_tensor(w.tokens, device="cuda"); hist = torch.as_tensor(w.hist, d
 for _ in range(3):
     layer.run_device(tok, hist)
 torch.cuda.synchronize()
+h = N.lib()
 j = N.STAGE_NAMES.index("gate")
-layer.run_device(tok, hist, stages=[0, 1])
-torch.cuda.synchronize()
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record(); layer.run_device(tok, hist, stages=[j]); e1.record(); torch.cuda.synchronize()
-h = N.load()
-buf = (C.c_ulonglong * (512 * 8))()
-fn = getattr(h, "smoe_probe_gate_ts"); fn.restype = C.c_int
-assert fn(buf, 512) == 0
-ts = np.frombuffer(buf, dtype=np.uint64).reshape(512, 8).astype(np.int64)
-act = ts[(ts[:, 4] > 0) & (ts[:, 0] > 0)]
-base = ts[ts[:, 0] > 0, 0].min()
-print(f"{name} n={n}: event {e0.elapsed_time(e1)*1e3:.1f} us, CTAs with a tile {len(act)}")
-for r in act[:4]:
-    print("  start+%.1f setup %.1f  producer_done %.1f  mma_done %.1f  tfull_seen %.1f  epi_done %.1f  exit %.1f (us from CTA start)"
-          % ((r[0]-base)/1e3, (r[1]-r[0])/1e3, (r[2]-r[0])/1e3, (r[3]-r[0])/1e3, (r[4]-r[0])/1e3, (r[5]-r[0])/1e3, (r[6]-r[0])/1e3))
+junk = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+out = []
+for rep in range(3):
+    layer.run_device(tok, hist, stages=[0, 1])
+    junk.fill_(rep)                                   # cold L2, like the layer after the SRS
+    torch.cuda.synchronize()
+    assert h.smoe_probe_gate_reset() == 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); layer.run_device(tok, hist, stages=[j]); e1.record(); torch.cuda.synchronize()
+    buf = (C.c_ulonglong * (2048 * 8))()
+    assert h.smoe_probe_gate_ts(buf, 2048) == 0
+    ts = np.frombuffer(buf, dtype=np.uint64).reshape(2048, 8).astype(np.int64)
+    act = ts[(ts[:, 0] > 0) & (ts[:, 5] > 0)]
+    base = ts[ts[:, 0] > 0, 0].min()
+    rel = (act - base) / 1e3
+    out.append({"config": name, "tokens": n, "event_us": e0.elapsed_time(e1) * 1e3,
+                "ctas_with_tile": int(len(act)),
+                "median_us": [round(float(x), 2) for x in np.median(rel, axis=0)],
+                "max_us": [round(float(x), 2) for x in rel.max(axis=0)]})
+    print(json.dumps(out[-1]), flush=True)
