@@ -54,6 +54,13 @@ __device__ unsigned long long g_gate_ts[2048][8];
   } while (0)
 #endif
 
+#ifndef SMOE_GATE_SPLIT
+#define SMOE_GATE_SPLIT 1         // two epilogue threads per row at N' = 64 (0: one)
+#endif
+#ifndef SMOE_GATE_REG_MAX_NP
+#define SMOE_GATE_REG_MAX_NP 64   // 32 (tournament for 48 / 64) measured: profiles/r2/gate/
+#endif
+
 constexpr int kGtThreads = 256;
 constexpr int kGtRows = 128;                               // MMA M: rows per tile
 constexpr uint32_t kGtBoxBytes = kGtRows * kGemmBK * 2;   // one 128 x 64 H box: 16 KiB
@@ -62,14 +69,24 @@ constexpr int kGtMaxK = 8;
 // NP = W rows (N rounded up to 16); SUB = 64-wide k-blocks per stage (one TMA
 // box each, so a stage reads SUB * 128 contiguous bytes of every hidden row);
 // ST = stages in the ring.
-// HALF: 64-row tiles (two CTAs per SM) for batches whose 128-row tiles would
-// leave SMs idle.  The MMA stays M = 128: rows 64..127 of its A operand are
-// the next 8 KiB of shared memory (the next box, or the W region), computed
-// and never read back -- a TMEM lane (= row) only depends on its own A row,
-// so every real row's logits are bit-identical to the 128-row kernel's.
-template <int NP, int SUB, int ST, int HALF = 0> struct GtShape {
+// Epilogue kind by N': up to kGtRegMaxNP every logit of a row lives in one
+// thread's registers and each of the k selections is a max-tree over all of
+// them; above it the row's logits are staged in shared memory and the
+// selection is a two-level tournament over 16-column chunks.
+constexpr int kGtRegMaxNP = SMOE_GATE_REG_MAX_NP;
+
+template <int NP, int SUB, int ST> struct GtShape {
   static constexpr int kStages = ST;
-  static constexpr int kRows = HALF ? 64 : kGtRows;        // real rows per tile
+  static constexpr bool kWide = NP > kGtRegMaxNP;
+  // register path at N' = 64: two epilogue threads per row (warps 4..11, the
+  // second four reading the upper 32 columns of the same TMEM lane quarters)
+  // halve each thread's selection chain and give every SMSP two warps
+  static constexpr int kSplit = (SMOE_GATE_SPLIT && !kWide && NP == 64) ? 2 : 1;
+  static constexpr int kThreads = 128 + 128 * kSplit;
+  static constexpr int kHalf = NP / kSplit;                // columns per epilogue thread
+  static constexpr uint32_t kXchBytes = kSplit > 1 ? 128 * 80 : 0;   // per row: 8 keys,
+                                                                      // 8 slots, max, sum
+  static constexpr int kRows = kGtRows;
   static constexpr uint32_t kBox = kRows * kGemmBK * 2;    // one H box (TMA)
   static constexpr uint32_t kHBytes = SUB * kBox;
   static constexpr uint32_t kWBox = NP * kGemmBK * 2;     // NP rows of 128 B
@@ -78,23 +95,22 @@ template <int NP, int SUB, int ST, int HALF = 0> struct GtShape {
   static constexpr uint32_t kTmemCols =
       2 * NP <= 32 ? 32 : 2 * NP <= 64 ? 64 : 2 * NP <= 128 ? 128 : 2 * NP <= 256 ? 256 : 512;
   static constexpr uint32_t kAccCols = kTmemCols / 2;      // column stride of the 2 accumulators
-  // N' > 64: each epilogue thread stages its row's logits in shared memory
+  // wide: each epilogue thread stages its row's logits in shared memory
   // (kWideRows rows at a time: 128, or 64 in two phases for N' > 192)
   static constexpr int kWideRows = NP > 192 ? 64 : 128;
   static constexpr int kWideLd = NP + 4;                   // floats per staged row (16 B pad)
-  static constexpr uint32_t kWideBytes = NP > 64 ? kWideRows * kWideLd * 4 : 0;
-  static constexpr size_t kSmem = 1024 + ST * kStageBytes + 128 + kWideBytes;
+  static constexpr uint32_t kWideBytes = kWide ? kWideRows * kWideLd * 4 : 0;
+  static constexpr size_t kSmem = 1024 + ST * kStageBytes + 128 + kWideBytes + kXchBytes;
   // D f32, A/B bf16, both K-major, N = NP, M = 128
   static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) |
                                      (uint32_t(NP >> 3) << 17) | (uint32_t(kGtRows >> 4) << 24);
 };
 
-template <int NP, int SUB, int ST, int HALF>
-__global__ void __launch_bounds__(HALF ? kGtThreads - 64 : kGtThreads, HALF ? 2 : 1)
+template <int NP, int SUB, int ST>
+__global__ void __launch_bounds__(GtShape<NP, SUB, ST>::kThreads, 1)
 gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
                const __grid_constant__ CUtensorMap tmap_w, const GateTcArgs a) {
-  using S = GtShape<NP, SUB, ST, HALF>;
-  static_assert(!HALF || NP <= 64, "64-row tiles: register-resident logits only");
+  using S = GtShape<NP, SUB, ST>;
   constexpr int kGtStages = S::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -104,6 +120,8 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_w + kGtStages * S::kWBytes);
   // bars: full[kGtStages], empty[kGtStages], tfull[2], tempty[2]
   float* wide = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 128);
+  // split epilogue exchange: row r at xch + r * 20 words
+  int32_t* xch = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(wide) + S::kWideBytes);
   __shared__ uint32_t tmem_holder;
   __shared__ int32_t s_cnt[SMOE_MAX_SHARDS];
   __shared__ int32_t s_prefix[SMOE_MAX_SHARDS + 1];
@@ -127,9 +145,8 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_addr(&bars[2 * kGtStages + b]), 1);
-      // one arrival per epilogue warp (64-row tiles: warps 4 and 5 only, the
-      // warps whose TMEM lane quarters hold rows 0..63)
-      mbar_init(smem_addr(&bars[2 * kGtStages + 2 + b]), HALF ? 2 : 4);
+      // one arrival per epilogue warp
+      mbar_init(smem_addr(&bars[2 * kGtStages + 2 + b]), 4 * S::kSplit);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -245,8 +262,9 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
       }
     }
   } else if (warp >= 4) {
-    // ===== epilogue: thread = row =====
-    const int ew = warp - 4;
+    // ===== epilogue: thread = row (kSplit threads per row at N' = 64) =====
+    const int ew = (warp - 4) & 3;                 // TMEM lane quarter
+    const int hf = (warp - 4) >> 2;                // column half (split epilogue)
     const int N = a.n_experts, K = a.k;
     uint32_t acc = 0, acc_phase = 0;
     unsigned long long my_local = 0, my_remote = 0, my_rrows = 0;
@@ -270,25 +288,28 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
       int sel_e[kGtMaxK];
       int32_t sel_k[kGtMaxK];
       float ex = 0.f;
-      if constexpr (NP <= 64) {
+      if constexpr (!S::kWide) {
         // every logit of the row in registers; the accumulator is released
         // before the selection so the MMAs of tile t + 2 can start
-        uint32_t v[NP];
+        constexpr int NH = S::kHalf;             // columns of this thread
+        const int c0 = hf * NH;                  // first slot of this thread's columns
+        uint32_t v[NH];
 #pragma unroll
-        for (int c = 0; c < NP / 16; ++c) SMOE_TMEM_LD16(taddr + c * 16, (v + c * 16));
+        for (int c = 0; c < NH / 16; ++c) SMOE_TMEM_LD16(taddr + c0 + c * 16, (v + c * 16));
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty0 + 8 * acc);     // accumulator free for tile t + 2
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
-        if (j >= s_cnt[gl]) continue;
-        constexpr int NT = NP <= 16 ? 16 : (NP <= 32 ? 32 : 64);   // tree leaves (power of 2)
+        if (S::kSplit == 1 && j >= s_cnt[gl]) continue;
+        constexpr int NT = NH <= 16 ? 16 : (NH <= 32 ? 32 : 64);   // tree leaves (power of 2)
         int32_t key[NT];
 #pragma unroll
         for (int e = 0; e < NT; ++e)
-          key[e] = e < N ? to_key(__uint_as_float(v[e < NP ? e : 0]) + s_bias[e < NP ? e : 0])
-                         : INT_MIN;
+          key[e] = (e < NH && c0 + e < N)
+                       ? to_key(__uint_as_float(v[e < NH ? e : 0]) + s_bias[c0 + (e < NH ? e : 0)])
+                       : INT_MIN;
         uint64_t taken = 0;      // a bit mask, not stores into key[]: a store at the
                                  // winner's index became local memory (STL)
 #pragma unroll
@@ -317,18 +338,81 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
                 ti[i] = r ? ti[2 * i + 1] : ti[2 * i];
               }
             }
-            sel_e[s] = ti[0];
+            sel_e[s] = c0 + ti[0];
             sel_k[s] = tv[0];
             taken |= 1ull << ti[0];
           }
         }
-        const float mx = key_to_f(sel_k[0]);
+        if constexpr (S::kSplit == 1) {
+          const float mx = key_to_f(sel_k[0]);
 #pragma unroll
-        for (int e = 0; e < NP; ++e)
-          if (e < N) ex += __expf(__uint_as_float(v[e]) + s_bias[e] - mx);
+          for (int e = 0; e < NP; ++e)
+            if (e < N) ex += __expf(__uint_as_float(v[e]) + s_bias[e] - mx);
+        } else {
+          // this half's softmax sum relative to its own max, then the upper
+          // half hands (top-k, max, sum) to the lower one through shared
+          // memory; the lower half merges the two sorted lists (its own
+          // entries -- the lower slots -- first on equal keys) and rescales
+          // the two sums to the row's max, in a fixed order
+          const float mh = key_to_f(sel_k[0]);
+          float sh = 0.f;                      // 0 when this half has no finite logit
+          if (mh > -INFINITY) {
+#pragma unroll
+            for (int e = 0; e < NH; ++e)
+              if (c0 + e < N) sh += __expf(__uint_as_float(v[e]) + s_bias[c0 + e] - mh);
+          }
+          int32_t* xr = xch + (ew * 32 + lane) * 20;
+          if (hf == 1) {
+#pragma unroll
+            for (int s = 0; s < kGtMaxK; ++s) {
+              xr[s] = sel_k[s];
+              xr[8 + s] = sel_e[s];
+            }
+            xr[16] = __float_as_int(mh);
+            xr[17] = __float_as_int(sh);
+          }
+          // the two warps of this lane quarter (barrier ids 1..4; 0 is
+          // __syncthreads); both barriers are warp-uniform
+          asm volatile("bar.sync %0, 64;" :: "r"(1 + ew) : "memory");
+          const bool mine = hf == 0 && j < s_cnt[gl];
+          float m1 = -INFINITY, s1 = 0.f;
+          if (mine) {
+            int32_t mk[kGtMaxK];
+            int me[kGtMaxK];
+            int ia = 0, ib = 0;
+#pragma unroll
+            for (int s = 0; s < kGtMaxK; ++s) {
+              mk[s] = INT_MIN;
+              me[s] = 0;
+              if (s < K) {
+                int32_t ka = INT_MIN;
+                int ea = 0;
+#pragma unroll
+                for (int q = 0; q < kGtMaxK; ++q)
+                  if (q == ia) { ka = sel_k[q]; ea = sel_e[q]; }
+                const int32_t kb_ = xr[ib];
+                if (ka >= kb_) { mk[s] = ka; me[s] = ea; ++ia; }
+                else { mk[s] = kb_; me[s] = xr[8 + ib]; ++ib; }
+              }
+            }
+#pragma unroll
+            for (int s = 0; s < kGtMaxK; ++s) {
+              sel_k[s] = mk[s];
+              sel_e[s] = me[s];
+            }
+            m1 = __int_as_float(xr[16]);
+            s1 = __int_as_float(xr[17]);
+          }
+          asm volatile("bar.sync %0, 64;" :: "r"(1 + ew) : "memory");     // xch reusable
+          if (!mine) continue;
+          const float mx = key_to_f(sel_k[0]);
+          // all -inf rows: NaN, as the single-thread path gives
+          ex = mx > -INFINITY ? sh * __expf(mh - mx) + s1 * __expf(m1 - mx) : __int_as_float(0x7fc00000);
+        }
       } else {
-        // N' > 64 (e.g. DeepSeek-V2, 160 experts): too many logits for one
-        // thread's registers.  A two-level tournament: one pass over the row
+        // N' > kGtRegMaxNP (e.g. DeepSeek-V2, 160 experts; and N' = 48 / 64,
+        // where the register path's k full-width tree passes made the
+        // epilogue as long as the tile's K loop).  A two-level tournament: one pass over the row
         // in 16-column TMEM chunks (warp-uniform loads) stages the biased
         // logits in shared memory and keeps each chunk's winner (max-tree,
         // the lower slot winning ties) plus an online softmax denominator;
@@ -506,23 +590,20 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
   }
 }
 
-template <int NP, int SUB, int ST, int HALF = 0>
+template <int NP, int SUB, int ST>
 static int launch_cfg(const CUtensorMap& mh, const CUtensorMap& mw, const GateTcArgs& a,
                       int64_t n_rows_bound, cudaStream_t st) {
-  using S = GtShape<NP, SUB, ST, HALF>;
-  static_assert(!HALF || 2 * (S::kSmem + 2048) <= 228 * 1024, "two CTAs per SM");
+  using S = GtShape<NP, SUB, ST>;
+  static_assert(S::kSmem <= 227 * 1024, "shared memory budget of one CTA per SM");
   static bool attr = false;
   if (!attr) {
-    SMOE_CUDA_TRY(cudaFuncSetAttribute(gate_tc_kernel<NP, SUB, ST, HALF>,
+    SMOE_CUDA_TRY(cudaFuncSetAttribute(gate_tc_kernel<NP, SUB, ST>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::kSmem));
     attr = true;
   }
-  const int64_t tiles = ceil_div(n_rows_bound, S::kRows) + a.shard_count;
-  const int grid =
-      (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (HALF ? 2 : 1) * num_sms()));
-  SMOE_CUDA_TRY(launch_pdl(gate_tc_kernel<NP, SUB, ST, HALF>, grid,
-                           HALF ? kGtThreads - 64 : kGtThreads, S::kSmem, st,
-                           mh, mw, a));
+  const int64_t tiles = ceil_div(n_rows_bound, kGtRows) + a.shard_count;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms()));
+  SMOE_CUDA_TRY(launch_pdl(gate_tc_kernel<NP, SUB, ST>, grid, S::kThreads, S::kSmem, st, mh, mw, a));
   SMOE_LAUNCH_CHECK();
   return SMOE_OK;
 }
@@ -538,29 +619,17 @@ static int ring_sub() {
   return sub;
 }
 
-// 64-row tiles while the 128-row tiles would not fill ~1.25 waves of SMs
-// (SMOE_GATE_HALF = 0 / 1 forces them off / on, tuning only)
-static bool use_half(int64_t n_rows_bound) {
-  static int mode = [] {
-    const char* e = getenv("SMOE_GATE_HALF");
-    return e ? atoi(e) : -1;
-  }();
-  if (mode >= 0) return mode == 1;
-  return 4 * ceil_div(n_rows_bound, kGtRows) <= 5 * (int64_t)num_sms();
-}
-
 template <int NP>
-static int launch_np(const CUtensorMap& mh, const CUtensorMap* mh64, const CUtensorMap& mw,
-                     const GateTcArgs& a, int64_t n_rows_bound, cudaStream_t st) {
-  if constexpr (NP <= 64) {
-    if (mh64 && use_half(n_rows_bound))
-      return launch_cfg<NP, 2, (NP <= 32 ? 4 : 3), 1>(*mh64, mw, a, n_rows_bound, st);
-  }
-  // wide gates: one k-block per stage keeps 4 stages of H + W(N' x 64) in smem
+static int launch_np(const CUtensorMap& mh, const CUtensorMap& mw, const GateTcArgs& a,
+                     int64_t n_rows_bound, cudaStream_t st) {
   if constexpr (NP > 64) {
     // wide gates: one k-block per stage, and fewer stages to leave room for
     // the staged logits (NP <= 160: 3 stages, else 2)
     return launch_cfg<NP, 1, (NP <= 160 ? 3 : 2)>(mh, mw, a, n_rows_bound, st);
+  } else if constexpr (GtShape<NP, 2, 3>::kWide) {
+    // shared-memory tournament at N' <= 64: 3 stages of 2 k-blocks leave room
+    // for the 128 staged rows
+    return launch_cfg<NP, 2, 3>(mh, mw, a, n_rows_bound, st);
   } else {
     switch (ring_sub()) {
       case 1: return launch_cfg<NP, 1, 8>(mh, mw, a, n_rows_bound, st);
@@ -586,19 +655,18 @@ bool gate_tc_supported(int32_t n_experts, int32_t top_k, int64_t d) {
          top_k <= n_experts && d % (4 * kGemmBK) == 0;
 }
 
-int launch_gate_tc(const CUtensorMap& map_h, const CUtensorMap* map_h64,
-                   const CUtensorMap& map_w, const GateTcArgs& a, int64_t n_rows_bound,
-                   cudaStream_t st) {
+int launch_gate_tc(const CUtensorMap& map_h, const CUtensorMap& map_w, const GateTcArgs& a,
+                   int64_t n_rows_bound, cudaStream_t st) {
   if (n_rows_bound <= 0) return SMOE_OK;
   switch (gate_tc_rows(a.n_experts)) {
-    case 16: return launch_np<16>(map_h, map_h64, map_w, a, n_rows_bound, st);
-    case 32: return launch_np<32>(map_h, map_h64, map_w, a, n_rows_bound, st);
-    case 48: return launch_np<48>(map_h, map_h64, map_w, a, n_rows_bound, st);
-    case 64: return launch_np<64>(map_h, map_h64, map_w, a, n_rows_bound, st);
-    case 128: return launch_np<128>(map_h, map_h64, map_w, a, n_rows_bound, st);
-    case 160: return launch_np<160>(map_h, map_h64, map_w, a, n_rows_bound, st);
-    case 192: return launch_np<192>(map_h, map_h64, map_w, a, n_rows_bound, st);
-    case 256: return launch_np<256>(map_h, map_h64, map_w, a, n_rows_bound, st);
+    case 16: return launch_np<16>(map_h, map_w, a, n_rows_bound, st);
+    case 32: return launch_np<32>(map_h, map_w, a, n_rows_bound, st);
+    case 48: return launch_np<48>(map_h, map_w, a, n_rows_bound, st);
+    case 64: return launch_np<64>(map_h, map_w, a, n_rows_bound, st);
+    case 128: return launch_np<128>(map_h, map_w, a, n_rows_bound, st);
+    case 160: return launch_np<160>(map_h, map_w, a, n_rows_bound, st);
+    case 192: return launch_np<192>(map_h, map_w, a, n_rows_bound, st);
+    case 256: return launch_np<256>(map_h, map_w, a, n_rows_bound, st);
     default: return SMOE_ERR_UNSUPPORTED;
   }
 }

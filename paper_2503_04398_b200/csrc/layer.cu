@@ -46,7 +46,7 @@ struct smoe_layer {
   CUtensorMap map_x_narrow, map_h_narrow;   // 32-row A boxes (decode-sized batches)
   // tensor-core gate: hidden rows of the resident shards (one arena) and W_g
   bool gate_tc = false;
-  CUtensorMap map_hs, map_hs64, map_wg;   // hs arena with 128- and 64-row boxes
+  CUtensorMap map_hs, map_wg;
   // SMOE_PIPELINE_DSMOE: all-reduce + slice instead of SRS, combine into
   // all-gather blocks + resume gather instead of the fused SAG
   int32_t pipeline = SMOE_PIPELINE_SMOE;
@@ -284,8 +284,6 @@ static int ensure_maps(smoe_layer* L) {
   if (arena &&
       make_tmap_bf16(&L->map_hs, L->buf[SMOE_BUF_HS][0], c.shard_count * (int64_t)c.max_tokens,
                      c.hidden, 128) == SMOE_OK &&
-      make_tmap_bf16(&L->map_hs64, L->buf[SMOE_BUF_HS][0], c.shard_count * (int64_t)c.max_tokens,
-                     c.hidden, 64) == SMOE_OK &&
       make_tmap_bf16(&L->map_wg, L->w_gate, c.n_experts, c.hidden,
                      gate_tc_rows(c.n_experts)) == SMOE_OK)
     L->gate_tc = true;
@@ -423,7 +421,7 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
         g.topk_ids = local_ptrs(L, SMOE_BUF_TOPK_IDS);
         g.topk_w = local_ptrs(L, SMOE_BUF_TOPK_W);
         g.stats = stats;
-        return launch_gate_tc(L->map_hs, &L->map_hs64, L->map_wg, g, n, st);
+        return launch_gate_tc(L->map_hs, L->map_wg, g, n, st);
       }
       return launch_gate(lr, local_ptrs(L, SMOE_BUF_HS), c.hidden, L->w_gate, L->b_gate,
                          c.n_experts, c.top_k, c.renormalize, L->slot_owner_d,

@@ -52,11 +52,8 @@ bool gate_tc_supported(int32_t n_experts, int32_t top_k, int64_t d);
 int gate_tc_enabled();                 // SMOE_OPT_GATE_TENSOR
 void set_gate_tc_enabled(int on);
 int gate_tc_rows(int32_t n_experts);   // W box rows (N rounded up to 16)
-// map_h: 128-row H boxes; map_h64 (optional): 64-row boxes of the same arena,
-// used for batches whose 128-row tiles would leave SMs idle
-int launch_gate_tc(const CUtensorMap& map_h, const CUtensorMap* map_h64,
-                   const CUtensorMap& map_w, const GateTcArgs& a, int64_t n_rows_bound,
-                   cudaStream_t st);
+int launch_gate_tc(const CUtensorMap& map_h, const CUtensorMap& map_w, const GateTcArgs& a,
+                   int64_t n_rows_bound, cudaStream_t st);
 
 
 size_t route_workspace_bytes(int64_t max_tokens, int32_t k, int32_t N, int32_t shard_count);
