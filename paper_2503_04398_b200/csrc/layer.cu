@@ -372,17 +372,16 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
   switch (stage) {
     case SMOE_STAGE_PLAN: {
       if (n > 0 && !tokens) return SMOE_ERR_INVALID_ARG;
-      SMOE_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(int64_t) * SMOE_STAT__COUNT, st));
-      SMOE_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
       const int64_t* lookup_hist = (hist && hist_depth >= L->hist_len) ? hist : nullptr;
-      return smoe_lookup_plan(tokens, n, lookup_hist, L->hist_len, L->t_labels, L->t_conf, L->vocab,
-                              L->a_best, L->a_conf, L->a_rows, c.n_shards,
-                              static_cast<int64_t*>(L->buf[SMOE_BUF_DEV][0]),
-                              static_cast<int64_t*>(L->buf[SMOE_BUF_FORWARD][0]),
-                              static_cast<int64_t*>(L->buf[SMOE_BUF_INVERSE][0]),
-                              static_cast<int32_t*>(L->buf[SMOE_BUF_PLAN_COUNTS][0]),
-                              static_cast<int64_t*>(L->buf[SMOE_BUF_GROUP][0]), err,
-                              L->buf[SMOE_BUF_WORKSPACE][0], plan_ws_aligned(&c), stream);
+      return layer_plan(tokens, n, lookup_hist, L->hist_len, L->t_labels, L->t_conf, L->vocab,
+                        L->a_best, L->a_conf, L->a_rows, c.n_shards,
+                        static_cast<int64_t*>(L->buf[SMOE_BUF_DEV][0]),
+                        static_cast<int64_t*>(L->buf[SMOE_BUF_FORWARD][0]),
+                        static_cast<int64_t*>(L->buf[SMOE_BUF_INVERSE][0]),
+                        static_cast<int32_t*>(L->buf[SMOE_BUF_PLAN_COUNTS][0]),
+                        static_cast<int64_t*>(L->buf[SMOE_BUF_GROUP][0]), err,
+                        L->buf[SMOE_BUF_WORKSPACE][0], plan_ws_aligned(&c), stats,
+                        SMOE_STAT__COUNT, st);
     }
     case SMOE_STAGE_SRS:
       // every process's partials for this batch are written before any peer

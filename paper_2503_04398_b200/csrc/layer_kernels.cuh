@@ -108,3 +108,15 @@ int launch_barrier(const ShardPtrs& signals, int32_t world, int32_t rank, uint32
                    uint32_t* epoch, cudaStream_t st);
 
 }  // namespace smoe
+
+namespace smoe {
+// PLAN stage of the layer (plan.cu): smoe_lookup_plan plus the per-forward
+// resets of `err` and stats[0, n_stats) -- folded into the single-CTA plan
+// kernel for decode-sized batches
+int layer_plan(const int64_t* tokens, int64_t n, const int64_t* hist, int32_t hist_len,
+               const int16_t* t_labels, const float* t_conf, int64_t vocab,
+               const int16_t* a_best, const float* a_conf, int64_t a_rows, int32_t n_clusters,
+               int64_t* dev_out, int64_t* forward, int64_t* inverse, int32_t* counts,
+               int64_t* group, int32_t* err, void* workspace, size_t workspace_bytes,
+               int64_t* stats, int32_t n_stats, cudaStream_t st);
+}  // namespace smoe

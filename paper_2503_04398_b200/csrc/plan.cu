@@ -171,8 +171,16 @@ plan_single_kernel(LookupTables t, int use_lookup, const int64_t* __restrict__ t
                    const int64_t* __restrict__ devices, int64_t n, int32_t G,
                    int64_t* __restrict__ dev_out, int64_t* __restrict__ forward,
                    int64_t* __restrict__ inverse, int32_t* __restrict__ counts_out,
-                   int64_t* __restrict__ group_out, int32_t* err) {
+                   int64_t* __restrict__ group_out, int32_t* err, int64_t* zero_stats,
+                   int32_t n_zero_stats) {
   pdl_enter();
+  // the layer's per-forward resets (error flag, event counters), folded in so
+  // a decode-sized forward starts with one kernel instead of two memsets and
+  // a kernel; the __syncthreads below orders them before any lookup error
+  if (zero_stats) {
+    if (threadIdx.x < n_zero_stats) zero_stats[threadIdx.x] = 0;
+    if (threadIdx.x == 0 && err) *err = 0;
+  }
   extern __shared__ int32_t smem[];
   int32_t* s_cnt = smem;                  // [G] tokens per device
   int32_t* s_base = smem + G;             // [G] running offset per device
@@ -240,10 +248,23 @@ plan_single_kernel(LookupTables t, int use_lookup, const int64_t* __restrict__ t
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// zero_stats (layer only): when non-null, err and zero_stats[0, n_zero_stats)
+// are reset before the lookup -- inside the kernel for single-tile batches,
+// by memsets otherwise.
 static int plan_impl(const LookupTables& t, int use_lookup, const int64_t* tokens,
                      const int64_t* devices, int64_t n, int32_t G, int64_t* dev_out,
                      int64_t* forward, int64_t* inverse, int32_t* counts, int64_t* group,
-                     int32_t* err, void* ws, size_t ws_bytes, cudaStream_t st) {
+                     int32_t* err, void* ws, size_t ws_bytes, cudaStream_t st,
+                     int64_t* zero_stats = nullptr, int32_t n_zero_stats = 0) {
+#ifndef SMOE_PLAN_FOLD
+#define SMOE_PLAN_FOLD 1      // 0: memsets before every plan (A/B builds)
+#endif
+  const bool single =
+      SMOE_PLAN_FOLD && n > 0 && n <= kPlanTile && n_zero_stats <= kPlanThreads;
+  if (zero_stats && !single) {
+    SMOE_CUDA_TRY(cudaMemsetAsync(zero_stats, 0, sizeof(int64_t) * n_zero_stats, st));
+    if (err) SMOE_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
+  }
   if (G < 1 || G > SMOE_MAX_PLAN_DEVICES) return SMOE_ERR_UNSUPPORTED;
   if (n < 0 || !counts || !group || (n > 0 && (!forward || !inverse))) return SMOE_ERR_INVALID_ARG;
   if (ws_bytes < smoe_plan_workspace_bytes(n, G) || (n > 0 && !ws)) return SMOE_ERR_INVALID_ARG;
@@ -261,7 +282,7 @@ static int plan_impl(const LookupTables& t, int use_lookup, const int64_t* token
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     SMOE_CUDA_TRY(launch_pdl(plan_single_kernel, 1, kPlanThreads, smem2, st, t, use_lookup,
                              tokens, devices, n, G, dev_out, forward, inverse, counts, group,
-                             err));
+                             err, single ? zero_stats : nullptr, n_zero_stats));
     SMOE_LAUNCH_CHECK();
     return SMOE_OK;
   }
@@ -328,3 +349,25 @@ extern "C" int smoe_lookup_plan(const int64_t* tokens, int64_t n, const int64_t*
   return plan_impl(t, 1, tokens, nullptr, n, n_clusters, dev_out, forward, inverse, counts,
                    group, err, workspace, workspace_bytes, as_stream(stream));
 }
+
+namespace smoe {
+// The layer's PLAN stage: smoe_lookup_plan + the per-forward resets of the
+// error flag and the event counters (see plan_impl).
+int layer_plan(const int64_t* tokens, int64_t n, const int64_t* hist, int32_t hist_len,
+               const int16_t* t_labels, const float* t_conf, int64_t vocab,
+               const int16_t* a_best, const float* a_conf, int64_t a_rows, int32_t n_clusters,
+               int64_t* dev_out, int64_t* forward, int64_t* inverse, int32_t* counts,
+               int64_t* group, int32_t* err, void* workspace, size_t workspace_bytes,
+               int64_t* stats, int32_t n_stats, cudaStream_t st) {
+  if (n > 0 && (!tokens || !t_labels || !t_conf)) return SMOE_ERR_INVALID_ARG;
+  if (hist && (!a_best || !a_conf || hist_len < 0)) return SMOE_ERR_INVALID_ARG;
+  LookupTables t{t_labels, t_conf, vocab, a_best, a_conf, a_rows, n_clusters, hist, hist_len};
+  if (n == 0) {
+    SMOE_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(int64_t) * n_stats, st));
+    SMOE_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
+  }
+  return plan_impl(t, 1, tokens, nullptr, n, n_clusters, dev_out, forward, inverse, counts,
+                   group, err, workspace, workspace_bytes, st, n > 0 ? stats : nullptr,
+                   n_stats);
+}
+}  // namespace smoe

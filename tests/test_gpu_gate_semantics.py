@@ -108,9 +108,13 @@ def test_exact_ties_break_in_slot_order(N, k, gate_kernel):
     assert np.linalg.norm(out - ref["out"]) / np.linalg.norm(ref["out"]) <= 1e-2
 
 
-@pytest.mark.parametrize("masked", ["all_but_one", "half"])
-@pytest.mark.parametrize("N", [16, 160])
+@pytest.mark.parametrize("masked", ["all_but_one", "half", "slot_upper_half",
+                                    "slot_lower_half"])
+@pytest.mark.parametrize("N", [16, 64, 160])
 def test_minus_inf_bias_masks(masked, N, gate_kernel):
+    # N = 64 runs the split epilogue (two threads per row, columns halved in
+    # s-EG slot order): the slot_*_half masks leave one thread's half with no
+    # finite logit at all
     if N > 64 and gate_kernel == 0:
         pytest.skip("the mma.sync / CUDA-core gates cover N <= 64")
     G, k, d, f, n = 4, 3, 256, 256, 500
@@ -121,8 +125,13 @@ def test_minus_inf_bias_masks(masked, N, gate_kernel):
     if masked == "all_but_one":
         bias[:] = -np.inf
         bias[5] = 0.0                           # one finite logit < k: the rest are -inf slots
-    else:
+    elif masked == "half":
         bias[rng.permutation(N)[: N // 2]] = -np.inf
+    else:
+        labels = np.asarray(w.bundle.expert_labels, dtype=np.int64)
+        n2o, _ = S.gate_permutation(labels, G)           # slot -> original expert
+        half = n2o[N // 2:] if masked == "slot_upper_half" else n2o[: N // 2]
+        bias[np.asarray(half)] = -np.inf
     layer, out, ref = _run(w.bundle, w.gate_w, w.w1, w.w3, w.w2, w.partials, w.tokens, k, bias)
     r = layer.routing(n)
     assert np.array_equal(r["experts"], ref["experts"])
