@@ -99,7 +99,12 @@ template <int NP, int SUB, int ST> struct GtShape {
   // (kWideRows rows at a time: 128, or 64 in two phases for N' > 192)
   static constexpr int kWideRows = NP > 192 ? 64 : 128;
   static constexpr int kWideLd = NP + 4;                   // floats per staged row (16 B pad)
-  static constexpr uint32_t kWideBytes = kWide ? kWideRows * kWideLd * 4 : 0;
+  // + per staged row: each 16-column chunk's winner key / slot / taken mask
+  // and the k selections (key, slot), stored field-major ([field][row]: the
+  // lanes of a warp hit consecutive banks)
+  static constexpr int kWideFields = 3 * (NP / 16) + 2 * kGtMaxK;
+  static constexpr uint32_t kWideBytes =
+      kWide ? kWideRows * kWideLd * 4 + kWideRows * kWideFields * 4 : 0;
   static constexpr size_t kSmem = 1024 + ST * kStageBytes + 128 + kWideBytes + kXchBytes;
   // D f32, A/B bf16, both K-major, N = NP, M = 128
   static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) |
@@ -410,25 +415,31 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
           ex = mx > -INFINITY ? sh * __expf(mh - mx) + s1 * __expf(m1 - mx) : __int_as_float(0x7fc00000);
         }
       } else {
-        // N' > kGtRegMaxNP (e.g. DeepSeek-V2, 160 experts; and N' = 48 / 64,
-        // where the register path's k full-width tree passes made the
-        // epilogue as long as the tile's K loop).  A two-level tournament: one pass over the row
-        // in 16-column TMEM chunks (warp-uniform loads) stages the biased
-        // logits in shared memory and keeps each chunk's winner (max-tree,
-        // the lower slot winning ties) plus an online softmax denominator;
+        // N' > kGtRegMaxNP (e.g. DeepSeek-V2, 160 experts): too many logits
+        // for one thread's registers.  A two-level tournament: one pass over
+        // the row in 16-column TMEM chunks (warp-uniform loads) stages the
+        // biased logits in shared memory with each chunk's winner (max-tree,
+        // the lower slot winning ties) and an online softmax denominator;
         // each selection takes the best chunk winner (the lower chunk on
-        // ties) and refills only that chunk -- from shared memory, since the
-        // winning chunk differs between the rows of a warp and a TMEM load
-        // address must not.  For N' > 192 the rows are staged 64 at a time.
+        // ties) and refills only that chunk from shared memory.  Every loop
+        // over chunks and selections is ROLLED, with the per-chunk state in
+        // the row's shared-memory record: fully unrolled, the N' = 160 epilogue
+        // was ~6 900 straight-line instructions per warp that missed the
+        // instruction cache on nearly every issue (34 us of an 82 us gate,
+        // profiles/r2/gate/).  For N' > 192 the rows are staged 64 at a time.
         constexpr int NC = NP / 16;
         constexpr int kGroups = 128 / S::kWideRows;          // 1, or 2 for N' > 192
         constexpr int kWarpsPerGroup = 4 / kGroups;
-        float* myrow = wide + ((ew % kWarpsPerGroup) * 32 + lane) * S::kWideLd;
-        int32_t cwk[NC];
-        int cwi[NC];
-        uint32_t tk[NC];
-        // max-tree over the keys of chunk c (x = staged logits, taken /
-        // invalid slots -> INT_MIN)
+        const int srow = (ew % kWarpsPerGroup) * 32 + lane;     // staging row of this thread
+        float* myrow = wide + srow * S::kWideLd;
+        constexpr int R = S::kWideRows;                          // field stride
+        int32_t* fld = reinterpret_cast<int32_t*>(wide + R * S::kWideLd) + srow;
+        int32_t* cwk = fld;                                      // [NC] chunk winner keys
+        int32_t* cwi = fld + NC * R;                             // [NC] their slots
+        int32_t* ctk = fld + 2 * NC * R;                         // [NC] taken masks
+        int32_t* sk = fld + 3 * NC * R;                          // [kGtMaxK] selections
+        int32_t* se = sk + kGtMaxK * R;
+        // max-tree over the 16 staged keys of chunk c (taken / invalid -> INT_MIN)
         auto chunk_best = [&](int c, const float (&x)[16], uint32_t taken, int32_t& bk,
                               int& bi) {
           int32_t tv[8];
@@ -459,7 +470,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
         for (int grp = 0; grp < kGroups; ++grp) {
           if (ew / kWarpsPerGroup == grp) {
             float m = -INFINITY;
-#pragma unroll
+#pragma unroll 1
             for (int c = 0; c < NC; ++c) {
               uint32_t v[16];
               SMOE_TMEM_LD16(taddr + c * 16, v);
@@ -471,8 +482,12 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
               for (int q = 0; q < 4; ++q)
                 *reinterpret_cast<float4*>(myrow + c * 16 + 4 * q) =
                     make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
-              tk[c] = 0;
-              chunk_best(c, x, 0u, cwk[c], cwi[c]);
+              int32_t bk;
+              int bi;
+              chunk_best(c, x, 0u, bk, bi);
+              cwk[c * R] = bk;
+              cwi[c * R] = bi;
+              ctk[c * R] = 0;
               float cm = -INFINITY;
 #pragma unroll
               for (int i = 0; i < 16; ++i)
@@ -490,38 +505,38 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+#pragma unroll 1
+            for (int s = 0; s < K; ++s) {
+              int32_t bk = cwk[0];
+              int bc = 0;
+#pragma unroll 1
+              for (int c = 1; c < NC; ++c) {
+                const int32_t ck = cwk[c * R];
+                if (ck > bk) { bk = ck; bc = c; }
+              }
+              const int bi = cwi[bc * R];
+              const uint32_t taken = (uint32_t)ctk[bc * R] | (1u << (bi & 15));
+              ctk[bc * R] = (int32_t)taken;
+              sk[s * R] = bk;
+              se[s * R] = bi;
+              if (s + 1 < K) {                   // refill the winning chunk (own row, smem)
+                float x[16];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const float4 f = *reinterpret_cast<const float4*>(myrow + bc * 16 + 4 * q);
+                  x[4 * q] = f.x; x[4 * q + 1] = f.y; x[4 * q + 2] = f.z; x[4 * q + 3] = f.w;
+                }
+                int32_t nk;
+                int ni;
+                chunk_best(bc, x, taken, nk, ni);
+                cwk[bc * R] = nk;
+                cwi[bc * R] = ni;
+              }
+            }
 #pragma unroll
             for (int s = 0; s < kGtMaxK; ++s) {
-              sel_e[s] = 0;
-              sel_k[s] = INT_MIN;
-              if (s < K) {
-                int32_t bk = cwk[0];
-                int bc = 0;
-#pragma unroll
-                for (int c = 1; c < NC; ++c)
-                  if (cwk[c] > bk) { bk = cwk[c]; bc = c; }
-                int bi = 0;
-                uint32_t taken = 0;
-#pragma unroll
-                for (int c = 0; c < NC; ++c)
-                  if (c == bc) { bi = cwi[c]; tk[c] |= 1u << (cwi[c] & 15); taken = tk[c]; }
-                sel_e[s] = bi;
-                sel_k[s] = bk;
-                if (s + 1 < K) {                   // refill the winning chunk (own row, smem)
-                  float x[16];
-#pragma unroll
-                  for (int q = 0; q < 4; ++q) {
-                    const float4 f = *reinterpret_cast<const float4*>(myrow + bc * 16 + 4 * q);
-                    x[4 * q] = f.x; x[4 * q + 1] = f.y; x[4 * q + 2] = f.z; x[4 * q + 3] = f.w;
-                  }
-                  int32_t nk;
-                  int ni;
-                  chunk_best(bc, x, taken, nk, ni);
-#pragma unroll
-                  for (int c = 0; c < NC; ++c)
-                    if (c == bc) { cwk[c] = nk; cwi[c] = ni; }
-                }
-              }
+              sel_k[s] = s < K ? sk[s * R] : INT_MIN;
+              sel_e[s] = s < K ? se[s * R] : 0;
             }
           }
           if constexpr (kGroups > 1) {

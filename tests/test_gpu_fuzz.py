@@ -15,15 +15,22 @@ from paper_2503_04398_b200 import SpecMoELayer, synth
 TOL = 1e-2
 
 
-def _cases(count=24, seed=None):
+def _cases(count=24, seed=None, wide=False):
+    """wide: N in 65..256 (the tcgen05 gate's N' = 128 / 160 / 192 / 256
+    tournament epilogue); else N <= 64 (register epilogue, split at N' = 64)."""
     import os
     seed = int(os.environ.get("SMOE_FUZZ_SEED", "2025")) if seed is None else seed
-    rng = np.random.default_rng(seed)
+    rng = np.random.default_rng(seed + (7919 if wide else 0))
     out = []
     for i in range(count):
         G = int(rng.choice([1, 2, 3, 4, 5, 8, 12, 16]))
-        per = int(rng.integers(1, max(2, 64 // G) + 1))
-        N = min(64, G * per)
+        if wide:
+            N = int(rng.integers(65, 257))
+            N -= N % G                              # clusters of equal size
+            N = max(N, 65 + (-65) % G)
+        else:
+            per = int(rng.integers(1, max(2, 64 // G) + 1))
+            N = min(64, G * per)
         k = int(rng.integers(1, min(8, N) + 1))
         d = int(rng.choice([256, 512, 768]))
         f = int(rng.choice([128, 256, 384]))
@@ -34,7 +41,8 @@ def _cases(count=24, seed=None):
     return out
 
 
-@pytest.mark.parametrize("c", _cases(), ids=lambda c: "case{i}-G{G}-N{N}-k{k}-d{d}-n{n}".format(**c))
+@pytest.mark.parametrize("c", _cases() + _cases(count=10, wide=True),
+                         ids=lambda c: "case{i}-G{G}-N{N}-k{k}-d{d}-n{n}".format(**c))
 def test_random_layer_matches_oracle(c):
     over = {"G": c["G"], "N": c["N"], "k": c["k"], "d": c["d"], "f": c["f"]}
     w = synth.make_workload("toy", n=c["n"], eps=c["eps"], seed=100 + c["i"], cfg_override=over)
