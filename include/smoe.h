@@ -46,6 +46,8 @@ extern "C" {
 #define SMOE_ERRBIT_HISTORY_RANGE  8  /* numpy IndexError on confidence[rows]*/
 #define SMOE_ERRBIT_INDEX_RANGE   16  /* numpy IndexError on a fancy index   */
 #define SMOE_ERRBIT_CAPACITY      32  /* a layer buffer would overflow        */
+#define SMOE_ERRBIT_TIMEOUT       64  /* an in-kernel wait on another grid    */
+                                    /* exceeded its bound (results invalid) */
 
 #define SMOE_MAX_SHARDS 16          /* EP degree G supported by the layer    */
 #define SMOE_MAX_PLAN_DEVICES 1024  /* n_devices supported by rebatch plan   */
@@ -71,6 +73,10 @@ const char* smoe_version(void);
                                         /* send each token row once per remote shard */
                                         /* (the owner fans it out to its experts),   */
                                         /* 0 = one row per remote (token, expert)    */
+#define SMOE_OPT_EARLY_DOWN          8  /* decode-sized batches: the down GEMM's  */
+                                        /* CTAs start on the SMs the up GEMM's     */
+                                        /* tail frees and wait per expert for its  */
+                                        /* hidden rows (1 = default, 0 = off)      */
 int smoe_set_option(int32_t key, int32_t value);
 int smoe_get_option(int32_t key);
 const char* smoe_status_string(int status);

@@ -77,6 +77,7 @@ ERRBIT_TOKEN_RANGE = 4
 ERRBIT_HISTORY_RANGE = 8
 ERRBIT_INDEX_RANGE = 16
 ERRBIT_CAPACITY = 32
+ERRBIT_TIMEOUT = 64
 MAX_SHARDS = 16
 OPT_GEMM_CTA_GROUP_UP, OPT_GEMM_CTA_GROUP_DOWN, OPT_GATE_TENSOR = 0, 1, 2
 OPT_GEMM_PAIR_MIN_ROWS = 3
@@ -84,6 +85,7 @@ OPT_PDL = 4
 OPT_PDL_STAGES = 5
 OPT_GEMM_NARROW_MAX_ROWS = 6
 OPT_DEDUP_DISPATCH = 7
+OPT_EARLY_DOWN = 8
 
 (BUF_PARTIAL, BUF_XIN, BUF_XMETA, BUF_YPAIR, BUF_OUT, BUF_COUNTS, BUF_SIGNAL, BUF_HS,
  BUF_TOPK_IDS, BUF_TOPK_W, BUF_PAIR_RANK, BUF_HMID, BUF_FORWARD, BUF_INVERSE, BUF_DEV,

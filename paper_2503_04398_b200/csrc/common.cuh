@@ -45,6 +45,7 @@ int pdl_enabled();                      // SMOE_OPT_PDL (default 1; env SMOE_PDL
 void set_pdl_enabled(int on);
 void set_pdl_stage(int stage);           // layer stage being launched (-1: none)
 int pdl_stage_mask();                    // SMOE_OPT_PDL_STAGES
+int pdl_stage_enabled(int stage);        // would `stage`'s kernels launch early?
 void set_pdl_stage_mask(int mask);
 
 // <<<grid, block, smem, st>>> with the PDL attribute when enabled.

@@ -36,6 +36,19 @@ struct GemmArgs {
   const int64_t* meta;       // scatter: per A row
   char* dst_base[SMOE_MAX_SHARDS];
   int64_t ldd;               // elements
+  // Per-problem readiness between the two expert GEMMs of a decode-sized
+  // forward (ready_role 0 = off).  Role 1 (up GEMM, one SM per 128-row tile):
+  // after its epilogue has stored a tile's hidden rows, one thread adds 1 to
+  // ready[p] (release, after a generic->async proxy fence).  Role 2 (down
+  // GEMM, launched early under PDL): skips griddepcontrol.wait and its TMA
+  // producer waits, per tile, until ready[p] counts every up tile of problem
+  // p (ceil(m / ready_up_tile_m) * ready_up_n_tiles); a wait past ~10 ms sets
+  // SMOE_ERRBIT_TIMEOUT in err and gives up instead of hanging.
+  int32_t* ready;
+  int32_t ready_role;
+  int32_t ready_up_tile_m;
+  int32_t ready_up_n_tiles;
+  int32_t* err;
 };
 
 // Encodes a 2D bf16 K-major tensor map (rows x cols, box 64 x box_rows, 128B swizzle).
@@ -60,6 +73,10 @@ void set_gemm_narrow_max_rows(int rows);
 
 // cg: 1 = one SM per 128x256 tile, 2 = SM pair per 256x256 tile, 0 = one SM
 // per 32x256 tile (narrow; tmap_a must have kGemmNarrowM-row boxes).
+// SMOE_OPT_EARLY_DOWN (default 1)
+int gemm_early_down();
+void set_gemm_early_down(int on);
+
 int launch_grouped_gemm(const CUtensorMap& tmap_a, const CUtensorMap& tmap_b,
                         const GemmArgs& args, int32_t epilogue, int cg, cudaStream_t stream);
 

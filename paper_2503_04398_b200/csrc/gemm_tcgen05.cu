@@ -182,7 +182,11 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
   // everything above touches constant data only (weights, tensor maps, smem,
   // TMEM); the problem table is written by the dispatch stage
   pdl_trigger();
-  pdl_wait();
+  // role 2 (the decode down GEMM): no grid-wide wait on the up GEMM -- its
+  // inputs written before the up GEMM started (problem table, row metadata)
+  // are visible once this grid runs, and the up GEMM's hidden rows are
+  // awaited per problem by the producer below
+  if (args.ready_role != 2) pdl_wait();
   // ---- problem table -> shared, tile prefix
   for (int p = threadIdx.x; p < np; p += kThreads) {
     const int64_t* q = args.problems + 4 * p;
@@ -228,6 +232,24 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         const int32_t b_box0 =
             ((sp.b_idx[tc.p] * args.n_tiles_n + tc.n_blk) * args.num_k_blocks) * kGemmBN +
             rank * (kGemmBN / CG);
+        if (args.ready_role == 2) {
+          // every up tile of this problem must have stored its hidden rows
+          const int32_t mp = sp.m[tc.p] > 0 ? sp.m[tc.p] : 0;
+          const int32_t need =
+              ((mp + args.ready_up_tile_m - 1) / args.ready_up_tile_m) * args.ready_up_n_tiles;
+          const long long t0 = clock64();
+          int32_t v;
+          do {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v)
+                         : "l"(args.ready + tc.p) : "memory");
+            if (v < need && clock64() - t0 > 20000000ll) {   // ~10 ms: never hang
+              if (args.err) atomicOr(args.err, SMOE_ERRBIT_TIMEOUT);
+              break;
+            }
+          } while (v < need);
+          // the rows were written through the generic proxy; TMA reads them
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         for (int32_t kb = 0; kb < args.num_k_blocks; ++kb) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
@@ -376,6 +398,16 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         }
         __syncwarp();
       }
+      if (args.ready_role == 1) {
+        // publish this tile's hidden rows to the early-started down GEMM:
+        // every epilogue thread fences its stores into the async proxy, the
+        // four epilogue warps meet, one thread releases the count
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (ew == 0 && lane == 0)
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" :: "l"(args.ready + tc.p)
+                       : "memory");
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -496,6 +528,10 @@ int gemm_b_box_rows(int cg) { return kGemmBN / cg; }
 // default: the narrow variant wins only while the expert-input buffer's
 // unused rows are zero (a fresh layer); in steady-state serving it measured
 // neutral to 3% slower under the power cap (profiles/r1_narrow/).
+static int g_early_down = 1;
+int gemm_early_down() { return g_early_down; }
+void set_gemm_early_down(int on) { g_early_down = on ? 1 : 0; }
+
 static int g_narrow_max_rows = -1;
 int gemm_narrow_max_rows() {
   if (g_narrow_max_rows < 0) {
@@ -509,6 +545,9 @@ void set_gemm_narrow_max_rows(int rows) { g_narrow_max_rows = rows; }
 int launch_grouped_gemm(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args,
                         int32_t epilogue, int cg, cudaStream_t st) {
   if (args.num_problems <= 0) return SMOE_OK;
+  // readiness counters: one SM per 128-row tile on both sides (the epilogue
+  // barrier counts four warps, the producer's target 128-row up tiles)
+  if (args.ready_role != 0 && (cg != 1 || !args.ready)) return SMOE_ERR_INVALID_ARG;
   if (args.num_problems > kGemmMaxProblems) return SMOE_ERR_UNSUPPORTED;
   const bool pair = cg == 2;
   if (cg == 0) {   // narrow m-blocks (tmap_a has kGemmNarrowM-row boxes)

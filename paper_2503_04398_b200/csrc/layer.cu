@@ -31,6 +31,7 @@ struct smoe_layer {
   std::vector<int32_t> slot_owner_h, slot_first_h;
   int32_t* slot_owner_d = nullptr;   // [N]
   int32_t* slot_first_d = nullptr;   // [G + 1]
+  int32_t* ready_d = nullptr;        // [kMaxExperts] up-tile counts (early down GEMM)
   int32_t local_slots = 0;           // expert slots owned by the resident shards
   // weights
   const void* w_gate = nullptr;
@@ -80,7 +81,8 @@ extern "C" int smoe_layer_create(const smoe_layer_config* cfg, smoe_layer** out)
   L->cfg = *cfg;
   std::memset(L->buf, 0, sizeof(L->buf));
   if (cudaMalloc(&L->slot_owner_d, sizeof(int32_t) * cfg->n_experts) != cudaSuccess ||
-      cudaMalloc(&L->slot_first_d, sizeof(int32_t) * (cfg->n_shards + 1)) != cudaSuccess) {
+      cudaMalloc(&L->slot_first_d, sizeof(int32_t) * (cfg->n_shards + 1)) != cudaSuccess ||
+      cudaMalloc(&L->ready_d, sizeof(int32_t) * kMaxExperts) != cudaSuccess) {
     delete L;
     return SMOE_ERR_CUDA;
   }
@@ -92,6 +94,7 @@ extern "C" void smoe_layer_destroy(smoe_layer* L) {
   if (!L) return;
   cudaFree(L->slot_owner_d);
   cudaFree(L->slot_first_d);
+  cudaFree(L->ready_d);
   delete L;
 }
 
@@ -330,6 +333,20 @@ static bool narrow_gemm(const smoe_layer* L, int64_t n) {
          n * (int64_t)c.top_k <= (int64_t)gemm_narrow_max_rows() * c.n_experts;
 }
 
+// decode-sized batch: at most gemm_pair_min_rows() routed rows per expert on
+// average (the layer's down GEMM then runs one SM per tile, see EXPERT_DOWN)
+static bool decode_batch(const smoe_layer* L, int64_t n) {
+  return n * (int64_t)L->cfg.top_k <= (int64_t)gemm_pair_min_rows() * L->cfg.n_experts;
+}
+
+// decode-sized batch whose down GEMM starts early (SMOE_OPT_EARLY_DOWN): both
+// GEMMs one SM per 128-row tile, the down GEMM launched under PDL
+static bool early_down(const smoe_layer* L, int64_t n) {
+  // (pdl_enabled() answers for the stage being launched: ask for the down GEMM's)
+  return gemm_early_down() && decode_batch(L, n) && !narrow_gemm(L, n) && L->maps_cg_up == 1 &&
+         pdl_stage_enabled(SMOE_STAGE_EXPERT_DOWN);
+}
+
 // hist: [n, hist_width] window of the previous layers' top-1 clusters (oldest
 // digit first), of which the newest hist_depth digits are valid.  The lookup
 // uses the n-gram table only for a full window (depth == width; the
@@ -467,6 +484,11 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       a.c = static_cast<char*>(L->buf[SMOE_BUF_HMID][0]);
       a.ldc = c.ffn;
       a.b_tiled = L->w_tiled;
+      if (early_down(L, n)) {
+        SMOE_CUDA_TRY(cudaMemsetAsync(L->ready_d, 0, sizeof(int32_t) * L->local_slots, st));
+        a.ready = L->ready_d;
+        a.ready_role = 1;
+      }
       // decode-sized batches stream the weights: narrow m-blocks keep more
       // weight tiles in flight per SM (gemm_tcgen05.cu, GemmShape NARROW)
       if (narrow_gemm(L, n) && L->maps_cg_up == 1)
@@ -487,7 +509,14 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       // decode-sized batches (<= gemm_pair_min_rows() routed rows per expert on
       // average): one SM per tile streams w2 in a single wave; the SM pair's
       // second, partial wave costs 5-16% there (profiles/r1_down_cta_group_small.jsonl)
-      const bool small = n * (int64_t)c.top_k <= (int64_t)gemm_pair_min_rows() * c.n_experts;
+      const bool small = decode_batch(L, n);
+      if (early_down(L, n)) {
+        a.ready = L->ready_d;
+        a.ready_role = 2;
+        a.ready_up_tile_m = kGemmBM;
+        a.ready_up_n_tiles = 2 * c.ffn / kGemmBN;
+        a.err = err;
+      }
       rc = narrow_gemm(L, n)
                ? launch_grouped_gemm(L->map_h_narrow, L->map_w2_single, a, kEpiScatter, 0, st)
            : small ? launch_grouped_gemm(L->map_h, L->map_w2_single, a, kEpiScatter, 1, st)
@@ -613,6 +642,10 @@ extern "C" int smoe_set_option(int32_t key, int32_t value) {
       if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
       g_dedup_dispatch = value;
       return SMOE_OK;
+    case SMOE_OPT_EARLY_DOWN:
+      if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
+      set_gemm_early_down(value);
+      return SMOE_OK;
     case SMOE_OPT_PDL:
       if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
       set_pdl_enabled(value);
@@ -635,6 +668,7 @@ extern "C" int smoe_get_option(int32_t key) {
   if (key == SMOE_OPT_PDL) return pdl_enabled();
   if (key == SMOE_OPT_PDL_STAGES) return pdl_stage_mask();
   if (key == SMOE_OPT_DEDUP_DISPATCH) return g_dedup_dispatch;
+  if (key == SMOE_OPT_EARLY_DOWN) return gemm_early_down();
   return -1;
 }
 
@@ -672,3 +706,10 @@ extern "C" int smoe_sag(const void* const* blocks, int32_t n_shards, const int64
   for (int i = 0; i < n_outs; ++i) o.p[i] = static_cast<char*>(outs[i]);
   return launch_sag(lr, hidden, b, o, n_outs, n_tokens, as_stream(stream));
 }
+
+#ifdef SMOE_DEBUG_READY
+extern "C" int smoe_debug_layer_ready(smoe_layer* L, int32_t* host, int32_t n) {
+  return cudaMemcpy(host, L->ready_d, sizeof(int32_t) * n, cudaMemcpyDeviceToHost) == cudaSuccess
+             ? 0 : -1;
+}
+#endif

@@ -42,6 +42,13 @@ int pdl_enabled() {
   return g_pdl && (g_pdl_stage < 0 || ((g_pdl_stage_mask >> g_pdl_stage) & 1));
 }
 void set_pdl_stage(int stage) { g_pdl_stage = stage; }
+int pdl_stage_enabled(int stage) {
+  const int saved = g_pdl_stage;
+  g_pdl_stage = stage;
+  const int on = pdl_enabled();
+  g_pdl_stage = saved;
+  return on;
+}
 int pdl_stage_mask() { pdl_enabled(); return g_pdl_stage_mask & 0xff; }
 void set_pdl_stage_mask(int mask) { pdl_enabled(); g_pdl_stage_mask = mask & 0xff; }
 void set_pdl_enabled(int on) { g_pdl = on ? 1 : 0; }

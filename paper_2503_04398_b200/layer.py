@@ -537,6 +537,9 @@ class SpecMoELayer:
 
     @staticmethod
     def _raise_for(bits: int):
+        if bits & N.ERRBIT_TIMEOUT:
+            raise RuntimeError("an in-kernel wait between the expert GEMMs timed out "
+                               "(results invalid); SMOE_OPT_EARLY_DOWN = 0 disables it")
         if bits & N.ERRBIT_CAPACITY:
             raise SchedulerError("expert_rows capacity exceeded; raise expert_rows")
         if bits & N.ERRBIT_DEVICE_RANGE:

@@ -57,8 +57,12 @@ def main():
     lib.smoe_set_option(key, old)
     times = [[] for _ in vals]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for _ in range(a.rounds):
-        for i, g in enumerate(graphs):
+    for r in range(a.rounds):
+        order = list(range(len(graphs)))
+        if r % 2:
+            order.reverse()                 # ABBA...: cancels drift within a round
+        for i in order:
+            g = graphs[i]
             for _ in range(3):
                 g.replay()
             e0.record()
