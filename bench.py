@@ -584,7 +584,7 @@ def main():
     # shards span processes)
     launches_per_step = 2 + 1 + 1 + 2 + 1 + 2 + 1 + (6 if world > 1 else 0)
     traffic = None
-    tf = ROOT / "profiles" / "r1_traffic.json"
+    tf = ROOT / "profiles" / "r2" / "traffic.json"
     if tf.exists():
         t_info = json.loads(tf.read_text())
         c = t_info["config"]
