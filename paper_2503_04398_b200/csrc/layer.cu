@@ -32,6 +32,7 @@ struct smoe_layer {
   int32_t* slot_owner_d = nullptr;   // [N]
   int32_t* slot_first_d = nullptr;   // [G + 1]
   int32_t* ready_d = nullptr;        // [kMaxExperts] up-tile counts (early down GEMM)
+  bool ready_armed = false;          // the last EXPERT_UP launch publishes them
   int32_t local_slots = 0;           // expert slots owned by the resident shards
   // weights
   const void* w_gate = nullptr;
@@ -484,7 +485,8 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       a.c = static_cast<char*>(L->buf[SMOE_BUF_HMID][0]);
       a.ldc = c.ffn;
       a.b_tiled = L->w_tiled;
-      if (early_down(L, n)) {
+      L->ready_armed = early_down(L, n);
+      if (L->ready_armed) {
         SMOE_CUDA_TRY(cudaMemsetAsync(L->ready_d, 0, sizeof(int32_t) * L->local_slots, st));
         a.ready = L->ready_d;
         a.ready_role = 1;
@@ -510,13 +512,16 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       // average): one SM per tile streams w2 in a single wave; the SM pair's
       // second, partial wave costs 5-16% there (profiles/r1_down_cta_group_small.jsonl)
       const bool small = decode_batch(L, n);
-      if (early_down(L, n)) {
+      // only behind an up GEMM that publishes this forward's counts (the
+      // option could have changed between the two stage calls)
+      if (L->ready_armed && early_down(L, n)) {
         a.ready = L->ready_d;
         a.ready_role = 2;
         a.ready_up_tile_m = kGemmBM;
         a.ready_up_n_tiles = 2 * c.ffn / kGemmBN;
         a.err = err;
       }
+      L->ready_armed = false;
       rc = narrow_gemm(L, n)
                ? launch_grouped_gemm(L->map_h_narrow, L->map_w2_single, a, kEpiScatter, 0, st)
            : small ? launch_grouped_gemm(L->map_h, L->map_w2_single, a, kEpiScatter, 1, st)

@@ -427,3 +427,50 @@ def test_programmatic_dependent_launch_is_bit_identical(stages):
     finally:
         N.check(lib.smoe_set_option(N.OPT_PDL, old[0]), "opt")
         N.check(lib.smoe_set_option(N.OPT_PDL_STAGES, old[1]), "opt")
+
+
+@pytest.mark.parametrize("toggle", ["off_on", "on_off", "steady"])
+def test_early_down_gemm_bit_identical(toggle):
+    """SMOE_OPT_EARLY_DOWN (decode-sized batches: the down GEMM starts on the
+    SMs the up GEMM's tail frees and waits per expert on counters the up
+    GEMM's epilogue publishes) changes only when tiles start: outputs match
+    the plain launch bit for bit, eager and graph-replayed -- also when the
+    option flips between the EXPERT_UP and EXPERT_DOWN stage calls (the down
+    GEMM only waits behind an up GEMM that published this forward's counts)."""
+    from paper_2503_04398_b200 import _native as N
+    lib = N.lib()
+    over = {"G": 8, "N": 64, "k": 6, "d": 512, "f": 256}
+    n = 64
+    w = synth.make_workload("toy", n=n, eps=0.3, seed=23, cfg_override=over, device=True)
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=6, max_tokens=n)
+    layer.partial_views(n).copy_(w.partials)
+    tok = torch.as_tensor(w.tokens, device="cuda")
+    hist = torch.as_tensor(w.hist, device="cuda")
+    old = lib.smoe_get_option(N.OPT_EARLY_DOWN)
+    try:
+        N.check(lib.smoe_set_option(N.OPT_EARLY_DOWN, 0), "opt")
+        layer.run_device(tok, hist)
+        torch.cuda.synchronize()
+        layer.check_errors()
+        want = layer.out_view(n).clone()
+        up = list(range(N.STAGE_NAMES.index("expert_up") + 1))
+        down = list(range(up[-1] + 1, len(N.STAGE_NAMES)))
+        first, second = {"off_on": (0, 1), "on_off": (1, 0), "steady": (1, 1)}[toggle]
+        for _ in range(2):
+            layer.out_view(n).zero_()
+            N.check(lib.smoe_set_option(N.OPT_EARLY_DOWN, first), "opt")
+            layer.run_device(tok, hist, stages=up)
+            N.check(lib.smoe_set_option(N.OPT_EARLY_DOWN, second), "opt")
+            layer.run_device(tok, hist, stages=down)
+            torch.cuda.synchronize()
+            layer.check_errors()
+            assert torch.equal(layer.out_view(n), want)
+        N.check(lib.smoe_set_option(N.OPT_EARLY_DOWN, 1), "opt")
+        g = layer.capture(tok, hist)
+        layer.out_view(n).zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        layer.check_errors()
+        assert torch.equal(layer.out_view(n), want)
+    finally:
+        N.check(lib.smoe_set_option(N.OPT_EARLY_DOWN, old), "opt")
