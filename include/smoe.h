@@ -59,7 +59,7 @@ const char* smoe_version(void);
 #define SMOE_OPT_GATE_TENSOR         2  /* layer gate: 1 = tcgen05 kernel (default), */
                                         /* 0 = mma.sync / CUDA-core kernels          */
 #define SMOE_OPT_GEMM_PAIR_MIN_ROWS  3  /* layer down GEMM: one SM per tile while    */
-                                        /* n*k <= this * n_experts (default 64)      */
+                                        /* n*k <= this * n_experts (default 1024)    */
 #define SMOE_OPT_PDL                 4  /* layer kernels: 1 = programmatic dependent */
                                         /* launch (default; env SMOE_PDL=0 to start  */
                                         /* with 0), 0 = plain stream order           */

@@ -518,8 +518,19 @@ static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
 static int g_cta_group[2] = {1, 2};
 
 int gemm_cta_group(int which) { return g_cta_group[which ? 1 : 0]; }
-static int g_pair_min_rows = 64;
-int gemm_pair_min_rows() { return g_pair_min_rows; }
+// -1: env SMOE_GEMM_PAIR_MIN_ROWS, else 1024.  The SM pair's 256-row tiles
+// pad half a tile per expert on average (one SM: half of 128 rows); below
+// ~1k routed rows per expert that padding outweighs the pair's ~10% MMA
+// advantage (DeepSeek-V2 16K, 614 rows: down GEMM 1.48 -> 1.34 ms on one SM,
+// profiles/r2/down_gemm/pair_min_rows_ab.jsonl; decode sizes: 5-16%)
+static int g_pair_min_rows = -1;
+int gemm_pair_min_rows() {
+  if (g_pair_min_rows < 0) {
+    const char* e = getenv("SMOE_GEMM_PAIR_MIN_ROWS");
+    g_pair_min_rows = (e && atoi(e) >= 0) ? atoi(e) : 1024;
+  }
+  return g_pair_min_rows;
+}
 void set_gemm_pair_min_rows(int rows) { g_pair_min_rows = rows; }
 void set_gemm_cta_group(int which, int cg) { g_cta_group[which ? 1 : 0] = (cg == 2) ? 2 : 1; }
 int gemm_b_box_rows(int cg) { return kGemmBN / cg; }

@@ -334,17 +334,17 @@ static bool narrow_gemm(const smoe_layer* L, int64_t n) {
          n * (int64_t)c.top_k <= (int64_t)gemm_narrow_max_rows() * c.n_experts;
 }
 
-// decode-sized batch: at most gemm_pair_min_rows() routed rows per expert on
-// average (the layer's down GEMM then runs one SM per tile, see EXPERT_DOWN)
-static bool decode_batch(const smoe_layer* L, int64_t n) {
+// at most gemm_pair_min_rows() routed rows per expert on average: the layer's
+// down GEMM runs one SM per 128-row tile (see EXPERT_DOWN)
+static bool down_single_sm(const smoe_layer* L, int64_t n) {
   return n * (int64_t)L->cfg.top_k <= (int64_t)gemm_pair_min_rows() * L->cfg.n_experts;
 }
 
-// decode-sized batch whose down GEMM starts early (SMOE_OPT_EARLY_DOWN): both
-// GEMMs one SM per 128-row tile, the down GEMM launched under PDL
+// down GEMM started early (SMOE_OPT_EARLY_DOWN): both GEMMs one SM per
+// 128-row tile, the down GEMM launched under PDL
 static bool early_down(const smoe_layer* L, int64_t n) {
   // (pdl_enabled() answers for the stage being launched: ask for the down GEMM's)
-  return gemm_early_down() && decode_batch(L, n) && !narrow_gemm(L, n) && L->maps_cg_up == 1 &&
+  return gemm_early_down() && down_single_sm(L, n) && !narrow_gemm(L, n) && L->maps_cg_up == 1 &&
          pdl_stage_enabled(SMOE_STAGE_EXPERT_DOWN);
 }
 
@@ -508,10 +508,11 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       for (int g = 0; g < c.n_shards; ++g) a.dst_base[g] = static_cast<char*>(L->buf[SMOE_BUF_YPAIR][g]);
       a.ldd = c.hidden;
       a.b_tiled = L->w_tiled;
-      // decode-sized batches (<= gemm_pair_min_rows() routed rows per expert on
-      // average): one SM per tile streams w2 in a single wave; the SM pair's
-      // second, partial wave costs 5-16% there (profiles/r1_down_cta_group_small.jsonl)
-      const bool small = decode_batch(L, n);
+      // <= gemm_pair_min_rows() routed rows per expert on average: one SM
+      // per tile (decode sizes: one wave instead of the pair's 1.7, 5-16%,
+      // profiles/r1_down_cta_group_small.jsonl; mid sizes: half the padding
+      // rows of the pair's 256-row tiles)
+      const bool small = down_single_sm(L, n);
       // only behind an up GEMM that publishes this forward's counts (the
       // option could have changed between the two stage calls)
       if (L->ready_armed && early_down(L, n)) {
