@@ -66,12 +66,30 @@ def to_host_like(y, like):
     return y.cpu().numpy()
 
 
-class ErrFlag:
-    """Device int32 error flag read back after a call (one small D2H)."""
+# Deferred error mode (scheduler.defer_errors): every call ORs its error bits
+# into one sticky device flag per device instead of its own, and nothing is
+# read back until scheduler.check_errors() -- no host synchronisation per call.
+_DEFER = {"on": False, "flags": {}}
 
-    def __init__(self):
+
+def sticky_flag():
+    t = torch()
+    dev = device()
+    f = _DEFER["flags"].get(str(dev))
+    if f is None:
+        f = t.zeros(1, dtype=t.int32, device=dev)
+        _DEFER["flags"][str(dev)] = f
+    return f
+
+
+class ErrFlag:
+    """Device int32 error flag read back after a call (one small D2H), or, in
+    deferred mode, a view of the sticky per-device flag."""
+
+    def __init__(self, allow_defer: bool = False):
         t = torch()
-        self.t = t.zeros(1, dtype=t.int32, device=device())
+        self.deferred = allow_defer and _DEFER["on"]
+        self.t = sticky_flag() if self.deferred else t.zeros(1, dtype=t.int32, device=device())
 
     @property
     def ptr(self) -> int:

@@ -139,6 +139,41 @@ def device_tables(bundle) -> DeviceTables:
     return dt
 
 
+def defer_errors(on: bool = True):
+    """Deferred error reporting for device-resident callers: while on, the
+    scheduler functions do not read their error flag back after each call
+    (which synchronises the host with the device); the kernels OR their bits
+    into a sticky per-device flag that `check_errors()` reads, resets and
+    raises from (SchedulerError / IndexError, as the immediate mode would).
+    rebatch_tokens still synchronises: its output size depends on the
+    device-computed group size (scheduler.py:136).  Usable as a context
+    manager: `with defer_errors(): ...; check_errors()`."""
+    prev = _dev._DEFER["on"]
+    _dev._DEFER["on"] = bool(on)
+
+    class _Ctx:
+        def __enter__(self):
+            return self
+
+        def __exit__(self, *exc):
+            _dev._DEFER["on"] = prev
+            return False
+    return _Ctx()
+
+
+def check_errors() -> None:
+    """Raise (and clear) the errors accumulated in deferred mode."""
+    f = _dev.sticky_flag()
+    bits = int(f.item())
+    f.zero_()
+    _raise_for(bits)
+
+
+def _check(err) -> None:
+    if not err.deferred:
+        _raise_for(err.bits())
+
+
 def _raise_for(bits: int, index_msg: str = "index out of range") -> None:
     if bits & _native.ERRBIT_DEVICE_RANGE:
         raise SchedulerError("device label out of range")
@@ -169,13 +204,13 @@ def lookup_devices(bundle, tokens, histories):
         hist_len = int(hist.shape[1])
     if n == 0:
         return _dev.to_host_like(out, tokens)
-    err = _dev.ErrFlag()
+    err = _dev.ErrFlag(allow_defer=True)
     _native.check(L.smoe_lookup_devices(
         _native.ptr(tok), n, _native.ptr(hist), hist_len, _native.ptr(tabs.t_labels),
         _native.ptr(tabs.t_conf), tabs.vocab, _native.ptr(tabs.a_best), _native.ptr(tabs.a_conf),
         tabs.a_rows, tabs.n_clusters, _native.ptr(out), err.ptr, _native.stream_ptr()),
         "lookup_devices")
-    _raise_for(err.bits())
+    _check(err)
     return _dev.to_host_like(out, tokens)
 
 
@@ -210,12 +245,12 @@ class _Plan:
         self.group_t = t.empty(1, dtype=t.int64, device=dev)
         ws_bytes = int(L.smoe_plan_workspace_bytes(n, n_devices))
         ws = t.empty(ws_bytes, dtype=t.uint8, device=dev)
-        err = _dev.ErrFlag()
+        err = _dev.ErrFlag(allow_defer=True)
         _native.check(L.smoe_rebatch_plan(
             _native.ptr(devices_t), n, n_devices, _native.ptr(self.forward),
             _native.ptr(self.inverse), _native.ptr(self.counts), _native.ptr(self.group_t),
             err.ptr, _native.ptr(ws), ws_bytes, _native.stream_ptr()), "rebatch_tokens")
-        _raise_for(err.bits())
+        _check(err)
         self.group = int(self.group_t.item())
         self.forward = self.forward[: n_devices * self.group]
 
@@ -232,12 +267,12 @@ def _gather(src_t, idx_t, pad_negative: bool, pad_value: int):
     if n_out == 0 or row_elems == 0:
         return out
     esz = src_t.element_size()
-    err = _dev.ErrFlag()
+    err = _dev.ErrFlag(allow_defer=True)
     _native.check(L.smoe_gather_rows(
         _native.ptr(src_t), src_t.shape[0], esz, row_elems, _native.ptr(idx_t), n_out,
         1 if pad_negative else 0, int(pad_value), _native.ptr(out), err.ptr,
         _native.stream_ptr()), "gather_rows")
-    _raise_for(err.bits())
+    _check(err)
     return out
 
 
@@ -305,11 +340,11 @@ def gate_permutation(expert_labels, n_clusters: int) -> GatePermutation:
     N = lab.numel()
     n2o = t.empty(N, dtype=t.int64, device=lab.device)
     o2n = t.empty(N, dtype=t.int64, device=lab.device)
-    err = _dev.ErrFlag()
+    err = _dev.ErrFlag(allow_defer=True)
     _native.check(L.smoe_gate_permutation(_native.ptr(lab), N, int(n_clusters), _native.ptr(n2o),
                                           _native.ptr(o2n), err.ptr, _native.stream_ptr()),
                   "gate_permutation")
-    _raise_for(err.bits())
+    _check(err)
     return GatePermutation(new_to_old=_dev.to_host_like(n2o, expert_labels),
                            old_to_new=_dev.to_host_like(o2n, expert_labels),
                            n_clusters=n_clusters)
@@ -338,11 +373,11 @@ def remap_topk(topk_experts, perm: GatePermutation):
     idx = _dev.to_device(topk_experts, t.int64)
     table = _dev.to_device(perm.old_to_new, t.int64)
     out = t.empty_like(idx)
-    err = _dev.ErrFlag()
+    err = _dev.ErrFlag(allow_defer=True)
     _native.check(L.smoe_remap_index(_native.ptr(idx), idx.numel(), _native.ptr(table),
                                      table.numel(), _native.ptr(out), err.ptr,
                                      _native.stream_ptr()), "remap_topk")
-    _raise_for(err.bits())
+    _check(err)
     return _dev.to_host_like(out, topk_experts)
 
 

@@ -68,6 +68,30 @@ def test_lookup_index_errors():
         S.lookup_devices(b, np.array([1]), np.array([[4, 4, 4]]))   # row 84 >= 16
 
 
+def test_deferred_errors_for_device_callers():
+    """defer_errors(): no per-call error read-back (host sync); the bits
+    accumulate on the device and check_errors() raises the same exception
+    class the immediate mode would, then clears them."""
+    import torch
+    rng = np.random.default_rng(3)
+    b = make_bundle(rng, 4, 10)
+    good = torch.tensor([1, 2, 3], device="cuda")
+    bad = torch.tensor([1, 10], device="cuda")           # token id >= vocab
+    with S.defer_errors():
+        out = S.lookup_devices(b, good, None)
+        S.lookup_devices(b, bad, None)                   # no exception here
+        assert out.is_cuda and out.shape == (3,)
+        with pytest.raises(IndexError):
+            S.check_errors()
+        S.check_errors()                                 # cleared
+        devs = torch.tensor([0, 5, 1], device="cuda")     # device label >= G
+        S.rebatch_tokens(good, devs, 4)
+        with pytest.raises(S.SchedulerError):
+            S.check_errors()
+    with pytest.raises(IndexError):                       # immediate mode again
+        S.lookup_devices(b, bad, None)
+
+
 def test_rebatch_golden():
     # test_scheduler.py:57-63 and :66-72
     sh, ix = S.rebatch_tokens(np.array([10, 11, 12, 13, 14]), np.array([1, 0, 1, 1, 0]), 2)
