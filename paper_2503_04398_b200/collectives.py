@@ -36,8 +36,10 @@ def _plan_tensors(indices: ShuffleIndices):
     fwd = fwd.to(t.int64).contiguous()
     if fwd.numel() < G * group:
         raise SchedulerError("forward index shorter than n_devices * group_size")
-    counts = (fwd[: G * group].view(G, group) >= 0).sum(1).to(t.int32) if group else \
-        t.zeros(G, dtype=t.int32, device=fwd.device)
+    counts = getattr(indices, "_counts_t", None)      # set by rebatch_tokens (device)
+    if counts is None or counts.numel() != G:
+        counts = (fwd[: G * group].view(G, group) >= 0).sum(1).to(t.int32) if group else \
+            t.zeros(G, dtype=t.int32, device=fwd.device)
     group_t = t.full((1,), group, dtype=t.int64, device=fwd.device)
     return fwd, counts, group_t, G, group
 

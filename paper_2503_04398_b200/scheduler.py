@@ -300,6 +300,9 @@ def rebatch_tokens(tokens, devices, n_devices: int):
     if as_torch:
         idx = ShuffleIndices(forward=plan.forward, inverse=plan.inverse,
                              group_size=plan.group, n_devices=int(n_devices))
+        # the plan kernel's per-group counts ride along for the standalone
+        # collectives (collectives._plan_tensors), so they need no recount
+        object.__setattr__(idx, "_counts_t", plan.counts)
         return shuffled, idx
     idx = ShuffleIndices(forward=plan.forward.cpu().numpy(), inverse=plan.inverse.cpu().numpy(),
                          group_size=plan.group, n_devices=int(n_devices))
