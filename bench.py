@@ -360,18 +360,45 @@ def main():
     barrier()
     ms_total = start.elapsed_time(end)
     # the per-stage breakdown (and the roofline's kernel times): a second pass
-    # with an event after every stage (events between stages stop the next
-    # stage from launching early, so these sum to a little more than the step)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(NS + 1)] for _ in range(args.steps)]
-    barrier()
-    torch.cuda.synchronize()
-    for s in range(args.steps):
-        ev[s][0].record(stream)
-        for j in range(NS):                 # one stage per launch group, event after each
-            layer.run_device(tok, hist, stages=[j])
-            ev[s][j + 1].record(stream)
-    torch.cuda.synchronize()
-    barrier()
+    # of K forwards with an event after every stage, captured as ONE CUDA
+    # graph (external event nodes) and replayed, so the host's per-stage
+    # launch path adds no gaps; events between stages still stop the next
+    # stage from launching early, so the stages sum to a little more than the
+    # step.  Eager fallback if the capture fails.
+    def staged_pass(steps):
+        evs = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(NS + 1)]
+               for _ in range(steps)]
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                cs = torch.cuda.current_stream()
+                for s_ in range(steps):
+                    evs[s_][0].record(cs)
+                    for j in range(NS):
+                        layer.run_device(tok, hist, stages=[j])
+                        evs[s_][j + 1].record(cs)
+            barrier()
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            barrier()
+            del g
+            return evs, "cuda-graph replay, external event nodes between stages"
+        except Exception:                   # eager: the same pass from the host
+            evs = [[torch.cuda.Event(enable_timing=True) for _ in range(NS + 1)]
+                   for _ in range(steps)]
+            barrier()
+            torch.cuda.synchronize()
+            for s_ in range(steps):
+                evs[s_][0].record(stream)
+                for j in range(NS):
+                    layer.run_device(tok, hist, stages=[j])
+                    evs[s_][j + 1].record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            return evs, "eager, events between stages"
+
+    ev, stage_timing = staged_pass(args.steps)
     stage_ms = {nm: float(np.mean([ev[s][j].elapsed_time(ev[s][j + 1]) for s in range(args.steps)]))
                 for j, nm in enumerate(N.STAGE_NAMES)}
     up_ms, down_ms = stage_ms["expert_up"], stage_ms["expert_down"]
@@ -605,7 +632,8 @@ def main():
               "local_activation_rate": st["measured_alpha"],
               "a2a_bytes_per_step": st["bytes"]["a2a_dispatch"] + st["bytes"]["a2a_combine"],
               "stage_bytes": st["bytes"], "group_size": st["group_size"],
-              "stages_ms": stage_ms, "stages_roofline": stages_rf,
+              "stages_ms": stage_ms, "stages_timing": stage_timing,
+              "stages_roofline": stages_rf,
               "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel<SwiGLU> (expert up)",
                            "achieved": achieved, "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
                            "frac": achieved / pk["bf16_sustained"], "traffic": traffic,
