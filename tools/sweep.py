@@ -98,7 +98,17 @@ def main():
                     help="interleaved 1 vs 2 vs 4 micro-batches on the main configs")
     ap.add_argument("--gate-ab", action="store_true",
                     help="interleaved tcgen05 gate vs mma.sync gate (SMOE_OPT_GATE_TENSOR)")
+    ap.add_argument("--batch-sweep", action="store_true",
+                    help="configs x 64 ... 65536 tokens (the DESIGN batch table)")
     args = ap.parse_args()
+    if args.batch_sweep:
+        for name, ep in (("mixtral", None), ("dsv2_lite", None), ("qwen2_57b", 8)):
+            for tok in (64, 512, 2048, 8192, 16384, 65536):
+                print(json.dumps(measure(name, tok, 0.2, ep)), flush=True)
+        for ep in (4, 2):
+            for tok in (2048, 16384):
+                print(json.dumps(measure("qwen2_57b", tok, 0.2, ep)), flush=True)
+        return
     if args.gate_ab:
         from paper_2503_04398_b200 import _native as N
         lib = N.lib()
