@@ -535,14 +535,15 @@ void set_gemm_pair_min_rows(int rows) { g_pair_min_rows = rows; }
 void set_gemm_cta_group(int which, int cg) { g_cta_group[which ? 1 : 0] = (cg == 2) ? 2 : 1; }
 int gemm_b_box_rows(int cg) { return kGemmBN / cg; }
 
-// -1: not set yet (env SMOE_GEMM_NARROW_MAX_ROWS, else 0 = off).  Off by
-// default: the narrow variant wins only while the expert-input buffer's
-// unused rows are zero (a fresh layer); in steady-state serving it measured
-// neutral to 3% slower under the power cap (profiles/r1_narrow/).
+// SMOE_OPT_EARLY_DOWN (see GemmArgs::ready)
 static int g_early_down = 1;
 int gemm_early_down() { return g_early_down; }
 void set_gemm_early_down(int on) { g_early_down = on ? 1 : 0; }
 
+// -1: not set yet (env SMOE_GEMM_NARROW_MAX_ROWS, else 0 = off).  Off by
+// default: the narrow variant wins only while the expert-input buffer's
+// unused rows are zero (a fresh layer); in steady-state serving it measured
+// neutral to 3% slower under the power cap (profiles/r1_narrow/).
 static int g_narrow_max_rows = -1;
 int gemm_narrow_max_rows() {
   if (g_narrow_max_rows < 0) {
