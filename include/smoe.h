@@ -77,6 +77,10 @@ const char* smoe_version(void);
                                         /* CTAs start on the SMs the up GEMM's     */
                                         /* tail frees and wait per expert for its  */
                                         /* hidden rows (1 = default, 0 = off)      */
+#define SMOE_OPT_ROUTE_IN_GATE       9  /* batches of <= 128 tokens: the tcgen05   */
+                                        /* gate ranks each shard's pairs and       */
+                                        /* publishes its count row (no route       */
+                                        /* kernel; 1 = default, 0 = off)           */
 int smoe_set_option(int32_t key, int32_t value);
 int smoe_get_option(int32_t key);
 const char* smoe_status_string(int status);

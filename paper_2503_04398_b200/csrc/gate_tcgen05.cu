@@ -211,7 +211,20 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
     blk = t - s_prefix[gl];
   };
 
-  if (warp == 0) {
+  if (warp == 3) {
+    // fused route: shards without rows have no tile -- CTA 0's idle warp
+    // publishes their zero rows of the count matrix
+    if (a.route && blockIdx.x == 0) {
+      const int32_t Nn = a.n_experts;
+      for (int gl = 0; gl < a.shard_count; ++gl) {
+        if (s_cnt[gl] != 0) continue;
+        const int64_t g = a.shard_begin + gl;
+        for (int e = lane; e < Nn; e += 32)
+          for (int i = 0; i < a.n_count_bufs; ++i)
+            reinterpret_cast<int32_t*>(a.count_bufs.p[i])[g * Nn + e] = 0;
+      }
+    }
+  } else if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer =====
       int32_t stage = 0;
@@ -594,6 +607,52 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
                 my_remote);
       atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + SMOE_STAT_REMOTE_ROWS), my_rrows);
     }
+    if (a.route && (int32_t)blockIdx.x < total && hf == 0) {
+      // ===== fused route (decode-sized batches: this CTA's one tile is all
+      // of its shard's rows): stable rank of every pair among the shard's
+      // pairs of its expert, in pair order p = row * k + s, 128 pairs per
+      // round (match_any ranks inside a warp, per-warp counts in shared
+      // memory) -- the route_rank_kernel result without its launch.  The
+      // ring's shared memory is idle now (its only tile is consumed).
+      int32_t gl, blk;
+      decode(blockIdx.x, gl, blk);
+      const int32_t Nn = a.n_experts;
+      const int tid_e = ew * 32 + lane;
+      int32_t* s_w = reinterpret_cast<int32_t*>(smem_h);    // [4][Nn] counts per warp
+      int32_t* s_pre = s_w + 4 * Nn;                         // [Nn] earlier rounds' counts
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      for (int e = tid_e; e < 5 * Nn; e += 128) s_w[e] = 0;
+      asm volatile("bar.sync 5, 128;" ::: "memory");         // + this tile's ids stored
+      const int64_t P = (int64_t)s_cnt[gl] * K;
+      const int32_t* ids = reinterpret_cast<const int32_t*>(s_ids[gl]);
+      int32_t* rank = reinterpret_cast<int32_t*>(a.pair_rank.p[gl]);
+      for (int64_t c0 = 0; c0 < P; c0 += 128) {
+        const int64_t p = c0 + tid_e;
+        const int32_t e = p < P ? ids[p] : -1;
+        const uint32_t peers = __match_any_sync(0xffffffffu, e);
+        const int32_t rw = __popc(peers & lanemask_lt());
+        if (e >= 0 && lane == __ffs(peers) - 1) s_w[ew * Nn + e] = __popc(peers);
+        asm volatile("bar.sync 5, 128;" ::: "memory");
+        if (e >= 0) {
+          int32_t r = s_pre[e] + rw;
+          for (int w = 0; w < ew; ++w) r += s_w[w * Nn + e];
+          rank[p] = r;
+        }
+        asm volatile("bar.sync 5, 128;" ::: "memory");
+        for (int ee = tid_e; ee < Nn; ee += 128) {
+          int32_t sum = 0;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) { sum += s_w[w * Nn + ee]; s_w[w * Nn + ee] = 0; }
+          s_pre[ee] += sum;
+        }
+        asm volatile("bar.sync 5, 128;" ::: "memory");
+      }
+      // the shard's row of the [G, N] count matrix, to every process
+      const int64_t g = a.shard_begin + gl;
+      for (int ee = tid_e; ee < Nn; ee += 128)
+        for (int i = 0; i < a.n_count_bufs; ++i)
+          reinterpret_cast<int32_t*>(a.count_bufs.p[i])[g * Nn + ee] = s_pre[ee];
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -653,6 +712,10 @@ static int launch_np(const CUtensorMap& mh, const CUtensorMap& mw, const GateTcA
     }
   }
 }
+
+static int g_route_fused = 1;
+int gate_route_fused() { return g_route_fused; }
+void set_gate_route_fused(int on) { g_route_fused = on ? 1 : 0; }
 
 static int g_gate_tc = 1;
 int gate_tc_enabled() { return g_gate_tc; }

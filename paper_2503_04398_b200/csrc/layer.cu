@@ -33,6 +33,7 @@ struct smoe_layer {
   int32_t* slot_first_d = nullptr;   // [G + 1]
   int32_t* ready_d = nullptr;        // [kMaxExperts] up-tile counts (early down GEMM)
   bool ready_armed = false;          // the last EXPERT_UP launch publishes them
+  bool route_fused = false;          // the last GATE launch also ran the route
   int32_t local_slots = 0;           // expert slots owned by the resident shards
   // weights
   const void* w_gate = nullptr;
@@ -438,13 +439,27 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
         g.topk_ids = local_ptrs(L, SMOE_BUF_TOPK_IDS);
         g.topk_w = local_ptrs(L, SMOE_BUF_TOPK_W);
         g.stats = stats;
+        // decode-sized batches (n <= 128: every shard's rows are one gate
+        // tile): the gate CTA of each shard also ranks its pairs and
+        // publishes its count row -- the ROUTE stage then only barriers
+        L->route_fused = gate_route_fused() && n > 0 && n <= 128;
+        if (L->route_fused) {
+          g.route = 1;
+          g.pair_rank = local_ptrs(L, SMOE_BUF_PAIR_RANK);
+          g.count_bufs = distinct_ptrs(L, SMOE_BUF_COUNTS, &g.n_count_bufs);
+        }
         return launch_gate_tc(L->map_hs, L->map_wg, g, n, st);
       }
+      L->route_fused = false;
       return launch_gate(lr, local_ptrs(L, SMOE_BUF_HS), c.hidden, L->w_gate, L->b_gate,
                          c.n_experts, c.top_k, c.renormalize, L->slot_owner_d,
                          local_ptrs(L, SMOE_BUF_TOPK_IDS), local_ptrs(L, SMOE_BUF_TOPK_W), stats,
                          n, st);
     case SMOE_STAGE_ROUTE: {
+      if (L->route_fused) {               // done by the gate kernel of this forward
+        L->route_fused = false;
+        return smoe_layer_barrier(L, stream);
+      }
       int32_t nb = 0;
       ShardPtrs cb = distinct_ptrs(L, SMOE_BUF_COUNTS, &nb);
       int32_t* chunk_counts = reinterpret_cast<int32_t*>(
@@ -652,6 +667,10 @@ extern "C" int smoe_set_option(int32_t key, int32_t value) {
       if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
       set_gemm_early_down(value);
       return SMOE_OK;
+    case SMOE_OPT_ROUTE_IN_GATE:
+      if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
+      set_gate_route_fused(value);
+      return SMOE_OK;
     case SMOE_OPT_PDL:
       if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
       set_pdl_enabled(value);
@@ -675,6 +694,7 @@ extern "C" int smoe_get_option(int32_t key) {
   if (key == SMOE_OPT_PDL_STAGES) return pdl_stage_mask();
   if (key == SMOE_OPT_DEDUP_DISPATCH) return g_dedup_dispatch;
   if (key == SMOE_OPT_EARLY_DOWN) return gemm_early_down();
+  if (key == SMOE_OPT_ROUTE_IN_GATE) return gate_route_fused();
   return -1;
 }
 

@@ -47,8 +47,18 @@ struct GateTcArgs {
   const int32_t* slot_owner;
   ShardPtrs topk_ids, topk_w;
   int64_t* stats;
+  // route fused into the gate (every shard's rows fit one tile, so a CTA
+  // holds all pairs of its shard): stable pair ranks per expert and the
+  // shard's row of the [G, N] count matrix, as route_rank_kernel computes
+  // them, written to every process's count buffer
+  int32_t route;
+  ShardPtrs pair_rank;       // per resident shard [n, k]
+  ShardPtrs count_bufs;      // one [G, N] int32 matrix per process
+  int32_t n_count_bufs;
 };
 bool gate_tc_supported(int32_t n_experts, int32_t top_k, int64_t d);
+int gate_route_fused();               // SMOE_OPT_ROUTE_IN_GATE
+void set_gate_route_fused(int on);
 int gate_tc_enabled();                 // SMOE_OPT_GATE_TENSOR
 void set_gate_tc_enabled(int on);
 int gate_tc_rows(int32_t n_experts);   // W box rows (N rounded up to 16)
