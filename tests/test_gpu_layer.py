@@ -474,3 +474,37 @@ def test_early_down_gemm_bit_identical(toggle):
         assert torch.equal(layer.out_view(n), want)
     finally:
         N.check(lib.smoe_set_option(N.OPT_EARLY_DOWN, old), "opt")
+
+
+@pytest.mark.parametrize("n,over", [(64, {"G": 8, "N": 64, "k": 6, "d": 512, "f": 256}),
+                                    (100, {"G": 4, "N": 160, "k": 6, "d": 256, "f": 256}),
+                                    (7, {"G": 16, "N": 16, "k": 2, "d": 256, "f": 256})])
+def test_route_in_gate_bit_identical(n, over):
+    """SMOE_OPT_ROUTE_IN_GATE (batches of <= 128 tokens: the gate ranks each
+    shard's pairs and publishes its count row, the route kernel is skipped)
+    gives the same outputs, pair counts and statistics as the route kernel --
+    also with shards that receive no token (G = 16, 7 tokens)."""
+    from paper_2503_04398_b200 import _native as N
+    lib = N.lib()
+    w = synth.make_workload("toy", n=n, eps=0.3, seed=29, cfg_override=over, device=True)
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=over["k"], max_tokens=n)
+    layer.partial_views(n).copy_(w.partials)
+    tok = torch.as_tensor(w.tokens, device="cuda")
+    hist = torch.as_tensor(w.hist, device="cuda")
+    old = lib.smoe_get_option(N.OPT_ROUTE_IN_GATE)
+    res = []
+    try:
+        for v in (0, 1):
+            N.check(lib.smoe_set_option(N.OPT_ROUTE_IN_GATE, v), "opt")
+            layer.counts_mat.fill_(-1)
+            layer.run_device(tok, hist)
+            torch.cuda.synchronize()
+            layer.check_errors()
+            st = layer.stats(n)
+            res.append((layer.out_view(n).clone(), st["pair_counts"], st["local_tokens"],
+                        st["remote_tokens"], layer.routing(n)["experts"]))
+    finally:
+        N.check(lib.smoe_set_option(N.OPT_ROUTE_IN_GATE, old), "opt")
+    assert torch.equal(res[0][0], res[1][0])
+    assert res[0][1] == res[1][1] and res[0][2:4] == res[1][2:4]
+    assert np.array_equal(res[0][4], res[1][4])
