@@ -25,10 +25,12 @@ def free_port():
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("world,over", [(2, {"G": 2, "N": 8}), (2, {"G": 4, "N": 16}),
-                                        (4, {"G": 8, "N": 16}), (8, {"G": 8, "N": 16})])
-def test_two_process_layer_matches_single_process(world, over):
-    n = 300
+@pytest.mark.parametrize("world,over,n", [(2, {"G": 2, "N": 8}, 300), (2, {"G": 4, "N": 16}, 300),
+                                          (4, {"G": 8, "N": 16}, 300), (8, {"G": 8, "N": 16}, 300),
+                                          # decode sizes: route fused into the gate (count rows
+                                          # pushed to every process), early-started down GEMM
+                                          (2, {"G": 4, "N": 16}, 100), (4, {"G": 8, "N": 16}, 64)])
+def test_two_process_layer_matches_single_process(world, over, n):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
