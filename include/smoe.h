@@ -81,6 +81,9 @@ const char* smoe_version(void);
                                         /* gate ranks each shard's pairs and       */
                                         /* publishes its count row (no route       */
                                         /* kernel; 1 = default, 0 = off)           */
+#define SMOE_OPT_GEMM_GROUP_M_UP    10  /* tile order of the layer's up / down GEMM: */
+#define SMOE_OPT_GEMM_GROUP_M_DOWN  11  /* 0 = derived (default), > 0 m-blocks per   */
+                                        /* group, < 0 -(n-blocks per group)          */
 int smoe_set_option(int32_t key, int32_t value);
 int smoe_get_option(int32_t key);
 const char* smoe_status_string(int status);

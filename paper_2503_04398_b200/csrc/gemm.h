@@ -73,6 +73,12 @@ void set_gemm_narrow_max_rows(int rows);
 
 // cg: 1 = one SM per 128x256 tile, 2 = SM pair per 256x256 tile, 0 = one SM
 // per 32x256 tile (narrow; tmap_a must have kGemmNarrowM-row boxes).
+// Tile order of the up (which = 0) / down (which = 1) GEMM: 0 = derived from
+// K (A-resident groups of m-blocks that fit ~40 MB of L2, else B-resident);
+// > 0: m-blocks per group; < 0: -(n-blocks per group).  SMOE_OPT_GEMM_GROUP_M_*.
+int gemm_group_m(int which);
+void set_gemm_group_m(int which, int v);
+
 // SMOE_OPT_EARLY_DOWN (default 1)
 int gemm_early_down();
 void set_gemm_early_down(int on);

@@ -485,6 +485,8 @@ static int launch_impl(const CUtensorMap& a, const CUtensorMap& b, const GemmArg
     g.group_m = fit >= 8 ? (int32_t)fit : 1;
     const char* e = getenv(EPI == kEpiSwiGLU ? "SMOE_GROUP_M_UP" : "SMOE_GROUP_M_DOWN");
     if (e && atoi(e) != 0) g.group_m = atoi(e);     // tuning experiments (< 0: n-groups)
+    const int opt = gemm_group_m(EPI == kEpiSwiGLU ? 0 : 1);   // SMOE_OPT_GEMM_GROUP_M_*
+    if (opt != 0) g.group_m = opt;
   }
   const int grid = (num_sms() / CG) * CG;
   if (CG == 1) {
@@ -534,6 +536,11 @@ int gemm_pair_min_rows() {
 void set_gemm_pair_min_rows(int rows) { g_pair_min_rows = rows; }
 void set_gemm_cta_group(int which, int cg) { g_cta_group[which ? 1 : 0] = (cg == 2) ? 2 : 1; }
 int gemm_b_box_rows(int cg) { return kGemmBN / cg; }
+
+// SMOE_OPT_GEMM_GROUP_M_UP / _DOWN: tile order override (0 = derived from K)
+static int g_group_m[2] = {0, 0};
+int gemm_group_m(int which) { return g_group_m[which ? 1 : 0]; }
+void set_gemm_group_m(int which, int v) { g_group_m[which ? 1 : 0] = v; }
 
 // SMOE_OPT_EARLY_DOWN (see GemmArgs::ready)
 static int g_early_down = 1;

@@ -45,6 +45,7 @@ struct smoe_layer {
   bool maps_ready = false;
   int maps_cg_up = 0, maps_cg_down = 0;
   CUtensorMap map_x, map_w13, map_h, map_w2;
+  CUtensorMap map_w13_single;        // w13 with one-SM boxes (decode sizes / narrow, see EXPERT_UP)
   CUtensorMap map_w2_single;         // w2 with one-SM boxes (small batches, see EXPERT_DOWN)
   CUtensorMap map_x_narrow, map_h_narrow;   // 32-row A boxes (decode-sized batches)
   // tensor-core gate: hidden rows of the resident shards (one arena) and W_g
@@ -264,6 +265,10 @@ static int ensure_maps(smoe_layer* L) {
                            L->w_tiled ? w13_rows * (c.hidden / kGemmBK) : w13_rows,
                            L->w_tiled ? kGemmBK : c.hidden, gemm_b_box_rows(gemm_cta_group(0)))))
     return rc;
+  if ((rc = make_tmap_bf16(&L->map_w13_single, L->w13,
+                           L->w_tiled ? w13_rows * (c.hidden / kGemmBK) : w13_rows,
+                           L->w_tiled ? kGemmBK : c.hidden, gemm_b_box_rows(1))))
+    return rc;
   if ((rc = make_tmap_bf16(&L->map_h, L->buf[SMOE_BUF_HMID][0], rows, c.ffn, kGemmBM))) return rc;
   if ((rc = make_tmap_bf16(&L->map_x_narrow, L->buf[SMOE_BUF_XIN][c.shard_begin], rows, c.hidden,
                            kGemmNarrowM)))
@@ -341,11 +346,19 @@ static bool down_single_sm(const smoe_layer* L, int64_t n) {
   return n * (int64_t)L->cfg.top_k <= (int64_t)gemm_pair_min_rows() * L->cfg.n_experts;
 }
 
+// cta_group of the up GEMM for this batch: the SM pair only when the option
+// asks for it and the batch is past the one-SM down GEMM's range (decode
+// sizes stream weights; one SM per tile there, and the early down GEMM's
+// readiness counters assume it)
+static int up_cg(const smoe_layer* L, int64_t n) {
+  return (L->maps_cg_up == 2 && !down_single_sm(L, n)) ? 2 : 1;
+}
+
 // down GEMM started early (SMOE_OPT_EARLY_DOWN): both GEMMs one SM per
 // 128-row tile, the down GEMM launched under PDL
 static bool early_down(const smoe_layer* L, int64_t n) {
   // (pdl_enabled() answers for the stage being launched: ask for the down GEMM's)
-  return gemm_early_down() && down_single_sm(L, n) && !narrow_gemm(L, n) && L->maps_cg_up == 1 &&
+  return gemm_early_down() && down_single_sm(L, n) && !narrow_gemm(L, n) && up_cg(L, n) == 1 &&
          pdl_stage_enabled(SMOE_STAGE_EXPERT_DOWN);
 }
 
@@ -508,9 +521,11 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       }
       // decode-sized batches stream the weights: narrow m-blocks keep more
       // weight tiles in flight per SM (gemm_tcgen05.cu, GemmShape NARROW)
-      if (narrow_gemm(L, n) && L->maps_cg_up == 1)
-        return launch_grouped_gemm(L->map_x_narrow, L->map_w13, a, kEpiSwiGLU, 0, st);
-      return launch_grouped_gemm(L->map_x, L->map_w13, a, kEpiSwiGLU, L->maps_cg_up, st);
+      if (narrow_gemm(L, n) && up_cg(L, n) == 1)
+        return launch_grouped_gemm(L->map_x_narrow, L->map_w13_single, a, kEpiSwiGLU, 0, st);
+      return up_cg(L, n) == 2
+                 ? launch_grouped_gemm(L->map_x, L->map_w13, a, kEpiSwiGLU, 2, st)
+                 : launch_grouped_gemm(L->map_x, L->map_w13_single, a, kEpiSwiGLU, 1, st);
     }
     case SMOE_STAGE_EXPERT_DOWN: {
       GemmArgs a{};
@@ -667,6 +682,11 @@ extern "C" int smoe_set_option(int32_t key, int32_t value) {
       if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
       set_gemm_early_down(value);
       return SMOE_OK;
+    case SMOE_OPT_GEMM_GROUP_M_UP:
+    case SMOE_OPT_GEMM_GROUP_M_DOWN:
+      if (value < -4096 || value > 4096) return SMOE_ERR_INVALID_ARG;
+      set_gemm_group_m(key == SMOE_OPT_GEMM_GROUP_M_DOWN, value);
+      return SMOE_OK;
     case SMOE_OPT_ROUTE_IN_GATE:
       if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
       set_gate_route_fused(value);
@@ -695,6 +715,8 @@ extern "C" int smoe_get_option(int32_t key) {
   if (key == SMOE_OPT_DEDUP_DISPATCH) return g_dedup_dispatch;
   if (key == SMOE_OPT_EARLY_DOWN) return gemm_early_down();
   if (key == SMOE_OPT_ROUTE_IN_GATE) return gate_route_fused();
+  if (key == SMOE_OPT_GEMM_GROUP_M_UP) return gemm_group_m(0);
+  if (key == SMOE_OPT_GEMM_GROUP_M_DOWN) return gemm_group_m(1);
   return -1;
 }
 

@@ -317,6 +317,53 @@ class SpecMoELayer:
             self._hist_depth_out = min(depth + 1, w)
         return self.out_view(n)
 
+    def tune_gemm_order(self, tokens_t, hist_t=None, candidates=((1, 0), (2, -2)),
+                        rounds: int = 4, reps: int = 2) -> dict:
+        """Pick the up GEMM's schedule -- (cta_group, tile order) -- for this
+        batch on this GPU by interleaved timing (ABBA rounds) of whole
+        forwards, set it process-wide (SMOE_OPT_GEMM_CTA_GROUP_UP /
+        SMOE_OPT_GEMM_GROUP_M_UP) and return the timings.  Every schedule
+        gives bit-identical outputs; which one is faster depends on the GPU
+        (under the power cap the SM pair's fewer shared-memory bytes per flop
+        trade against its L2 misses, profiles/r2/gemm_cg_up/).  Decode-sized
+        batches always run one SM per tile: nothing to tune there."""
+        t = _dev.torch()
+        lib = self.lib
+        n = int(t.as_tensor(tokens_t).reshape(-1).shape[0])
+        pair_min = lib.smoe_get_option(N.OPT_GEMM_PAIR_MIN_ROWS)
+        cur = (lib.smoe_get_option(N.OPT_GEMM_CTA_GROUP_UP),
+               lib.smoe_get_option(N.OPT_GEMM_GROUP_M_UP))
+        if n * self.k <= pair_min * self.N:
+            return {"choice": list(cur), "tuned": False}
+
+        def use(c):
+            N.check(lib.smoe_set_option(N.OPT_GEMM_CTA_GROUP_UP, int(c[0])), "opt")
+            N.check(lib.smoe_set_option(N.OPT_GEMM_GROUP_M_UP, int(c[1])), "opt")
+
+        ms = {c: [] for c in candidates}
+        for c in candidates:                      # warm each schedule (maps, caches)
+            use(c)
+            self.run_device(tokens_t, hist_t)
+        t.cuda.synchronize()
+        for r in range(rounds):
+            order = list(candidates) if r % 2 == 0 else list(reversed(candidates))
+            for c in order:
+                use(c)
+                self.run_device(tokens_t, hist_t)
+                e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(reps):
+                    self.run_device(tokens_t, hist_t)
+                e1.record()
+                t.cuda.synchronize()
+                ms[c].append(e0.elapsed_time(e1) / reps)
+        med = {c: sorted(v)[len(v) // 2] for c, v in ms.items()}
+        best = min(candidates, key=lambda c: med[c])
+        use(best)
+        self.check_errors()
+        return {"choice": list(best), "tuned": True,
+                "median_ms": {f"cg{c[0]}_gm{c[1]}": round(v, 4) for c, v in med.items()}}
+
     def capture(self, tokens_t, hist_t=None, hist_depth=None):
         """Record one forward over these device tensors as a CUDA graph.
 

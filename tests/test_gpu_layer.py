@@ -508,3 +508,41 @@ def test_route_in_gate_bit_identical(n, over):
     assert torch.equal(res[0][0], res[1][0])
     assert res[0][1] == res[1][1] and res[0][2:4] == res[1][2:4]
     assert np.array_equal(res[0][4], res[1][4])
+
+
+def test_up_gemm_schedules_bit_identical_and_tuner():
+    """The up GEMM's schedules (one SM per 128x256 tile; SM pair per 256x256
+    tile with n-grouped order) give bit-identical layer outputs, and
+    tune_gemm_order picks one of them and leaves it set (restored here)."""
+    from paper_2503_04398_b200 import _native as N
+    lib = N.lib()
+    over = {"G": 4, "N": 8, "k": 2, "d": 512, "f": 256}
+    n = 8192                                      # 2 048 rows per expert: past the one-SM range
+    w = synth.make_workload("toy", n=n, eps=0.3, seed=31, cfg_override=over, device=True)
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=n)
+    layer.partial_views(n).copy_(w.partials)
+    tok = torch.as_tensor(w.tokens, device="cuda")
+    hist = torch.as_tensor(w.hist, device="cuda")
+    old = (lib.smoe_get_option(N.OPT_GEMM_CTA_GROUP_UP), lib.smoe_get_option(N.OPT_GEMM_GROUP_M_UP))
+    outs = []
+    try:
+        for cg, gm in ((1, 0), (2, -2), (2, 0), (1, -2)):
+            N.check(lib.smoe_set_option(N.OPT_GEMM_CTA_GROUP_UP, cg), "opt")
+            N.check(lib.smoe_set_option(N.OPT_GEMM_GROUP_M_UP, gm), "opt")
+            layer.out_view(n).zero_()
+            layer.run_device(tok, hist)
+            torch.cuda.synchronize()
+            layer.check_errors()
+            outs.append(layer.out_view(n).clone())
+        for o in outs[1:]:
+            assert torch.equal(o, outs[0])
+        res = layer.tune_gemm_order(tok, hist, rounds=2, reps=1)
+        assert res["tuned"] and tuple(res["choice"]) in ((1, 0), (2, -2))
+        assert (lib.smoe_get_option(N.OPT_GEMM_CTA_GROUP_UP),
+                lib.smoe_get_option(N.OPT_GEMM_GROUP_M_UP)) == tuple(res["choice"])
+        layer.run_device(tok, hist)
+        torch.cuda.synchronize()
+        assert torch.equal(layer.out_view(n), outs[0])
+    finally:
+        N.check(lib.smoe_set_option(N.OPT_GEMM_CTA_GROUP_UP, old[0]), "opt")
+        N.check(lib.smoe_set_option(N.OPT_GEMM_GROUP_M_UP, old[1]), "opt")
