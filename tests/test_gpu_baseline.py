@@ -102,7 +102,10 @@ def _dsmoe_oracle(w, n, partials=None):
 
 @pytest.mark.parametrize("n,over", [(300, {"G": 2, "N": 8}), (1000, {"G": 8, "N": 16}),
                                     (777, {"G": 8, "N": 64, "k": 6, "d": 512, "f": 256}),
-                                    (2600, {"G": 4, "N": 8})])
+                                    (2600, {"G": 4, "N": 8}),
+                                    # decode sizes: route fused into the gate, early down GEMM
+                                    (64, {"G": 8, "N": 64, "k": 6, "d": 512, "f": 256}),
+                                    (100, {"G": 4, "N": 8})])
 def test_dsmoe_pipeline_matches_oracle(n, over):
     """SMOE_PIPELINE_DSMOE (all-reduce + slice, combine into all-gather blocks
     + resume) on the s-MoE kernels: plan = position sharding (comm.py:202),
