@@ -546,3 +546,27 @@ def test_up_gemm_schedules_bit_identical_and_tuner():
     finally:
         N.check(lib.smoe_set_option(N.OPT_GEMM_CTA_GROUP_UP, old[0]), "opt")
         N.check(lib.smoe_set_option(N.OPT_GEMM_GROUP_M_UP, old[1]), "opt")
+
+
+def test_decode_path_errors_and_recovery():
+    """At decode sizes (route fused into the gate, early-started down GEMM,
+    plan-kernel resets) the reference's errors still surface -- capacity,
+    token range -- and the next clean batch is right (the per-forward
+    resets and readiness counters do not leak between batches)."""
+    from paper_2503_04398_b200.scheduler import SchedulerError
+    over = {"G": 8, "N": 64, "k": 6, "d": 512, "f": 256}
+    n = 64
+    w = synth.make_workload("toy", n=n, eps=0.3, seed=41, cfg_override=over)
+    parts = torch.from_numpy(w.partials).to(torch.bfloat16)
+    ref = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=6, max_tokens=n)
+    want = ref.forward(parts, w.tokens, w.hist).clone()
+    tight = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=6, max_tokens=n,
+                         expert_rows=4)
+    with pytest.raises(SchedulerError):
+        tight.forward(parts, w.tokens, w.hist)
+    bad = w.tokens.copy()
+    bad[3] = 10 ** 7
+    with pytest.raises(IndexError):
+        ref.forward(parts, bad, w.hist)
+    for _ in range(2):
+        assert torch.equal(ref.forward(parts, w.tokens, w.hist), want)
