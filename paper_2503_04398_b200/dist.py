@@ -115,6 +115,7 @@ class ShardGroup:
         peer["partial_b_local"] = tensor(local["partial_b"], (L, n, d),
                                          "<i2").view(torch.bfloat16)
         peer["out_local"] = tensor(local["out"], (n, d), "<i2").view(torch.bfloat16)
+        peer["xin_local"] = tensor(local["xin"], (L, R, d), "<i2").view(torch.bfloat16)
         for name, rows in extra.items():
             peer[name + "_local"] = tensor(local[name], (rows, d), "<i2").view(torch.bfloat16)
         peer["counts_local"] = tensor(local["counts"], (G, layer.N), "<i4")

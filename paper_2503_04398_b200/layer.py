@@ -170,6 +170,16 @@ class SpecMoELayer:
         self.topk_w = t.empty((L, n, k), dtype=t.float32, device=dev)
         self.pair_rank = t.empty((L, n, k), dtype=t.int32, device=dev)
         self.hmid = t.empty((L * R, f), dtype=bf, device=dev)
+        # Rows of a 128-row GEMM tile past an expert's routed rows are whatever
+        # the expert-input / hidden buffers hold, and the MMA rate depends on
+        # operand values: at decode sizes the DSV2-Lite up GEMM takes 163 us
+        # over zeros (a fresh allocation) or large values, 122 us over small
+        # noise (profiles/r1_gemm_l2/decode_padding_fill_scan.csv).  Start
+        # them as small noise; those rows are never stored, so no result
+        # depends on it.
+        gen = t.Generator(device=dev).manual_seed(0)
+        (self.xin if self.group is None else peer["xin_local"]).normal_(0.0, 0.01, generator=gen)
+        self.hmid.normal_(0.0, 0.01, generator=gen)
         self.forward_buf = t.empty(G * n, dtype=t.int64, device=dev)
         self.inverse = t.empty(n, dtype=t.int64, device=dev)
         self.dev = t.empty(n, dtype=t.int64, device=dev)
