@@ -570,3 +570,38 @@ def test_decode_path_errors_and_recovery():
         ref.forward(parts, bad, w.hist)
     for _ in range(2):
         assert torch.equal(ref.forward(parts, w.tokens, w.hist), want)
+
+
+@pytest.mark.parametrize("n,over", [(64, {"G": 8, "N": 64, "k": 6, "d": 512, "f": 256}),
+                                    (3000, {"G": 4, "N": 8, "k": 2, "d": 512, "f": 256}),
+                                    (300, {"G": 4, "N": 160, "k": 6, "d": 256, "f": 256})])
+def test_expert_buffer_padding_never_reaches_outputs(n, over):
+    """The expert-input / hidden buffers start as small noise (layer.py) and
+    hold stale rows of earlier batches: rows past an expert's routed rows feed
+    the padding of its GEMM tiles but must never reach an output.  Poisoning
+    both buffers (and the gate and combine arenas) with NaN / inf leaves the
+    layer's outputs and statistics bit-identical."""
+    w = synth.make_workload("toy", n=n, eps=0.3, seed=43, cfg_override=over, device=True)
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=over["k"], max_tokens=n)
+    layer.partial_views(n).copy_(w.partials)
+    tok = torch.as_tensor(w.tokens, device="cuda")
+    hist = torch.as_tensor(w.hist, device="cuda")
+    layer.run_device(tok, hist)
+    torch.cuda.synchronize()
+    layer.check_errors()
+    want = layer.out_view(n).clone()
+    st = layer.stats(n)
+    want_stats = (st["pair_counts"], st["local_tokens"], st["remote_tokens"])
+    assert torch.isfinite(want.float()).all()
+    for poison in (float("nan"), float("inf")):
+        # + the gate's input arena (rows past a shard's count fill the last
+        # 128-row gate tile) and the combine's pair rows
+        for buf in (layer.xin, layer.hmid, layer.hs, layer.ypair):
+            buf.fill_(poison)
+        layer.out_view(n).zero_()
+        layer.run_device(tok, hist)
+        torch.cuda.synchronize()
+        layer.check_errors()
+        assert torch.equal(layer.out_view(n), want)
+        st = layer.stats(n)
+        assert (st["pair_counts"], st["local_tokens"], st["remote_tokens"]) == want_stats
