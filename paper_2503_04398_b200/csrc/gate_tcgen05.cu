@@ -39,9 +39,10 @@
 namespace smoe {
 
 // Timeline probe (build variant -DSMOE_GATE_PROBE only, tools/probe/gate_timeline.py):
-// %globaltimer per CTA at fixed points of its first tile.
+// %globaltimer per CTA at fixed points of its first tile (16 slots; 8..12 and 14
+// are inside the register epilogue / fused route, recorded by its first thread).
 #ifdef SMOE_GATE_PROBE
-__device__ unsigned long long g_gate_ts[2048][8];
+__device__ unsigned long long g_gate_ts[2048][16];
 #define GATE_TS(i)                                                                   \
   do {                                                                               \
     unsigned long long t_;                                                           \
@@ -320,6 +321,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
         if (lane == 0) mbar_arrive(tempty0 + 8 * acc);     // accumulator free for tile t + 2
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
+        if (threadIdx.x == 128) GATE_TS(8);                // logits in registers
         if (S::kSplit == 1 && j >= s_cnt[gl]) continue;
         constexpr int NT = NH <= 16 ? 16 : (NH <= 32 ? 32 : 64);   // tree leaves (power of 2)
         int32_t key[NT];
@@ -361,6 +363,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
             taken |= 1ull << ti[0];
           }
         }
+        if (threadIdx.x == 128) GATE_TS(9);                // k selections done
         if constexpr (S::kSplit == 1) {
           const float mx = key_to_f(sel_k[0]);
 #pragma unroll
@@ -391,6 +394,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
           }
           // the two warps of this lane quarter (barrier ids 1..4; 0 is
           // __syncthreads); both barriers are warp-uniform
+          if (threadIdx.x == 128) GATE_TS(10);               // softmax sum, exchange written
           asm volatile("bar.sync %0, 64;" :: "r"(1 + ew) : "memory");
           const bool mine = hf == 0 && j < s_cnt[gl];
           float m1 = -INFINITY, s1 = 0.f;
@@ -422,6 +426,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
             s1 = __int_as_float(xr[17]);
           }
           asm volatile("bar.sync %0, 64;" :: "r"(1 + ew) : "memory");     // xch reusable
+          if (threadIdx.x == 128) GATE_TS(11);               // halves merged
           if (!mine) continue;
           const float mx = key_to_f(sel_k[0]);
           // all -inf rows: NaN, as the single-thread path gives
@@ -594,7 +599,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
       }
     }
     __syncwarp();
-    if (ew == 0 && lane == 0) GATE_TS(6);                 // epilogue warp 4 done
+    if (ew == 0 && lane == 0 && hf == 0) GATE_TS(6);      // epilogue warp 4 done
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       my_local += __shfl_xor_sync(0xffffffffu, my_local, o);
@@ -607,6 +612,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
                 my_remote);
       atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + SMOE_STAT_REMOTE_ROWS), my_rrows);
     }
+    if (threadIdx.x == 128) GATE_TS(12);                  // + stats atomics
     if (a.route && (int32_t)blockIdx.x < total && hf == 0) {
       // ===== fused route (decode-sized batches: this CTA's one tile is all
       // of its shard's rows): stable rank of every pair among the shard's
@@ -652,6 +658,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
       for (int ee = tid_e; ee < Nn; ee += 128)
         for (int i = 0; i < a.n_count_bufs; ++i)
           reinterpret_cast<int32_t*>(a.count_bufs.p[i])[g * Nn + ee] = s_pre[ee];
+      if (threadIdx.x == 128) GATE_TS(14);                // fused route done
     }
   }
   tc_fence_before();
@@ -754,13 +761,13 @@ int launch_gate_tc(const CUtensorMap& map_h, const CUtensorMap& map_w, const Gat
 #ifdef SMOE_GATE_PROBE
 extern "C" int smoe_probe_gate_ts(unsigned long long* host, int rows) {
   if (rows > 2048) rows = 2048;
-  return cudaMemcpyFromSymbol(host, smoe::g_gate_ts, sizeof(unsigned long long) * 8 * rows) ==
+  return cudaMemcpyFromSymbol(host, smoe::g_gate_ts, sizeof(unsigned long long) * 16 * rows) ==
                  cudaSuccess
              ? 0
              : -1;
 }
 extern "C" int smoe_probe_gate_reset() {
-  static unsigned long long zero[2048 * 8];
+  static unsigned long long zero[2048 * 16];
   return cudaMemcpyToSymbol(smoe::g_gate_ts, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;
 }
 #endif

@@ -351,25 +351,37 @@ def test_layer_all_tokens_on_one_shard_of_sixteen():
     assert np.linalg.norm(out - ref["out"]) / np.linalg.norm(ref["out"]) <= TOL
 
 
-def test_batch_invariance_across_cuts():
-    """A token's output (and routing, next-layer history) is bit-identical
-    whether it is processed in a 1100-token batch or in decode-sized pieces
-    (1, 7, 64, 300, 728 tokens): no kernel's per-row arithmetic depends on
-    the other rows of its batch, and the batch-size-dependent kernel choices
-    (one-SM vs SM-pair GEMMs, row vs chunk movers) are bit-identical."""
-    over = {"G": 8, "N": 16, "k": 2, "d": 512, "f": 384}
+@pytest.mark.parametrize("over,renorm", [
+    ({"G": 8, "N": 16, "k": 2, "d": 512, "f": 384}, True),
+    ({"G": 8, "N": 64, "k": 6, "d": 512, "f": 256}, False),
+    ({"G": 8, "N": 64, "k": 8, "d": 512, "f": 256}, True),
+    ({"G": 4, "N": 40, "k": 4, "d": 512, "f": 256}, False)])
+def test_batch_invariance_across_cuts(over, renorm):
+    """A token's output (and routing, weights, next-layer history) is
+    bit-identical whether it is processed in a 1100-token batch or in
+    decode-sized pieces (1, 7, 64, 300, 728 tokens): no kernel's per-row
+    arithmetic depends on the other rows of its batch, and the
+    batch-size-dependent kernel choices (one-SM vs SM-pair GEMMs, row vs chunk
+    movers, the gate's route fused at <= 128 tokens) are bit-identical; N = 64
+    runs the gate's split (two threads per row) epilogue, N = 40 its N' = 48
+    register tree."""
     n = 1100
     w = synth.make_workload("toy", n=n, eps=0.3, seed=99, cfg_override=over)
     parts = torch.from_numpy(w.partials).to(torch.bfloat16)
-    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=2, max_tokens=n)
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=over["k"], max_tokens=n,
+                         renormalize=renorm)
     full = layer.forward(parts, w.tokens, w.hist).clone()
     full_hist = layer.next_history(n).clone()
+    full_route = layer.routing(n)
     lo = 0
     for size in (1, 7, 64, 300, 728):
         hi = lo + size
         got = layer.forward(parts[:, lo:hi].contiguous(), w.tokens[lo:hi], w.hist[lo:hi])
         assert torch.equal(got, full[lo:hi]), (lo, hi)
         assert torch.equal(layer.next_history(size), full_hist[lo:hi])
+        route = layer.routing(size)
+        for key in route:
+            assert np.array_equal(np.asarray(route[key]), np.asarray(full_route[key])[lo:hi]), key
         lo = hi
     assert lo == n
 

@@ -5,7 +5,10 @@
 
 Points (per CTA, first tile, %globaltimer ns): 0 entry, 1 set-up done (TMEM,
 barriers, counts), 2 last TMA of the tile issued, 3 first stage landed, 4 last
-MMA issued, 5 accumulator ready in the epilogue, 6 epilogue warp done, 7 exit.
+MMA issued, 5 accumulator ready in the epilogue, 6 epilogue warp done, 7 exit;
+register epilogue (first thread): 8 logits in registers, 9 k selections done,
+10 softmax sum + exchange written, 11 halves merged, 12 stats atomics done,
+14 fused route done.
 Prints the median / max over CTAs of each point relative to the earliest entry.
 """
 import ctypes as C
@@ -34,9 +37,9 @@ for rep in range(3):
     assert h.smoe_probe_gate_reset() == 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); layer.run_device(tok, hist, stages=[j]); e1.record(); torch.cuda.synchronize()
-    buf = (C.c_ulonglong * (2048 * 8))()
+    buf = (C.c_ulonglong * (2048 * 16))()
     assert h.smoe_probe_gate_ts(buf, 2048) == 0
-    ts = np.frombuffer(buf, dtype=np.uint64).reshape(2048, 8).astype(np.int64)
+    ts = np.frombuffer(buf, dtype=np.uint64).reshape(2048, 16).astype(np.int64)
     act = ts[(ts[:, 0] > 0) & (ts[:, 5] > 0)]
     base = ts[ts[:, 0] > 0, 0].min()
     rel = (act - base) / 1e3
