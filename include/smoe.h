@@ -84,6 +84,10 @@ const char* smoe_version(void);
 #define SMOE_OPT_GEMM_GROUP_M_UP    10  /* tile order of the layer's up / down GEMM: */
 #define SMOE_OPT_GEMM_GROUP_M_DOWN  11  /* 0 = derived (default), > 0 m-blocks per   */
                                         /* group, < 0 -(n-blocks per group)          */
+#define SMOE_OPT_DECODE_UP_PDL      12  /* batches with the early-started down GEMM: */
+                                        /* the up GEMM launches under PDL too (its  */
+                                        /* readiness counters are reset by the plan */
+                                        /* kernel; 1 = default, 0 = plain launch)   */
 int smoe_set_option(int32_t key, int32_t value);
 int smoe_get_option(int32_t key);
 const char* smoe_status_string(int status);

@@ -89,6 +89,7 @@ OPT_EARLY_DOWN = 8
 OPT_ROUTE_IN_GATE = 9
 OPT_GEMM_GROUP_M_UP = 10
 OPT_GEMM_GROUP_M_DOWN = 11
+OPT_DECODE_UP_PDL = 12
 
 (BUF_PARTIAL, BUF_XIN, BUF_XMETA, BUF_YPAIR, BUF_OUT, BUF_COUNTS, BUF_SIGNAL, BUF_HS,
  BUF_TOPK_IDS, BUF_TOPK_W, BUF_PAIR_RANK, BUF_HMID, BUF_FORWARD, BUF_INVERSE, BUF_DEV,

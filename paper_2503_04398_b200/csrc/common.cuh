@@ -26,6 +26,43 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // Number of SMs on the current device (cached per process).
 int num_sms();
 
+// ---- stage timeline probe (build variant -DSMOE_TIMELINE only) -----------
+// Per kernel kind k (0 plan, 1 SRS, 2 gate, 4 dispatch, 5 up GEMM, 6 down
+// GEMM, 7 combine + SAG) and CTA (< 256): %globaltimer at entry, after the
+// PDL wait, and the last warp's exit -- a Gantt chart of one graph replay
+// (tools/probe/forward_timeline.py).  Each translation unit has its own
+// table, read through smoe_probe_tl_<unit>.
+#ifdef SMOE_TIMELINE
+static __device__ unsigned long long g_tl[8][256][3];
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SMOE_TL_ENTER(k) \
+  do { if (threadIdx.x == 0 && blockIdx.x < 256) smoe::g_tl[k][blockIdx.x][0] = smoe::tl_now(); } while (0)
+#define SMOE_TL_WAITED(k) \
+  do { if (threadIdx.x == 0 && blockIdx.x < 256) smoe::g_tl[k][blockIdx.x][1] = smoe::tl_now(); } while (0)
+#define SMOE_TL_EXIT(k)                                                          \
+  do {                                                                           \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x < 256)                             \
+      atomicMax(&smoe::g_tl[k][blockIdx.x][2], smoe::tl_now());                  \
+  } while (0)
+#define SMOE_TL_EXPORT(unit)                                                      \
+  extern "C" int smoe_probe_tl_##unit(unsigned long long* host) {                 \
+    return cudaMemcpyFromSymbol(host, smoe::g_tl, sizeof(smoe::g_tl)) == cudaSuccess ? 0 : -1; \
+  }                                                                               \
+  extern "C" int smoe_probe_tl_reset_##unit() {                                   \
+    static unsigned long long zero[8 * 256 * 3];                                  \
+    return cudaMemcpyToSymbol(smoe::g_tl, zero, sizeof(zero)) == cudaSuccess ? 0 : -1; \
+  }
+#else
+#define SMOE_TL_ENTER(k) do { } while (0)
+#define SMOE_TL_WAITED(k) do { } while (0)
+#define SMOE_TL_EXIT(k) do { } while (0)
+#define SMOE_TL_EXPORT(unit)
+#endif
+
 // ---- programmatic dependent launch (PDL) --------------------------------
 // Layer-path kernels are launched with programmatic stream serialisation:
 // the next kernel on the stream may start while this one still runs.  Every

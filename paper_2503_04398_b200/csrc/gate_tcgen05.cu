@@ -137,6 +137,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
   __shared__ int32_t s_owner[NP];        // cluster of each expert slot (locality count)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  SMOE_TL_ENTER(2);
   if (threadIdx.x == 0) GATE_TS(0);
   if (threadIdx.x < NP) {
     s_bias[threadIdx.x] = (a.b_gate && threadIdx.x < a.n_experts) ? a.b_gate[threadIdx.x] : 0.f;
@@ -169,6 +170,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
   // shard row counts come from the plan stage
   pdl_trigger();
   pdl_wait();
+  SMOE_TL_WAITED(2);
   if (threadIdx.x < 32) {
     // one lane per shard: the count loads are in flight together
     const int i = threadIdx.x;
@@ -669,6 +671,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
                  :: "r"(tmem_base), "r"(S::kTmemCols) : "memory");
   }
+  SMOE_TL_EXIT(2);
 }
 
 template <int NP, int SUB, int ST>
@@ -771,3 +774,5 @@ extern "C" int smoe_probe_gate_reset() {
   return cudaMemcpyToSymbol(smoe::g_gate_ts, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;
 }
 #endif
+
+SMOE_TL_EXPORT(gate)

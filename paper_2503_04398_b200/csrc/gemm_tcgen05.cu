@@ -145,6 +145,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t np = args.num_problems;
+  constexpr int kTl = EPI == kEpiSwiGLU ? 5 : 6;
+  SMOE_TL_ENTER(kTl);
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;     // CTA rank inside the SM pair
   // CTA -> tile assignment follows blockIdx: the launch order places
   // consecutive CTAs on the two SMs of a TPC, then round-robin over GPCs, so
@@ -187,6 +189,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
   // are visible once this grid runs, and the up GEMM's hidden rows are
   // awaited per problem by the producer below
   if (args.ready_role != 2) pdl_wait();
+  SMOE_TL_WAITED(kTl);
   // ---- problem table -> shared, tile prefix
   for (int p = threadIdx.x; p < np; p += kThreads) {
     const int64_t* q = args.problems + 4 * p;
@@ -423,6 +426,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;"
                    :: "r"(tmem_base), "r"(kTmemCols) : "memory");
   }
+  SMOE_TL_EXIT(kTl);
 }
 
 // ---------------------------------------------------------------- host
@@ -675,3 +679,5 @@ extern "C" int smoe_grouped_gemm(const void* A, int64_t a_rows, int64_t K, const
   args.ldc = ldc;
   return launch_grouped_gemm(ta, tb, args, epilogue, cg, as_stream(stream));
 }
+
+SMOE_TL_EXPORT(gemm)

@@ -33,6 +33,7 @@ struct smoe_layer {
   int32_t* slot_first_d = nullptr;   // [G + 1]
   int32_t* ready_d = nullptr;        // [kMaxExperts] up-tile counts (early down GEMM)
   bool ready_armed = false;          // the last EXPERT_UP launch publishes them
+  bool ready_zeroed = false;         // this forward's PLAN reset them
   bool route_fused = false;          // the last GATE launch also ran the route
   int32_t local_slots = 0;           // expert slots owned by the resident shards
   // weights
@@ -213,6 +214,7 @@ static ShardPtrs distinct_ptrs_local_first(const smoe_layer* L, int slot, int32_
 }
 
 static int g_dedup_dispatch = 1;      // SMOE_OPT_DEDUP_DISPATCH
+static int g_decode_up_pdl = 1;       // SMOE_OPT_DECODE_UP_PDL
 
 static int check_bound(const smoe_layer* L) {
   const auto& c = L->cfg;
@@ -405,7 +407,7 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
     case SMOE_STAGE_PLAN: {
       if (n > 0 && !tokens) return SMOE_ERR_INVALID_ARG;
       const int64_t* lookup_hist = (hist && hist_depth >= L->hist_len) ? hist : nullptr;
-      return layer_plan(tokens, n, lookup_hist, L->hist_len, L->t_labels, L->t_conf, L->vocab,
+      rc = layer_plan(tokens, n, lookup_hist, L->hist_len, L->t_labels, L->t_conf, L->vocab,
                         L->a_best, L->a_conf, L->a_rows, c.n_shards,
                         static_cast<int64_t*>(L->buf[SMOE_BUF_DEV][0]),
                         static_cast<int64_t*>(L->buf[SMOE_BUF_FORWARD][0]),
@@ -413,7 +415,9 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
                         static_cast<int32_t*>(L->buf[SMOE_BUF_PLAN_COUNTS][0]),
                         static_cast<int64_t*>(L->buf[SMOE_BUF_GROUP][0]), err,
                         L->buf[SMOE_BUF_WORKSPACE][0], plan_ws_aligned(&c), stats,
-                        SMOE_STAT__COUNT, st);
+                        SMOE_STAT__COUNT, st, L->ready_d, L->local_slots);
+      L->ready_zeroed = rc == SMOE_OK;
+      return rc;
     }
     case SMOE_STAGE_SRS:
       // every process's partials for this batch are written before any peer
@@ -514,11 +518,23 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       a.ldc = c.ffn;
       a.b_tiled = L->w_tiled;
       L->ready_armed = early_down(L, n);
+      // decode sizes: launched under PDL (its CTA placement does not matter
+      // when no two tiles share a weight tile), behind counters the PLAN
+      // kernel reset -- a memset here would sit between the dispatch and
+      // this launch (~6 us of launch gap, tools/probe/forward_timeline.py)
+      const bool up_pdl = L->ready_armed && L->ready_zeroed && g_decode_up_pdl;
       if (L->ready_armed) {
-        SMOE_CUDA_TRY(cudaMemsetAsync(L->ready_d, 0, sizeof(int32_t) * L->local_slots, st));
+        if (!L->ready_zeroed)              // stage calls without this forward's PLAN
+          SMOE_CUDA_TRY(cudaMemsetAsync(L->ready_d, 0, sizeof(int32_t) * L->local_slots, st));
         a.ready = L->ready_d;
         a.ready_role = 1;
       }
+      L->ready_zeroed = false;
+      if (up_pdl) set_pdl_stage(-1);       // PDL as for any early-launched stage
+      struct Restore {
+        bool on;
+        ~Restore() { if (on) set_pdl_stage(SMOE_STAGE_EXPERT_UP); }
+      } restore{up_pdl};
       // decode-sized batches stream the weights: narrow m-blocks keep more
       // weight tiles in flight per SM (gemm_tcgen05.cu, GemmShape NARROW)
       if (narrow_gemm(L, n) && up_cg(L, n) == 1)
@@ -687,6 +703,10 @@ extern "C" int smoe_set_option(int32_t key, int32_t value) {
       if (value < -4096 || value > 4096) return SMOE_ERR_INVALID_ARG;
       set_gemm_group_m(key == SMOE_OPT_GEMM_GROUP_M_DOWN, value);
       return SMOE_OK;
+    case SMOE_OPT_DECODE_UP_PDL:
+      if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
+      g_decode_up_pdl = value;
+      return SMOE_OK;
     case SMOE_OPT_ROUTE_IN_GATE:
       if (value != 0 && value != 1) return SMOE_ERR_INVALID_ARG;
       set_gate_route_fused(value);
@@ -715,6 +735,7 @@ extern "C" int smoe_get_option(int32_t key) {
   if (key == SMOE_OPT_DEDUP_DISPATCH) return g_dedup_dispatch;
   if (key == SMOE_OPT_EARLY_DOWN) return gemm_early_down();
   if (key == SMOE_OPT_ROUTE_IN_GATE) return gate_route_fused();
+  if (key == SMOE_OPT_DECODE_UP_PDL) return g_decode_up_pdl;
   if (key == SMOE_OPT_GEMM_GROUP_M_UP) return gemm_group_m(0);
   if (key == SMOE_OPT_GEMM_GROUP_M_DOWN) return gemm_group_m(1);
   return -1;

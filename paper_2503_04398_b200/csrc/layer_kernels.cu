@@ -139,7 +139,9 @@ __device__ __forceinline__ void srs_span(const char* const (&src_base)[G], int64
 template <int G>
 __global__ void __launch_bounds__(256)
 srs_kernel(LocalRows lr, ShardPtrs partials, int64_t d, ShardPtrs hs, int32_t whole_rows) {
+  SMOE_TL_ENTER(1);
   pdl_enter();
+  SMOE_TL_WAITED(1);
   __shared__ RowMap rm;
   __shared__ char* s_hs[SMOE_MAX_SHARDS];
   stage_ptrs(s_hs, hs);
@@ -170,6 +172,7 @@ srs_kernel(LocalRows lr, ShardPtrs partials, int64_t d, ShardPtrs hs, int32_t wh
                   c * kChunkVecs, min(vecs, (c + 1) * kChunkVecs), lane);
     }
   }
+  SMOE_TL_EXIT(1);
 }
 
 int launch_srs(const LocalRows& lr, const ShardPtrs& partials, int64_t d, const ShardPtrs& hs,
@@ -756,7 +759,9 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
                 ShardPtrs hs, ShardPtrs topk_ids, ShardPtrs pair_rank, ShardPtrs xin,
                 ShardPtrs xmeta, int64_t expert_rows, int64_t* problems, int32_t* err,
                 int32_t whole_rows, ShardPtrs xfan, int64_t* stats) {
+  SMOE_TL_ENTER(4);
   pdl_enter();
+  SMOE_TL_WAITED(4);
   __shared__ RowMap rm;
   __shared__ int32_t s_M[kMaxExperts];
   __shared__ int32_t s_seg[kMaxExperts];
@@ -884,6 +889,7 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
       for (int i = 0; i < nd; ++i) DISPATCH_ST(dst[i] + v * 16, a);
     }
   }
+  SMOE_TL_EXIT(4);
 }
 
 // Owner side of the deduplicated dispatch: every expert-input row whose
@@ -1005,7 +1011,9 @@ __global__ void __launch_bounds__(256, MINB)
 combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtrs topk_w,
                    ShardPtrs outs, HistUpdate hu, int32_t whole_rows, int64_t block_rows,
                    int32_t* err) {
+  SMOE_TL_ENTER(7);
   pdl_enter();
+  SMOE_TL_WAITED(7);
   __shared__ RowMap rm;
   __shared__ char* s_y[SMOE_MAX_SHARDS];
   __shared__ char* s_wts[SMOE_MAX_SHARDS];
@@ -1063,6 +1071,7 @@ combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtr
     combine_span<G>(dst_base, s_y[gl] + j * k * d * 2, wk, k, d, i_dst, c * cv,
                     min(vecs, (c + 1) * cv), lane);
   }
+  SMOE_TL_EXIT(7);
 }
 
 int launch_combine_sag(const LocalRows& lr, int32_t k, int64_t d, const ShardPtrs& ypair,
@@ -1278,3 +1287,5 @@ int launch_barrier(const ShardPtrs& signals, int32_t world, int32_t rank, uint32
 }
 
 }  // namespace smoe
+
+SMOE_TL_EXPORT(layer)

@@ -121,12 +121,13 @@ int launch_barrier(const ShardPtrs& signals, int32_t world, int32_t rank, uint32
 
 namespace smoe {
 // PLAN stage of the layer (plan.cu): smoe_lookup_plan plus the per-forward
-// resets of `err` and stats[0, n_stats) -- folded into the single-CTA plan
-// kernel for decode-sized batches
+// resets of `err`, stats[0, n_stats) and zero_i32[0, n_zero_i32) -- folded
+// into the single-CTA plan kernel for decode-sized batches
 int layer_plan(const int64_t* tokens, int64_t n, const int64_t* hist, int32_t hist_len,
                const int16_t* t_labels, const float* t_conf, int64_t vocab,
                const int16_t* a_best, const float* a_conf, int64_t a_rows, int32_t n_clusters,
                int64_t* dev_out, int64_t* forward, int64_t* inverse, int32_t* counts,
                int64_t* group, int32_t* err, void* workspace, size_t workspace_bytes,
-               int64_t* stats, int32_t n_stats, cudaStream_t st);
+               int64_t* stats, int32_t n_stats, cudaStream_t st, int32_t* zero_i32 = nullptr,
+               int32_t n_zero_i32 = 0);
 }  // namespace smoe

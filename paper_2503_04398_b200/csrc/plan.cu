@@ -172,8 +172,10 @@ plan_single_kernel(LookupTables t, int use_lookup, const int64_t* __restrict__ t
                    int64_t* __restrict__ dev_out, int64_t* __restrict__ forward,
                    int64_t* __restrict__ inverse, int32_t* __restrict__ counts_out,
                    int64_t* __restrict__ group_out, int32_t* err, int64_t* zero_stats,
-                   int32_t n_zero_stats) {
+                   int32_t n_zero_stats, int32_t* zero_i32, int32_t n_zero_i32) {
+  SMOE_TL_ENTER(0);
   pdl_enter();
+  SMOE_TL_WAITED(0);
   // the layer's per-forward resets (error flag, event counters), folded in so
   // a decode-sized forward starts with one kernel instead of two memsets and
   // a kernel; the __syncthreads below orders them before any lookup error
@@ -181,6 +183,9 @@ plan_single_kernel(LookupTables t, int use_lookup, const int64_t* __restrict__ t
     if (threadIdx.x < n_zero_stats) zero_stats[threadIdx.x] = 0;
     if (threadIdx.x == 0 && err) *err = 0;
   }
+  // + the early-started down GEMM's per-expert readiness counters (no memset
+  // node in front of the up GEMM, which can then launch under PDL)
+  for (int i = threadIdx.x; i < n_zero_i32; i += blockDim.x) zero_i32[i] = 0;
   extern __shared__ int32_t smem[];
   int32_t* s_cnt = smem;                  // [G] tokens per device
   int32_t* s_base = smem + G;             // [G] running offset per device
@@ -244,6 +249,7 @@ plan_single_kernel(LookupTables t, int use_lookup, const int64_t* __restrict__ t
     const int64_t d = sl / group, r = sl - d * group;
     if (r >= s_cnt[d]) forward[sl] = -1;
   }
+  SMOE_TL_EXIT(0);
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -255,7 +261,8 @@ static int plan_impl(const LookupTables& t, int use_lookup, const int64_t* token
                      const int64_t* devices, int64_t n, int32_t G, int64_t* dev_out,
                      int64_t* forward, int64_t* inverse, int32_t* counts, int64_t* group,
                      int32_t* err, void* ws, size_t ws_bytes, cudaStream_t st,
-                     int64_t* zero_stats = nullptr, int32_t n_zero_stats = 0) {
+                     int64_t* zero_stats = nullptr, int32_t n_zero_stats = 0,
+                     int32_t* zero_i32 = nullptr, int32_t n_zero_i32 = 0) {
 #ifndef SMOE_PLAN_FOLD
 #define SMOE_PLAN_FOLD 1      // 0: memsets before every plan (A/B builds)
 #endif
@@ -265,6 +272,8 @@ static int plan_impl(const LookupTables& t, int use_lookup, const int64_t* token
     SMOE_CUDA_TRY(cudaMemsetAsync(zero_stats, 0, sizeof(int64_t) * n_zero_stats, st));
     if (err) SMOE_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
   }
+  if (zero_i32 && n_zero_i32 > 0 && !single)
+    SMOE_CUDA_TRY(cudaMemsetAsync(zero_i32, 0, sizeof(int32_t) * n_zero_i32, st));
   if (G < 1 || G > SMOE_MAX_PLAN_DEVICES) return SMOE_ERR_UNSUPPORTED;
   if (n < 0 || !counts || !group || (n > 0 && (!forward || !inverse))) return SMOE_ERR_INVALID_ARG;
   if (ws_bytes < smoe_plan_workspace_bytes(n, G) || (n > 0 && !ws)) return SMOE_ERR_INVALID_ARG;
@@ -282,7 +291,8 @@ static int plan_impl(const LookupTables& t, int use_lookup, const int64_t* token
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     SMOE_CUDA_TRY(launch_pdl(plan_single_kernel, 1, kPlanThreads, smem2, st, t, use_lookup,
                              tokens, devices, n, G, dev_out, forward, inverse, counts, group,
-                             err, single ? zero_stats : nullptr, n_zero_stats));
+                             err, single ? zero_stats : nullptr, n_zero_stats,
+                             single ? zero_i32 : nullptr, single ? n_zero_i32 : 0));
     SMOE_LAUNCH_CHECK();
     return SMOE_OK;
   }
@@ -358,16 +368,21 @@ int layer_plan(const int64_t* tokens, int64_t n, const int64_t* hist, int32_t hi
                const int16_t* a_best, const float* a_conf, int64_t a_rows, int32_t n_clusters,
                int64_t* dev_out, int64_t* forward, int64_t* inverse, int32_t* counts,
                int64_t* group, int32_t* err, void* workspace, size_t workspace_bytes,
-               int64_t* stats, int32_t n_stats, cudaStream_t st) {
+               int64_t* stats, int32_t n_stats, cudaStream_t st, int32_t* zero_i32,
+               int32_t n_zero_i32) {
   if (n > 0 && (!tokens || !t_labels || !t_conf)) return SMOE_ERR_INVALID_ARG;
   if (hist && (!a_best || !a_conf || hist_len < 0)) return SMOE_ERR_INVALID_ARG;
   LookupTables t{t_labels, t_conf, vocab, a_best, a_conf, a_rows, n_clusters, hist, hist_len};
   if (n == 0) {
     SMOE_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(int64_t) * n_stats, st));
     SMOE_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
+    if (zero_i32 && n_zero_i32 > 0)
+      SMOE_CUDA_TRY(cudaMemsetAsync(zero_i32, 0, sizeof(int32_t) * n_zero_i32, st));
   }
   return plan_impl(t, 1, tokens, nullptr, n, n_clusters, dev_out, forward, inverse, counts,
                    group, err, workspace, workspace_bytes, st, n > 0 ? stats : nullptr,
-                   n_stats);
+                   n_stats, n > 0 ? zero_i32 : nullptr, n_zero_i32);
 }
 }  // namespace smoe
+
+SMOE_TL_EXPORT(plan)
