@@ -617,3 +617,51 @@ def test_expert_buffer_padding_never_reaches_outputs(n, over):
         assert torch.equal(layer.out_view(n), want)
         st = layer.stats(n)
         assert (st["pair_counts"], st["local_tokens"], st["remote_tokens"]) == want_stats
+
+
+@pytest.mark.parametrize("up_pdl", [0, 1])
+def test_decode_up_gemm_pdl_bit_identical(up_pdl):
+    """SMOE_OPT_DECODE_UP_PDL: at decode sizes the up GEMM launches under PDL
+    behind readiness counters the plan kernel resets (no memset node between
+    the dispatch and the up GEMM).  Outputs equal the plain launch's bit for
+    bit, eager, graph-replayed, and when an EXPERT_UP stage call runs twice
+    without a PLAN in between (the counters are then reset by a memset)."""
+    from paper_2503_04398_b200 import _native as N
+    lib = N.lib()
+    over = {"G": 8, "N": 64, "k": 6, "d": 512, "f": 256}
+    n = 64
+    w = synth.make_workload("toy", n=n, eps=0.3, seed=47, cfg_override=over, device=True)
+    layer = SpecMoELayer(w.bundle, w.gate_w, w.w1, w.w3, w.w2, top_k=6, max_tokens=n)
+    layer.partial_views(n).copy_(w.partials)
+    tok = torch.as_tensor(w.tokens, device="cuda")
+    hist = torch.as_tensor(w.hist, device="cuda")
+    old = lib.smoe_get_option(N.OPT_DECODE_UP_PDL)
+    try:
+        N.check(lib.smoe_set_option(N.OPT_DECODE_UP_PDL, 0), "opt")
+        layer.run_device(tok, hist)
+        torch.cuda.synchronize()
+        layer.check_errors()
+        want = layer.out_view(n).clone()
+        N.check(lib.smoe_set_option(N.OPT_DECODE_UP_PDL, up_pdl), "opt")
+        for _ in range(3):
+            layer.out_view(n).zero_()
+            layer.run_device(tok, hist)
+            torch.cuda.synchronize()
+            layer.check_errors()
+            assert torch.equal(layer.out_view(n), want)
+        up = N.STAGE_NAMES.index("expert_up")
+        layer.out_view(n).zero_()
+        layer.run_device(tok, hist, stages=list(range(up + 1)))
+        layer.run_device(tok, hist, stages=list(range(up, len(N.STAGE_NAMES))))
+        torch.cuda.synchronize()
+        layer.check_errors()
+        assert torch.equal(layer.out_view(n), want)
+        g = layer.capture(tok, hist)
+        for _ in range(3):
+            layer.out_view(n).zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            layer.check_errors()
+            assert torch.equal(layer.out_view(n), want)
+    finally:
+        N.check(lib.smoe_set_option(N.OPT_DECODE_UP_PDL, old), "opt")
