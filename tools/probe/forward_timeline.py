@@ -46,7 +46,11 @@ def main():
     ap.add_argument("tokens", type=int)
     ap.add_argument("--replays", type=int, default=3)
     ap.add_argument("--big", type=int, default=2048)
+    ap.add_argument("--opt", action="append", default=[], help="KEY=VALUE smoe_set_option")
     a = ap.parse_args()
+    for kv in a.opt:
+        key, val = (int(x) for x in kv.split("="))
+        N.check(N.lib().smoe_set_option(key, val), "set_option")
     n = a.tokens
     big = synth.make_workload(a.config, n=a.big, eps=0.2, seed=0, device=True)
     layer = SpecMoELayer(big.bundle, big.gate_w, big.w1, big.w3, big.w2, top_k=big.cfg["k"],
