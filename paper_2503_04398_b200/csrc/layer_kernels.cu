@@ -760,7 +760,14 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
                 ShardPtrs xmeta, int64_t expert_rows, int64_t* problems, int32_t* err,
                 int32_t whole_rows, ShardPtrs xfan, int64_t* stats) {
   SMOE_TL_ENTER(4);
-  pdl_enter();
+  // the dependents' early launch is triggered at the END of this kernel: at
+  // decode sizes the next kernel is the PDL-launched up GEMM, whose 148
+  // resident-but-waiting CTAs slowed the gate and this kernel by ~2 us when
+  // they were launched from its start (tools/probe/forward_timeline.py);
+  // triggered here they still launch as the copies finish -- DSV2-Lite /
+  // Qwen2 / Mixtral 64-token forward -0.9 / -5.3 / -4.3 us
+  // (profiles/r2/decode/dispatch_late_trigger/)
+  pdl_wait();
   SMOE_TL_WAITED(4);
   __shared__ RowMap rm;
   __shared__ int32_t s_M[kMaxExperts];
@@ -889,6 +896,7 @@ dispatch_kernel(LocalRows lr, int32_t N, int32_t k, int64_t d, const int32_t* __
       for (int i = 0; i < nd; ++i) DISPATCH_ST(dst[i] + v * 16, a);
     }
   }
+  pdl_trigger();
   SMOE_TL_EXIT(4);
 }
 
