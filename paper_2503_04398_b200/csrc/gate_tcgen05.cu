@@ -167,8 +167,10 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   // everything above reads constant data only (weights, tensor maps); the
-  // shard row counts come from the plan stage
-  pdl_trigger();
+  // shard row counts come from the plan stage.  The dependents' early launch
+  // is triggered at the END of this kernel: the dispatch kernel's CTAs,
+  // resident and waiting from the start, slowed this gate (64-token forward
+  // DSV2-Lite / Qwen2 -6.5 / -5.5 us, profiles/r2/decode/pdl_trigger/)
   pdl_wait();
   SMOE_TL_WAITED(2);
   if (threadIdx.x < 32) {
@@ -671,6 +673,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
                  :: "r"(tmem_base), "r"(S::kTmemCols) : "memory");
   }
+  pdl_trigger();
   SMOE_TL_EXIT(2);
 }
 
