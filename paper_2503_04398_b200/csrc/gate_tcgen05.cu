@@ -61,6 +61,9 @@ __device__ unsigned long long g_gate_ts[2048][16];
 #ifndef SMOE_GATE_REG_MAX_NP
 #define SMOE_GATE_REG_MAX_NP 64   // 32 (tournament for 48 / 64) measured: profiles/r2/gate/
 #endif
+#ifndef SMOE_GATE_WARP_ROWS
+#define SMOE_GATE_WARP_ROWS 1     // a warp per row for tiles of <= 32 rows, N' >= 32 (0: off)
+#endif
 
 constexpr int kGtThreads = 256;
 constexpr int kGtRows = 128;                               // MMA M: rows per tile
@@ -107,6 +110,11 @@ template <int NP, int SUB, int ST> struct GtShape {
   static constexpr uint32_t kWideBytes =
       kWide ? kWideRows * kWideLd * 4 + kWideRows * kWideFields * 4 : 0;
   static constexpr size_t kSmem = 1024 + ST * kStageBytes + 128 + kWideBytes + kXchBytes;
+  // register path, tiles of <= 32 valid rows: rows staged in shared memory,
+  // a warp per row (static __shared__: plain LDS / STS)
+  static constexpr bool kWarpRows = SMOE_GATE_WARP_ROWS && !kWide && NP >= 32;
+  static constexpr int kWrLd = NP + 1;
+  static constexpr int kWrFloats = kWarpRows ? 32 * kWrLd + 4 * kSplit * 64 : 1;
   // D f32, A/B bf16, both K-major, N = NP, M = 128
   static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) |
                                      (uint32_t(NP >> 3) << 17) | (uint32_t(kGtRows >> 4) << 24);
@@ -135,6 +143,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
   __shared__ char* s_wts[SMOE_MAX_SHARDS];
   __shared__ float s_bias[NP];
   __shared__ int32_t s_owner[NP];        // cluster of each expert slot (locality count)
+  __shared__ float wr[S::kWrFloats];      // warp-per-row staging + scratch
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   SMOE_TL_ENTER(2);
@@ -291,6 +300,15 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
     const int N = a.n_experts, K = a.k;
     uint32_t acc = 0, acc_phase = 0;
     unsigned long long my_local = 0, my_remote = 0, my_rrows = 0;
+    // order-preserving int keys (+0 and -0 merged, -inf an ordinary
+    // candidate); INT_MIN marks "not a candidate" (slots >= N, slots
+    // already taken), so fewer than k finite logits still give k distinct
+    // slots, as the stable argsort of the reference idiom does
+    auto to_key = [](float x) {
+      const int32_t b = __float_as_int(x + 0.0f);
+      return b >= 0 ? b : b ^ 0x7fffffff;
+    };
+    auto key_to_f = [](int32_t k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); };
     for (int32_t t = blockIdx.x; t < total; t += gridDim.x) {
       int32_t gl, blk;
       decode(t, gl, blk);
@@ -299,15 +317,6 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
       if (ew == 0 && lane == 0 && t == (int32_t)blockIdx.x) GATE_TS(5);   // accumulator ready
       const uint32_t taddr = tmem_base + acc * S::kAccCols + ((uint32_t)(ew * 32) << 16);
       const int64_t j = (int64_t)blk * S::kRows + ew * 32 + lane;
-      // order-preserving int keys (+0 and -0 merged, -inf an ordinary
-      // candidate); INT_MIN marks "not a candidate" (slots >= N, slots
-      // already taken), so fewer than k finite logits still give k distinct
-      // slots, as the stable argsort of the reference idiom does
-      auto to_key = [](float x) {
-        const int32_t b = __float_as_int(x + 0.0f);
-        return b >= 0 ? b : b ^ 0x7fffffff;
-      };
-      auto key_to_f = [](int32_t k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); };
       int sel_e[kGtMaxK];
       int32_t sel_k[kGtMaxK];
       float ex = 0.f;
@@ -326,6 +335,116 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
         if (threadIdx.x == 128) GATE_TS(8);                // logits in registers
+        if constexpr (S::kWarpRows) {
+          const int32_t rows_t = min(S::kRows, s_cnt[gl] - blk * S::kRows);
+          if (rows_t <= 32) {
+            // ===== warp per row (tile-uniform branch); arithmetic as below
+            {
+              const int r = ew * 32 + lane;
+              if (r < rows_t) {
+                float* dst = wr + r * S::kWrLd + c0;
+#pragma unroll
+                for (int e = 0; e < NH; ++e) dst[e] = __uint_as_float(v[e]) + s_bias[c0 + e];
+              }
+            }
+            asm volatile("bar.sync 6, %0;" :: "n"(128 * S::kSplit) : "memory");
+            const int we = warp - 4;
+            float* sc = wr + 32 * S::kWrLd + we * 64;
+            const bool v0 = lane < N, v1 = lane + 32 < N;
+            for (int r = we; r < rows_t; r += 4 * S::kSplit) {
+              const float* xr = wr + r * S::kWrLd;
+              const float x0 = v0 ? xr[lane] : 0.f;
+              const float x1 = v1 ? xr[lane + 32] : 0.f;
+              int32_t k0 = v0 ? to_key(x0) : INT_MIN;
+              int32_t k1 = v1 ? to_key(x1) : INT_MIN;
+              const int32_t h0 = __reduce_max_sync(0xffffffffu, k0);
+              const int32_t h1 = __reduce_max_sync(0xffffffffu, k1);
+              int sel_e[kGtMaxK];
+              int32_t sel_k[kGtMaxK];
+#pragma unroll
+              for (int s = 0; s < kGtMaxK; ++s) {
+                sel_e[s] = 0;
+                sel_k[s] = INT_MIN;
+                if (s < K) {
+                  // the max key, then the lowest slot holding it (the tree's order)
+                  const int32_t mk = __reduce_max_sync(0xffffffffu, max(k0, k1));
+                  const uint32_t b0 = __ballot_sync(0xffffffffu, k0 == mk);
+                  const uint32_t b1 = __ballot_sync(0xffffffffu, k1 == mk);
+                  const int bs = b0 ? __ffs(b0) - 1 : 31 + __ffs(b1);
+                  sel_e[s] = bs;
+                  sel_k[s] = mk;
+                  if (bs == lane) k0 = INT_MIN;
+                  if (bs == lane + 32) k1 = INT_MIN;
+                }
+              }
+              // softmax denominator: terms in parallel, lane 0 sums them in
+              // the thread paths' column order
+              float ex_r = 0.f;
+              if constexpr (S::kSplit == 1) {
+                const float mx = key_to_f(sel_k[0]);
+                if (v0) sc[lane] = __expf(x0 - mx);
+                if (v1) sc[lane + 32] = __expf(x1 - mx);
+                __syncwarp();
+                if (lane == 0) {
+                  for (int e = 0; e < NP; ++e)
+                    if (e < N) ex_r += sc[e];
+                }
+              } else {
+                const float mh = key_to_f(h0), m1 = key_to_f(h1);
+                if (v0) sc[lane] = __expf(x0 - mh);
+                if (v1) sc[lane + 32] = __expf(x1 - m1);
+                __syncwarp();
+                if (lane == 0) {
+                  float sh = 0.f, s1 = 0.f;
+                  if (mh > -INFINITY) {
+                    for (int e = 0; e < 32; ++e)
+                      if (e < N) sh += sc[e];
+                  }
+                  if (m1 > -INFINITY) {
+                    for (int e = 0; e < 32; ++e)
+                      if (32 + e < N) s1 += sc[32 + e];
+                  }
+                  const float mx = key_to_f(sel_k[0]);
+                  ex_r = mx > -INFINITY ? sh * __expf(mh - mx) + s1 * __expf(m1 - mx)
+                                        : __int_as_float(0x7fc00000);
+                }
+              }
+              // weights / stores / locality, lane s = selection s (the tail's expressions)
+              const float inv = __shfl_sync(0xffffffffu, 1.0f / ex_r, 0);
+              const float mx = key_to_f(sel_k[0]);
+              int my_e = 0;
+              int32_t my_k = INT_MIN;
+#pragma unroll
+              for (int s = 0; s < kGtMaxK; ++s)
+                if (lane == s) { my_e = sel_e[s]; my_k = sel_k[s]; }
+              const float p_s = lane < K ? __expf(key_to_f(my_k) - mx) * inv : 0.f;
+              float psum = 0.f;
+#pragma unroll
+              for (int s = 0; s < kGtMaxK; ++s) psum += __shfl_sync(0xffffffffu, p_s, s);
+              const float scale = a.renorm ? 1.0f / psum : 1.0f;
+              const int64_t jr = (int64_t)blk * S::kRows + r;
+              const int32_t g = a.shard_begin + gl;
+              const int32_t o = lane < K ? s_owner[my_e] : -1 - lane;
+              if (lane < K) {
+                reinterpret_cast<int32_t*>(s_ids[gl])[jr * K + lane] = my_e;
+                reinterpret_cast<float*>(s_wts[gl])[jr * K + lane] = p_s * scale;
+              }
+              const uint32_t same = __match_any_sync(0xffffffffu, o);
+              const uint32_t kmask = (1u << K) - 1u;
+              const uint32_t loc = __ballot_sync(0xffffffffu, lane < K && o == g);
+              const uint32_t first = __ballot_sync(0xffffffffu, (same & lanemask_lt()) == 0u);
+              if (lane == 0) {
+                const int nl = __popc(loc);
+                my_local += nl;
+                my_remote += K - nl;
+                my_rrows += __popc(first & kmask & ~loc);
+              }
+              __syncwarp();
+            }
+            asm volatile("bar.sync 6, %0;" :: "n"(128 * S::kSplit) : "memory");
+            continue;
+          }
+        }
         if (S::kSplit == 1 && j >= s_cnt[gl]) continue;
         constexpr int NT = NH <= 16 ? 16 : (NH <= 32 ? 32 : 64);   // tree leaves (power of 2)
         int32_t key[NT];
