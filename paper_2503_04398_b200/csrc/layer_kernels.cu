@@ -1020,8 +1020,12 @@ combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtr
                    ShardPtrs outs, HistUpdate hu, int32_t whole_rows, int64_t block_rows,
                    int32_t* err) {
   SMOE_TL_ENTER(7);
-  pdl_enter();
-  SMOE_TL_WAITED(7);
+  // Everything this kernel reads except the pair rows (ypair, written by
+  // the down GEMM it follows) was written by kernels that completed before
+  // the dispatch passed its wait -- the plan (counts, group, forward), the
+  // gate (weights, ids) and the caller (input history): the first work
+  // item's metadata is loaded before the wait, under the down GEMM's tail.
+  pdl_trigger();
   __shared__ RowMap rm;
   __shared__ char* s_y[SMOE_MAX_SHARDS];
   __shared__ char* s_wts[SMOE_MAX_SHARDS];
@@ -1042,13 +1046,38 @@ combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtr
   const bool whole = rm.total >= whole_rows;
   const int64_t chunks = whole ? 1 : (vecs + kChunkVecs - 1) / kChunkVecs;
   const int64_t cv = whole ? vecs : kChunkVecs;
+  // the first item's token position, weights and history digit
+  int64_t pre_i = 0, pre_v = 0;
+  float pre_w[kGateMaxK];
+  if (w0 < (int64_t)rm.total * chunks) {
+    const int64_t q = whole ? w0 : w0 / chunks, c = w0 - q * chunks;
+    int32_t gl; int64_t j;
+    decode_row(rm, lr.shard_count, q, gl, j);
+    const int64_t g = lr.shard_begin + gl;
+    pre_i = lr.forward[g * rm.group + j];
+    const float* w = reinterpret_cast<const float*>(s_wts[gl]) + j * k;
+#pragma unroll
+    for (int s = 0; s < kGateMaxK; ++s) pre_w[s] = s < k ? w[s] : 0.f;
+    if (c == 0 && hu.n_hist_outs > 0 && lane < hu.hist_len) {
+      const int64_t L = hu.hist_len;
+      if (lane == L - 1) {
+        const int32_t top1 = reinterpret_cast<const int32_t*>(s_ids[gl])[j * k];
+        pre_v = hu.slot_owner[top1];
+      } else {
+        pre_v = hu.hist_in ? hu.hist_in[pre_i * L + lane + 1] : 0;
+      }
+    }
+  }
+  pdl_wait();
+  SMOE_TL_WAITED(7);
   for (int64_t it = w0; it < (int64_t)rm.total * chunks; it += nwarps) {
+    const bool first_item = it == w0;
     const int64_t q = whole ? it : it / chunks;
     const int64_t c = it - q * chunks;
     int32_t gl; int64_t j;
     decode_row(rm, lr.shard_count, q, gl, j);
     const int64_t g = lr.shard_begin + gl;
-    const int64_t i = lr.forward[g * rm.group + j];    // original token position
+    const int64_t i = first_item ? pre_i : lr.forward[g * rm.group + j];   // original position
     // block_rows > 0 (DS-MoE pipeline): the row goes to its all-gather slot
     // g * group + j instead (the resume is a separate gather, not fused)
     const int64_t i_dst = block_rows > 0 ? g * rm.group + j : i;
@@ -1061,7 +1090,9 @@ combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtr
       // top-1 expert (the device of this routing event, predictor.py:165-166)
       const int64_t L = hu.hist_len;
       int64_t v;
-      if (lane == L - 1) {
+      if (first_item) {
+        v = pre_v;
+      } else if (lane == L - 1) {
         const int32_t top1 = reinterpret_cast<const int32_t*>(s_ids[gl])[j * k];
         v = hu.slot_owner[top1];
       } else {
@@ -1075,7 +1106,7 @@ combine_sag_kernel(LocalRows lr, int32_t k, int64_t d, ShardPtrs ypair, ShardPtr
     const float* w = reinterpret_cast<const float*>(s_wts[gl]) + j * k;
     float wk[kGateMaxK];
 #pragma unroll
-    for (int s = 0; s < kGateMaxK; ++s) wk[s] = s < k ? w[s] : 0.f;
+    for (int s = 0; s < kGateMaxK; ++s) wk[s] = first_item ? pre_w[s] : (s < k ? w[s] : 0.f);
     combine_span<G>(dst_base, s_y[gl] + j * k * d * 2, wk, k, d, i_dst, c * cv,
                     min(vecs, (c + 1) * cv), lane);
   }
