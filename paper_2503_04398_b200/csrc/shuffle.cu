@@ -27,9 +27,11 @@ int num_sms() {
 
 static int g_pdl = -1;
 // Layer stages whose kernels may launch early (SMOE_PDL_STAGES bit mask over
-// SMOE_STAGE_*).  Not the up GEMM: its persistent CTAs take tiles by blockIdx
-// and the launch order's CTA placement is worth 5-10% there; an early launch
-// lands the CTAs wherever the dispatch kernel leaves room (profiles/r1_pdl/).
+// SMOE_STAGE_*).  Not the up GEMM at large batches: its persistent CTAs take
+// tiles by blockIdx and the launch order's CTA placement is worth 5-10% there;
+// an early launch lands the CTAs wherever the dispatch kernel leaves room
+// (profiles/r1_pdl/).  At decode sizes (no two tiles share a weight tile) the
+// layer launches it early anyway (SMOE_OPT_DECODE_UP_PDL, layer.cu).
 static int g_pdl_stage_mask = ~(1 << SMOE_STAGE_EXPERT_UP);
 static thread_local int g_pdl_stage = -1;
 int pdl_enabled() {
