@@ -40,18 +40,26 @@ struct LookupTables {
 // int16 table value sign-extended as numpy's astype(int64) does).
 __device__ __forceinline__ int64_t lookup_one(const LookupTables& t, int64_t i,
                                               int64_t tok, int32_t* err) {
+  // Two rounds of loads instead of four: the history row does not depend on
+  // the token, and the four table entries are read together (a row's entries
+  // only when the row is in range); the checks and their order -- token range
+  // first, then history range -- are the reference's.
+  int64_t row = 0;
+  if (t.hist != nullptr) {
+    const int64_t* h = t.hist + i * (int64_t)t.hist_len;
+    for (int j = 0; j < t.hist_len; ++j) row = row * t.n_clusters + __ldg(h + j);
+    if (row < 0) row += t.a_rows;
+  }
   if (tok < 0) tok += t.vocab;                       // numpy negative wrap
   if (tok < 0 || tok >= t.vocab) { set_err(err, SMOE_ERRBIT_TOKEN_RANGE); return 0; }
+  const bool row_ok = t.hist != nullptr && row >= 0 && row < t.a_rows;
   const int64_t stat = (int64_t)__ldg(t.t_labels + tok);
+  const float thr = t.hist != nullptr ? __ldg(t.t_conf + tok) : 0.f;
+  const float conf = row_ok ? __ldg(t.a_conf + row) : 0.f;
+  const int64_t best = row_ok ? (int64_t)__ldg(t.a_best + row) : 0;
   if (t.hist == nullptr) return stat;                // scheduler.py:88-89
-  int64_t row = 0;
-  const int64_t* h = t.hist + i * (int64_t)t.hist_len;
-  for (int j = 0; j < t.hist_len; ++j) row = row * t.n_clusters + __ldg(h + j);
-  if (row < 0) row += t.a_rows;
-  if (row < 0 || row >= t.a_rows) { set_err(err, SMOE_ERRBIT_HISTORY_RANGE); return stat; }
-  const float conf = __ldg(t.a_conf + row);
-  const float thr = __ldg(t.t_conf + tok);
-  return (conf > thr) ? (int64_t)__ldg(t.a_best + row) : stat;   // strict >, :95
+  if (!row_ok) { set_err(err, SMOE_ERRBIT_HISTORY_RANGE); return stat; }
+  return (conf > thr) ? best : stat;                 // strict >, :95
 }
 
 __global__ void __launch_bounds__(kPlanThreads)
