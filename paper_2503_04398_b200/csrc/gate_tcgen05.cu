@@ -175,13 +175,13 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
                  :: "r"(smem_addr(&tmem_holder)), "r"(S::kTmemCols) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  // everything above reads constant data only (weights, tensor maps); the
-  // shard row counts come from the plan stage.  The dependents' early launch
+  // Everything above reads constant data only (weights, tensor maps).  The
+  // shard row counts (plan) are read before the wait too: the SRS kernel this
+  // gate follows triggers only after its own wait, i.e. after the plan
+  // completed (profiles/r2/decode/prewait2/).  The dependents' early launch
   // is triggered at the END of this kernel: the dispatch kernel's CTAs,
   // resident and waiting from the start, slowed this gate (64-token forward
   // DSV2-Lite / Qwen2 -6.5 / -5.5 us, profiles/r2/decode/pdl_trigger/)
-  pdl_wait();
-  SMOE_TL_WAITED(2);
   if (threadIdx.x < 32) {
     // one lane per shard: the count loads are in flight together
     const int i = threadIdx.x;
@@ -208,6 +208,8 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmap_h,
       }
     }
   }
+  pdl_wait();
+  SMOE_TL_WAITED(2);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();

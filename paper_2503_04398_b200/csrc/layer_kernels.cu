@@ -140,7 +140,10 @@ template <int G>
 __global__ void __launch_bounds__(256)
 srs_kernel(LocalRows lr, ShardPtrs partials, int64_t d, ShardPtrs hs, int32_t whole_rows) {
   SMOE_TL_ENTER(1);
-  pdl_enter();
+  // wait, THEN trigger: the gate launched behind this kernel may then read
+  // the plan's outputs before its own wait (the plan has completed)
+  pdl_wait();
+  pdl_trigger();
   SMOE_TL_WAITED(1);
   __shared__ RowMap rm;
   __shared__ char* s_hs[SMOE_MAX_SHARDS];

@@ -230,6 +230,7 @@ plan_single_kernel(LookupTables t, int use_lookup, const int64_t* __restrict__ t
   if (threadIdx.x == 0) *group_out = group;
 #pragma unroll
   for (int c = 0; c < kPlanChunks; ++c) {
+    if (c * kPlanThreads >= n) break;                // CTA-uniform: no rows in this chunk
     const int64_t i = c * kPlanThreads + threadIdx.x;
     const int32_t d = dv[c];
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
