@@ -49,6 +49,10 @@ struct GemmArgs {
   int32_t ready_up_tile_m;
   int32_t ready_up_n_tiles;
   int32_t* err;
+  // non-null (the decode down GEMM, whose CTAs start staggered as the up
+  // GEMM's tiles finish): tiles are taken from this zeroed counter instead of
+  // blockIdx-strided, so early-starting CTAs take more of them (cg == 1)
+  int32_t* tile_counter;
 };
 
 // Encodes a 2D bf16 K-major tensor map (rows x cols, box 64 x box_rows, 128B swizzle).

@@ -141,7 +141,12 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
   uint64_t* bars = reinterpret_cast<uint64_t*>(staging + S::kStaging);
   // bars: full[kStages], empty[kStages], tfull[2], tempty[2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
-  typename S::Problems& sp = *reinterpret_cast<typename S::Problems*>(bars + 2 * kStages + 8);
+  // dynamic tiles: tile-index ring of 4 (full / empty mbarriers + the index)
+  const uint32_t tile_full0 = smem_addr(bars + 2 * kStages + 8);
+  const uint32_t tile_empty0 = smem_addr(bars + 2 * kStages + 12);
+  volatile int32_t* s_tile = reinterpret_cast<volatile int32_t*>(bars + 2 * kStages + 16);
+  typename S::Problems& sp = *reinterpret_cast<typename S::Problems*>(bars + 2 * kStages + 20);
+  const bool dyn = CG == 1 && args.tile_counter != nullptr;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t np = args.num_problems;
@@ -163,6 +168,10 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_addr(&bars[2 * kStages + a]), 1);
       mbar_init(smem_addr(&bars[2 * kStages + 2 + a]), 4 * CG);   // one arrival per epilogue warp
+    }
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(tile_full0 + 8 * s, 1);            // the producer publishes a tile index
+      mbar_init(tile_empty0 + 8 * s, 1 + 4);       // the MMA issuer + the 4 epilogue warps read it
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -224,7 +233,20 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       int32_t stage = 0;
       uint32_t phase = 0;
       int32_t cursor = 0;
-      for (int32_t t = unit; t < total_tiles; t += n_units) {
+      // dynamic tiles: the next index is fetched once this tile's loads are
+      // all issued (the ring's depth hides the atomic's round trip, and a CTA
+      // never holds more than the tile it is about to load)
+      int32_t next_t = dyn ? atomicAdd(args.tile_counter, 1) : 0;
+      for (int32_t it = 0;; ++it) {
+        int32_t t = unit + it * n_units;
+        if (dyn) {
+          const int slot = it & 3;
+          t = next_t;
+          if (it >= 4) mbar_wait(tile_empty0 + 8 * slot, ((it >> 2) - 1) & 1);
+          s_tile[slot] = t;
+          mbar_arrive(tile_full0 + 8 * slot);
+        }
+        if (t >= total_tiles) break;
         const TileCoord tc = decode_tile<kTileM>(sp, np, args.n_tiles_n, args.group_m, t, cursor);
         const int32_t a_row =
             (int32_t)(sp.a_off[tc.p] + (int64_t)tc.m_blk * kTileM + rank * kGemmBM);
@@ -272,6 +294,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
+        if (dyn) next_t = atomicAdd(args.tile_counter, 1);
       }
     }
   } else if (warp == 1) {
@@ -280,7 +303,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       int32_t stage = 0;
       uint32_t phase = 0;
       uint32_t acc = 0, acc_phase = 0;
-      for (int32_t t = unit; t < total_tiles; t += n_units) {
+      for (int32_t it = 0;; ++it) {
+        int32_t t = unit + it * n_units;
+        if (dyn) {
+          const int slot = it & 3;
+          mbar_wait(tile_full0 + 8 * slot, (it >> 2) & 1);
+          t = s_tile[slot];
+          mbar_arrive(tile_empty0 + 8 * slot);
+        }
+        if (t >= total_tiles) break;
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kGemmBN;
@@ -310,7 +341,16 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     uint8_t* stg = staging + ew * (32 * 64);
     uint32_t acc = 0, acc_phase = 0;
     int32_t cursor = 0;
-    for (int32_t t = unit; t < total_tiles; t += n_units) {
+    for (int32_t it = 0;; ++it) {
+      int32_t t = unit + it * n_units;
+      if (dyn) {
+        const int slot = it & 3;
+        mbar_wait(tile_full0 + 8 * slot, (it >> 2) & 1);
+        t = s_tile[slot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tile_empty0 + 8 * slot);
+      }
+      if (t >= total_tiles) break;
       const TileCoord tc = decode_tile<kTileM>(sp, np, args.n_tiles_n, args.group_m, t, cursor);
       const int32_t m = sp.m[tc.p];
       const int32_t row0 = tc.m_blk * kTileM + rank * kGemmBM + ew * 32;   // first row of warp

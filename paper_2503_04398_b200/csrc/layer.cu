@@ -31,7 +31,8 @@ struct smoe_layer {
   std::vector<int32_t> slot_owner_h, slot_first_h;
   int32_t* slot_owner_d = nullptr;   // [N]
   int32_t* slot_first_d = nullptr;   // [G + 1]
-  int32_t* ready_d = nullptr;        // [kMaxExperts] up-tile counts (early down GEMM)
+  int32_t* ready_d = nullptr;        // [kMaxExperts + 1] up-tile counts (early down GEMM)
+                                     // + the down GEMM's dynamic tile counter
   bool ready_armed = false;          // the last EXPERT_UP launch publishes them
   bool ready_zeroed = false;         // this forward's PLAN reset them
   bool route_fused = false;          // the last GATE launch also ran the route
@@ -86,7 +87,7 @@ extern "C" int smoe_layer_create(const smoe_layer_config* cfg, smoe_layer** out)
   std::memset(L->buf, 0, sizeof(L->buf));
   if (cudaMalloc(&L->slot_owner_d, sizeof(int32_t) * cfg->n_experts) != cudaSuccess ||
       cudaMalloc(&L->slot_first_d, sizeof(int32_t) * (cfg->n_shards + 1)) != cudaSuccess ||
-      cudaMalloc(&L->ready_d, sizeof(int32_t) * kMaxExperts) != cudaSuccess) {
+      cudaMalloc(&L->ready_d, sizeof(int32_t) * (kMaxExperts + 1)) != cudaSuccess) {
     delete L;
     return SMOE_ERR_CUDA;
   }
@@ -415,7 +416,7 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
                         static_cast<int32_t*>(L->buf[SMOE_BUF_PLAN_COUNTS][0]),
                         static_cast<int64_t*>(L->buf[SMOE_BUF_GROUP][0]), err,
                         L->buf[SMOE_BUF_WORKSPACE][0], plan_ws_aligned(&c), stats,
-                        SMOE_STAT__COUNT, st, L->ready_d, L->local_slots);
+                        SMOE_STAT__COUNT, st, L->ready_d, L->local_slots + 1);
       L->ready_zeroed = rc == SMOE_OK;
       return rc;
     }
@@ -525,7 +526,8 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
       const bool up_pdl = L->ready_armed && L->ready_zeroed && g_decode_up_pdl;
       if (L->ready_armed) {
         if (!L->ready_zeroed)              // stage calls without this forward's PLAN
-          SMOE_CUDA_TRY(cudaMemsetAsync(L->ready_d, 0, sizeof(int32_t) * L->local_slots, st));
+          SMOE_CUDA_TRY(
+              cudaMemsetAsync(L->ready_d, 0, sizeof(int32_t) * (L->local_slots + 1), st));
         a.ready = L->ready_d;
         a.ready_role = 1;
       }
@@ -567,6 +569,12 @@ static int layer_stage(smoe_layer* L, int32_t stage, const int64_t* tokens,
         a.ready_up_tile_m = kGemmBM;
         a.ready_up_n_tiles = 2 * c.ffn / kGemmBN;
         a.err = err;
+#ifndef SMOE_DYN_DOWN
+#define SMOE_DYN_DOWN 1
+#endif
+        // its CTAs start staggered (on the SMs the up GEMM frees): tiles
+        // from a counter, so the early starters take more of them
+        if (SMOE_DYN_DOWN) a.tile_counter = L->ready_d + L->local_slots;
       }
       L->ready_armed = false;
       rc = narrow_gemm(L, n)
